@@ -1,0 +1,357 @@
+#!/usr/bin/env python3
+"""bench.py — throughput of the B200 KKT/Krylov hot path (BASELINE.json metric).
+
+Default (N=1): BASELINE config 2 — the isolated, source-batched KKT operator
+apply on a 512x256 grid (20-cell PML), K=64 sources, 256 receivers, complex128.
+One step = one fused KKT apply over all sources with inputs resident in HBM.
+The JSON line also carries the complex64 apply, the Krylov iteration
+throughput of BASELINE config 1 (exact and ILU(4) preconditioners) and the
+end-to-end number through the C ABI with host buffers.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's own CPU kkt_apply (oracle/_ref, the
+unmodified reference core) on the same config with all host threads.
+Multi-GPU: replicas only (the north star fixes one GPU).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KKT applies/sec and Krylov iters/sec at 1 B200; achieved HBM GB/s vs peak"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons through NVML while running."""
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index=0, period=0.01):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period = period
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def result(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def timed_events(stream_ptr, fn, steps):
+    """CUDA-event time of `steps` calls of fn() on the library's own stream."""
+    import torch
+    s = torch.cuda.ExternalStream(stream_ptr)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for i in range(steps):
+        fn(i)
+    e1.record(s)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3
+
+
+def barrier_max(t, ws):
+    if ws == 1:
+        return t
+    import torch
+    import torch.distributed as dist
+    x = torch.tensor([t], dtype=torch.float64, device="cuda")
+    dist.all_reduce(x, op=dist.ReduceOp.MAX)
+    return float(x.item())
+
+
+def load_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2204_06489_b200 import _abi
+    from paper_2204_06489_b200 import api as fw
+    from paper_2204_06489_b200.problem import c1_problem, c2_problem, random_kkt
+
+    peak, peak_src = peaks()
+    p = c2_problem()
+    st = fw.GnState(p, exact=False, c64=True)
+    n, K = p.n, p.K
+    alg_bytes = 80 * K * n + 24 * n            # complex128 per apply
+    alg_bytes32 = 40 * K * n + 12 * n
+    xs = [fw.KktVector.from_host(st, random_kkt(p, 11 + i)) for i in range(2)]
+    ys = [fw.KktVector(st) for _ in range(2)]
+    L = fw.lib()
+    sp = st.stream_ptr()
+
+    def step(i):
+        fw._check(L.fwi_dev_kkt_apply(st.h, xs[i & 1].h, ys[i & 1].h))
+
+    for i in range(args.warmup):
+        step(i)
+    st.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    with ClockSampler(local) as clk:
+        t = timed_events(sp, step, args.steps)
+    t = barrier_max(t, ws)
+    per = t / args.steps
+    value = ws * args.steps / t
+    achieved = alg_bytes / per / 1e9
+
+    # complex64 apply (reported separately)
+    xs32 = [fw.KktVector.from_host(st, random_kkt(p, 21 + i).astype(np.float32), _abi.FWI_C64)
+            for i in range(2)]
+    ys32 = [fw.KktVector(st, _abi.FWI_C64) for _ in range(2)]
+
+    def step32(i):
+        fw._check(L.fwi_dev_kkt_apply(st.h, xs32[i & 1].h, ys32[i & 1].h))
+
+    for i in range(args.warmup):
+        step32(i)
+    t32 = barrier_max(timed_events(sp, step32, args.steps), ws)
+    per32 = t32 / args.steps
+
+    # end to end through the C ABI: pinned host in -> apply -> host out, every step
+    e2e_steps = max(3, min(args.steps, 20))
+    hin = [np.ascontiguousarray(random_kkt(p, 31 + i)) for i in range(2)]
+    hout = np.empty(st.vec_len)
+    for a in hin + [hout]:
+        fw.host_register(a)
+    xin, yout = fw.KktVector(st), fw.KktVector(st)
+
+    def e2e_step(i):
+        xin.upload(hin[i & 1])
+        fw.kkt_apply(st, xin, yout)
+        yout.to_host(hout)
+
+    e2e_step(0)
+    if ws > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for i in range(e2e_steps):
+        e2e_step(i)
+    te = barrier_max(time.perf_counter() - t0, ws)
+    for a in hin + [hout]:
+        fw.host_unregister(a)
+    vec_bytes = st.vec_len * 8
+
+    # Krylov iterations/s on BASELINE config 1 (exact and ILU(4) preconditioners)
+    krylov = {}
+    if not args.skip_krylov:
+        q = c1_problem()
+        q.d_obs = fw.simulate(q)
+        s1 = fw.GnState(q, exact=True, ilu_level=4)
+        for mode in (fw.PrecondMode.exact, fw.PrecondMode.ilu):
+            fw.fsgn_gmres_step(s1, fw.FsgnOptions(mode=mode, tol=1e-3, maxit=3, ecg_stride=0))
+            t0 = time.perf_counter()
+            ds, log = fw.fsgn_gmres_step(s1, fw.FsgnOptions(mode=mode, restart=30, tol=1e-3, maxit=60,
+                                                            ecg_stride=0))
+            tw = time.perf_counter() - t0
+            it = log.iterations()
+            krylov[mode.name] = {"iterations": it, "converged": log.converged,
+                                 "final_residual": log.final_residual(),
+                                 "iters_per_s": it / log.entries[-1].wall_time,
+                                 "step_wall_s": tw}
+        s1.close()
+
+    cpu = None
+    if rank == 0 and not args.skip_cpu:
+        cpu = cpu_baseline_apply(p, sample_applies=None)
+
+    if rank == 0:
+        tr = load_traffic().get("kkt_apply_c128_c2")
+        line = {
+            "metric": METRIC, "value": value, "unit": "applies/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (seeded; BASELINE config 2 shapes and distributions)",
+            "config": {"workload": "C2: isolated batched KKT apply, 512x256 grid, 20-cell PML, "
+                                   "K=64 sources, R=256 receivers, complex128",
+                       "nx": 512, "nz": 256, "K": K, "R": 256, "n": n,
+                       "l2": "inputs larger than L2 (2 alternating 270 MB input vectors + 134 MB u "
+                             "+ 2 outputs per step pair)",
+                       "parallelism": f"replicas x{ws}"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_source": peak_src,
+                         "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "kernel": "kkt_apply_kernel<F64>"},
+            "c64": {"applies_per_s": ws / per32, "ms_per_apply": per32 * 1e3,
+                    "achieved_gbs": alg_bytes32 / per32 / 1e9,
+                    "frac": alg_bytes32 / per32 / 1e9 / peak},
+            "krylov": krylov,
+            "e2e": {"value": ws * e2e_steps / te, "unit": "applies/s", "h2d_bytes_per_step": vec_bytes,
+                    "d2h_bytes_per_step": vec_bytes,
+                    "path": "fwi_dev_vec_upload -> fwi_dev_kkt_apply -> fwi_dev_vec_download "
+                            "(pinned host buffers)"},
+            "gpu_launches": args.steps,
+            "clocks": clk.result(),
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# reference CPU arm (oracle/_ref: the unmodified reference core, all threads)
+# ---------------------------------------------------------------------------
+def ref_threads(p):
+    n_cpu = os.cpu_count() or 1
+    try:
+        with open("/proc/meminfo") as f:
+            avail_kb = int([l for l in f if l.startswith("MemAvailable")][0].split()[1])
+    except Exception:
+        avail_kb = 16 << 20
+    per_apply = 3 * p.vec_len * 8  # output + temporaries of one serial kkt_apply
+    by_mem = max(1, int(avail_kb * 1024 * 0.5 // per_apply))
+    return max(1, min(n_cpu, by_mem))
+
+
+def cpu_baseline_apply(p, sample_applies=None):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    from paper_2204_06489_b200.problem import random_kkt
+    ref = po.Ref(p, full=False, exact=False)
+    x = random_kkt(p, 11)
+    th = ref_threads(p)
+    na = sample_applies or max(th, 2 * th)
+    sec = ref.bench_kkt_apply(x, th, na)
+    return {"value": na / sec, "unit": "applies/s", "cores": th, "kind": "reference",
+            "sample": f"{na} reference kkt_apply calls (C2, complex128) over {th} host threads, "
+                      f"{sec:.1f} s wall; {os.cpu_count()} host CPUs"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2204_06489_b200.problem import c2_problem, random_kkt
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    p = c2_problem()
+    ref = po.Ref(p, full=False, exact=False)
+    x = random_kkt(p, 11)
+    th = ref_threads(p)
+    per_step = th
+    for _ in range(args.warmup):
+        ref.bench_kkt_apply(x, th, th)
+    tot = 0.0
+    for _ in range(args.steps):
+        tot += ref.bench_kkt_apply(x, th, per_step)
+    value = args.steps * per_step / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "applies/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (seeded; BASELINE config 2 shapes and distributions)",
+        "config": {"workload": "C2: isolated batched KKT apply, 512x256 grid, 20-cell PML, "
+                               "K=64 sources, R=256 receivers, complex128",
+                   "nx": 512, "nz": 256, "K": 64, "R": 256, "n": p.n},
+        "cpu_baseline": {"value": value, "unit": "applies/s", "cores": th, "kind": "reference",
+                         "sample": f"each step = {per_step} serial reference kkt_apply calls over {th} "
+                                   f"host threads ({os.cpu_count()} CPUs)"},
+        "e2e": {"value": value, "unit": "applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-krylov", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        if args.steps > 5:
+            args.steps = 5   # each reference step is a bounded multi-second CPU sample
+        args.warmup = min(args.warmup, 1)
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -162,6 +162,8 @@ int fwi_dev_ctx_info(const fwi_dev_ctx* ctx, fwi_state_info* out);
 int fwi_dev_ctx_set_epsilon(fwi_dev_ctx* ctx, double epsilon);
 int fwi_dev_ctx_set_drop_reg_term(fwi_dev_ctx* ctx, int drop);
 int fwi_dev_ctx_synchronize(fwi_dev_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t), for event timing / interop. */
+int fwi_dev_ctx_stream(const fwi_dev_ctx* ctx, void** stream);
 /* Downloads: u (K*n complex), r and d_pred (num_data complex), and the
  * assembled operator as 5-point coefficient planes (each n complex):
  * A(i,i), A(i,i+1), A(i,i+nx). Couplings into Dirichlet columns are 0. */
@@ -217,6 +219,15 @@ typedef int (*fwi_observer_cb)(void* user, int iteration, const double* x_dev);
 int fwi_dev_gmres_generic(int64_t n, fwi_op_cb apply, fwi_op_cb precond, fwi_observer_cb observer,
                           void* user, const double* b_dev, double* x_dev, int restart, double tol,
                           int maxit, fwi_convergence_log* log);
+
+/* ---- raw device memory helpers (for callback-driven use from FFI hosts) -- */
+int fwi_dev_malloc(void** out, int64_t bytes);
+int fwi_dev_free(void* p);
+int fwi_dev_memcpy_h2d(void* dst_dev, const void* src_host, int64_t bytes);
+int fwi_dev_memcpy_d2h(void* dst_host, const void* src_dev, int64_t bytes);
+/* Page-lock an existing host buffer (so uploads/downloads run at DMA speed). */
+int fwi_host_register(void* host, int64_t bytes);
+int fwi_host_unregister(void* host);
 
 #ifdef __cplusplus
 }

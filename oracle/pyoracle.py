@@ -257,3 +257,147 @@ def ref_gn_step(p: Problem, solver=1, max_inner=30, inner_tol=1e-12, restart=30,
     _ck(lib, lib.ref_gn_step(C.byref(d), solver, max_inner, inner_tol, restart, ilu_level, v_min,
                              v_max, _p(s_out), C.byref(mi), C.byref(mf), C.byref(lb.c)))
     return s_out, mi.value, mf.value, lb.to_log()
+
+
+# ---------------------------------------------------------------------------
+# our plain-C restatement (oracle/fwi_oracle.c)
+# ---------------------------------------------------------------------------
+def orc_lib() -> C.CDLL:
+    global _orc_lib
+    if _orc_lib is None:
+        lib = _load(ORC_SO)
+        vp = C.c_void_p
+        lib.orc_last_error.restype = C.c_char_p
+        lib.orc_last_error_index.restype = C.c_int
+        for name, args in {
+            "orc_state_create": [C.c_void_p, C.POINTER(vp)],
+            "orc_kkt_apply": [vp, _dp, _dp],
+            "orc_kkt_rhs": [vp, _dp],
+            "orc_precond_apply": [vp, C.c_int, _dp, _dp],
+            "orc_solve": [vp, C.c_int, C.c_int, _dp, _dp],
+            "orc_ilu_factor": [vp, C.c_int, C.c_double],
+            "orc_gradient": [vp, _dp],
+            "orc_hessian_apply": [vp, _dp, _dp],
+            "orc_fsgn": [vp, C.c_void_p, _dp, C.c_void_p],
+        }.items():
+            f = getattr(lib, name)
+            f.argtypes = args
+            f.restype = C.c_int
+        for name in ("orc_get_u", "orc_get_residual", "orc_get_dpred"):
+            getattr(lib, name).argtypes = [vp, _dp]
+            getattr(lib, name).restype = None
+        lib.orc_get_csr.argtypes = [vp, _ip, _ip, _dp]
+        lib.orc_get_csr.restype = None
+        lib.orc_state_info.argtypes = [vp, _ip, _ip, _ip, _ip, _dp]
+        lib.orc_state_info.restype = None
+        lib.orc_state_free.argtypes = [vp]
+        lib.orc_state_free.restype = None
+        lib.orc_solve_count.argtypes = [vp, C.c_int]
+        lib.orc_solve_count.restype = C.c_longlong
+        lib.orc_set_epsilon.argtypes = [vp, C.c_double]
+        lib.orc_set_epsilon.restype = None
+        lib.orc_set_drop.argtypes = [vp, C.c_int]
+        lib.orc_set_drop.restype = None
+        _orc_lib = lib
+    return _orc_lib
+
+
+class Orc(Ref):
+    """Same interface as Ref, backed by the plain-C restatement."""
+
+    def __init__(self, p: Problem, *, exact: bool = True, ilu_level: int = -1, ilu_shift: float = 0.0):
+        lib = orc_lib()
+        self.lib, self.p = lib, p
+        d, self._keep = p.desc(exact_factor=exact, ilu_level=ilu_level, ilu_diag_shift=ilu_shift)
+        h = C.c_void_p()
+        _ck(lib, lib.orc_state_create(C.byref(d), C.byref(h)), prefix="orc")
+        self.h = h
+        n, K, nd, nnz = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        om = C.c_double()
+        lib.orc_state_info(h, C.byref(n), C.byref(K), C.byref(nd), C.byref(nnz), C.byref(om))
+        self.n, self.K, self.num_data, self.nnz, self.omega = n.value, K.value, nd.value, nnz.value, om.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.orc_state_free(self.h)
+            self.h = None
+
+    def _c(self, code):
+        _ck(self.lib, code, prefix="orc")
+
+    def u(self):
+        out = np.empty(self.K * self.n, np.complex128)
+        self.lib.orc_get_u(self.h, _p(out))
+        return out
+
+    def residual(self):
+        out = np.empty(max(self.num_data, 1), np.complex128)
+        self.lib.orc_get_residual(self.h, _p(out))
+        return out[: self.num_data]
+
+    def dpred(self):
+        out = np.empty(max(self.num_data, 1), np.complex128)
+        self.lib.orc_get_dpred(self.h, _p(out))
+        return out[: self.num_data]
+
+    def csr(self):
+        rp = np.empty(self.n + 1, np.int32)
+        ci = np.empty(self.nnz, np.int32)
+        va = np.empty(self.nnz, np.complex128)
+        self.lib.orc_get_csr(self.h, rp.ctypes.data_as(_ip), ci.ctypes.data_as(_ip), _p(va))
+        return rp, ci, va
+
+    def set_epsilon(self, e):
+        self.lib.orc_set_epsilon(self.h, e)
+
+    def set_drop(self, d):
+        self.lib.orc_set_drop(self.h, int(d))
+
+    def kkt_apply(self, x):
+        x = np.ascontiguousarray(x, np.float64)
+        out = np.empty(self.vec_len)
+        self._c(self.lib.orc_kkt_apply(self.h, _p(x), _p(out)))
+        return out
+
+    def kkt_rhs(self):
+        out = np.empty(self.vec_len)
+        self._c(self.lib.orc_kkt_rhs(self.h, _p(out)))
+        return out
+
+    def precond_apply(self, x, mode):
+        x = np.ascontiguousarray(x, np.float64)
+        out = np.empty(self.vec_len)
+        self._c(self.lib.orc_precond_apply(self.h, mode, _p(x), _p(out)))
+        return out
+
+    def solve(self, b, mode, adjoint):
+        b = np.ascontiguousarray(b, np.complex128)
+        out = np.empty(self.n, np.complex128)
+        self._c(self.lib.orc_solve(self.h, mode, int(adjoint), _p(b), _p(out)))
+        return out
+
+    def solve_count(self, mode):
+        return self.lib.orc_solve_count(self.h, mode)
+
+    def gradient(self):
+        out = np.empty(self.n)
+        self._c(self.lib.orc_gradient(self.h, _p(out)))
+        return out
+
+    def hessian_apply(self, v):
+        v = np.ascontiguousarray(v, np.float64)
+        out = np.empty(self.n)
+        self._c(self.lib.orc_hessian_apply(self.h, _p(v), _p(out)))
+        return out
+
+    def ilu_factor_status(self, level, shift):
+        code = self.lib.orc_ilu_factor(self.h, level, shift)
+        return (code, self.lib.orc_last_error_index()) if code else (0, -1)
+
+    def fsgn(self, mode=_abi.FWI_PRECOND_EXACT, restart=30, tol=1e-10, maxit=30, ecg_stride=0,
+             ecg_stop_tol=0.0):
+        o = _abi.FsgnOptions(mode, restart, tol, maxit, ecg_stride, ecg_stop_tol)
+        ds = np.empty(self.n)
+        lb = _abi.LogBuffer(maxit + 2)
+        self._c(self.lib.orc_fsgn(self.h, C.byref(o), _p(ds), C.byref(lb.c)))
+        return ds, lb.to_log()

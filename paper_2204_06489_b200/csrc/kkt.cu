@@ -1,0 +1,212 @@
+// kkt.cu — K1: the fused, source-batched KKT operator apply and the KKT
+// right-hand side.
+//
+// Reference: kkt_apply (src/kkt.cpp:78-96) with apply_f (:50-58),
+// apply_p (:60-66), accumulate_re_p_adjoint (:68-74) and spmv
+// (src/sparse.cpp:69-91); kkt_rhs (src/kkt.cpp:98-112).
+//
+//   out.du_k = F_k du_k + A^H lambda_k
+//   out.la_k = A du_k - w^2 u_k * ds
+//   out.ds   = eps ds - sum_k Re(w^2 conj(u_k) lambda_k)      (k = 0..K-1 in order)
+//
+// One pass: each thread owns one grid node, loads its five stencil
+// coefficients once, then walks the K sources in order, reading du_k, la_k and
+// u_k at the node (and du_k, la_k at the 4 neighbours, served from L1 by the
+// neighbouring threads of the CTA tile), writing out.du_k and out.la_k, and
+// carrying the ds row's K-sum in a register. A(i,i-1) and A(i,i-nx) come from
+// the east/south planes of the neighbours (exact complex symmetry),
+// and A^H lambda is a gather with conjugated coefficients in ascending row
+// order — the same summation order as the reference's column scatter, so the
+// complex128 result is bit-identical to the reference.
+#include "ctx.cuh"
+
+namespace fwi_b200 {
+
+namespace {
+
+// complex128: reference-faithful rounding (no FMA), see common.cuh
+struct F64 {
+    using T = double2;
+    using R = double;
+    static __device__ __forceinline__ T zero() { return make_double2(0.0, 0.0); }
+    static __device__ __forceinline__ T add(T a, T b) { return cadd(a, b); }
+    static __device__ __forceinline__ T sub(T a, T b) { return csub(a, b); }
+    static __device__ __forceinline__ T mul(T a, T b) { return cmul(a, b); }
+    static __device__ __forceinline__ T mulc(T a, T b) { return cmulc(a, b); }
+    static __device__ __forceinline__ T rm(R r, T a) { return rmul(r, a); }
+    static __device__ __forceinline__ R radd(R a, R b) { return __dadd_rn(a, b); }
+    static __device__ __forceinline__ R rmulr(R a, R b) { return __dmul_rn(a, b); }
+    static __device__ __forceinline__ R rsub(R a, R b) { return __dsub_rn(a, b); }
+    // Re(w2 * conj(u) * z) exactly as std::real(w2 * std::conj(u) * z)
+    static __device__ __forceinline__ R re_pconj(R w2, T u, T z) {
+        const R a = __dmul_rn(u.x, w2), b = __dmul_rn(-u.y, w2);
+        return __dsub_rn(__dmul_rn(a, z.x), __dmul_rn(b, z.y));
+    }
+    // (w2 * u) * v
+    static __device__ __forceinline__ T pmul(R w2, T u, R v) {
+        return make_double2(__dmul_rn(__dmul_rn(w2, u.x), v), __dmul_rn(__dmul_rn(w2, u.y), v));
+    }
+};
+
+// complex64: plain fast arithmetic (reported separately with its deviation)
+struct F32 {
+    using T = float2;
+    using R = float;
+    static __device__ __forceinline__ T zero() { return make_float2(0.f, 0.f); }
+    static __device__ __forceinline__ T add(T a, T b) { return make_float2(a.x + b.x, a.y + b.y); }
+    static __device__ __forceinline__ T sub(T a, T b) { return make_float2(a.x - b.x, a.y - b.y); }
+    static __device__ __forceinline__ T mul(T a, T b) {
+        return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+    }
+    static __device__ __forceinline__ T mulc(T a, T b) {
+        return make_float2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+    }
+    static __device__ __forceinline__ T rm(R r, T a) { return make_float2(r * a.x, r * a.y); }
+    static __device__ __forceinline__ R radd(R a, R b) { return a + b; }
+    static __device__ __forceinline__ R rmulr(R a, R b) { return a * b; }
+    static __device__ __forceinline__ R rsub(R a, R b) { return a - b; }
+    static __device__ __forceinline__ R re_pconj(R w2, T u, T z) { return w2 * (u.x * z.x + u.y * z.y); }
+    static __device__ __forceinline__ T pmul(R w2, T u, R v) { return make_float2(w2 * u.x * v, w2 * u.y * v); }
+};
+
+template <class A>
+__global__ void __launch_bounds__(256) kkt_apply_kernel(
+    int nx, int nz, int K, int64_t n, typename A::R w2, typename A::R eps,
+    const typename A::T* __restrict__ diag, const typename A::T* __restrict__ east,
+    const typename A::T* __restrict__ south, const typename A::T* __restrict__ u,
+    const int* __restrict__ nrec_ptr, const int* __restrict__ nrec_k,
+    const double* __restrict__ nrec_w2, const typename A::T* __restrict__ du,
+    const typename A::R* __restrict__ ds, const typename A::T* __restrict__ la,
+    typename A::T* __restrict__ odu, typename A::R* __restrict__ ods, typename A::T* __restrict__ ola) {
+    using T = typename A::T;
+    using R = typename A::R;
+    const int ix = blockIdx.x * blockDim.x + threadIdx.x;
+    const int iz = blockIdx.y * blockDim.y + threadIdx.y;
+    if (ix >= nx || iz >= nz) return;
+    const int64_t c = int64_t(iz) * nx + ix;
+    const bool bnd = on_boundary(ix, iz, nx, nz);
+    const bool hN = !bnd && !on_boundary(ix, iz - 1, nx, nz);
+    const bool hW = !bnd && !on_boundary(ix - 1, iz, nx, nz);
+    const bool hE = !bnd && !on_boundary(ix + 1, iz, nx, nz);
+    const bool hS = !bnd && !on_boundary(ix, iz + 1, nx, nz);
+    const T cD = diag[c];
+    const T cN = hN ? south[c - nx] : A::zero();
+    const T cW = hW ? east[c - 1] : A::zero();
+    const T cE = hE ? east[c] : A::zero();
+    const T cS = hS ? south[c] : A::zero();
+    const R dsv = ds[c];
+    int q = nrec_ptr[c];
+    const int qe = nrec_ptr[c + 1];
+    R pl = R(0);
+    for (int k = 0; k < K; ++k) {
+        const int64_t o = int64_t(k) * n + c;
+        // row 3: A du - P ds (ascending column order: -nx, -1, 0, +1, +nx)
+        T s = A::zero();
+        T t = A::zero();
+        if (hN) {
+            s = A::add(s, A::mul(cN, du[o - nx]));
+            t = A::add(t, A::mulc(cN, la[o - nx]));
+        }
+        if (hW) {
+            s = A::add(s, A::mul(cW, du[o - 1]));
+            t = A::add(t, A::mulc(cW, la[o - 1]));
+        }
+        const T duc = du[o];
+        const T lac = la[o];
+        s = A::add(s, A::mul(cD, duc));
+        t = A::add(t, A::mulc(cD, lac));
+        if (hE) {
+            s = A::add(s, A::mul(cE, du[o + 1]));
+            t = A::add(t, A::mulc(cE, la[o + 1]));
+        }
+        if (hS) {
+            s = A::add(s, A::mul(cS, du[o + nx]));
+            t = A::add(t, A::mulc(cS, la[o + nx]));
+        }
+        const T uc = u[o];
+        ola[o] = A::sub(s, A::pmul(w2, uc, dsv));
+        // row 1: F du + A^H lambda; F accumulates duplicate receivers in data order
+        if (q < qe && nrec_k[q] == k) {
+            T f = A::zero();
+            while (q < qe && nrec_k[q] == k) {
+                f = A::add(f, A::rm(R(nrec_w2[q]), duc));
+                ++q;
+            }
+            t = A::add(f, t);
+        }
+        odu[o] = t;
+        // row 2 partial sum, sources in order
+        pl = A::radd(pl, A::re_pconj(w2, uc, lac));
+    }
+    ods[c] = A::rsub(A::rmulr(eps, dsv), pl);
+}
+
+// kkt_rhs (src/kkt.cpp:98-112): b = (Q^H W^T W r scattered per source,
+// -eps s or 0, 0). One thread per source keeps the reference's data order
+// for duplicate receivers.
+__global__ void kkt_rhs_scatter(int K, int64_t n, const int* __restrict__ off,
+                                const int* __restrict__ node, const double* __restrict__ w,
+                                const double2* __restrict__ r, double2* __restrict__ du) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    for (int j = off[k]; j < off[k + 1]; ++j) {
+        const double ww = __dmul_rn(w[j], w[j]);
+        double2& d = du[int64_t(k) * n + node[j]];
+        d = cadd(d, rmul(ww, r[j]));
+    }
+}
+
+__global__ void kkt_rhs_ds(int64_t n, double neg_eps, const double* __restrict__ s,
+                           double* __restrict__ ds) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        ds[i] = __dmul_rn(neg_eps, s[i]);
+}
+
+}  // namespace
+
+void kkt_apply_raw(Ctx& c, const double* xi, double* out) {
+    dim3 blk(32, 8), grd((c.nx + 31) / 32, (c.nz + 7) / 8);
+    double* x = const_cast<double*>(xi);
+    kkt_apply_kernel<F64><<<grd, blk, 0, c.stream>>>(
+        c.nx, c.nz, c.K, c.n, c.w2, c.eps, c.diag.p, c.east.p, c.south.p, c.u.p, c.nrec_ptr.p,
+        c.nrec_k.p, c.nrec_w2.p, c.du_of(x), c.ds_of(x), c.la_of(x), c.du_of(out), c.ds_of(out),
+        c.la_of(out));
+    CK_LAUNCH();
+}
+
+void kkt_apply(Ctx& c, const Vec& xi, Vec& out) {
+    require(xi.ctx == &c && out.ctx == &c, "KktVector does not conform to the state");
+    require(xi.prec == out.prec, "kkt_apply: precision mismatch");
+    require(&xi != &out, "kkt_apply: output must not alias the input");
+    if (xi.prec == FWI_C128) {
+        kkt_apply_raw(c, xi.d.p, out.d.p);
+        return;
+    }
+    require(c.u32.p != nullptr, "kkt_apply: context was created without the complex64 copy");
+    dim3 blk(32, 8), grd((c.nx + 31) / 32, (c.nz + 7) / 8);
+    const int64_t kn2 = 2 * int64_t(c.K) * c.n;
+    float* x = const_cast<float*>(xi.f.p);
+    float* o = out.f.p;
+    kkt_apply_kernel<F32><<<grd, blk, 0, c.stream>>>(
+        c.nx, c.nz, c.K, c.n, float(c.w2), float(c.eps), c.diag32.p, c.east32.p, c.south32.p,
+        c.u32.p, c.nrec_ptr.p, c.nrec_k.p, c.nrec_w2.p, reinterpret_cast<float2*>(x), x + kn2,
+        reinterpret_cast<float2*>(x + kn2 + c.ds_stride), reinterpret_cast<float2*>(o), o + kn2,
+        reinterpret_cast<float2*>(o + kn2 + c.ds_stride));
+    CK_LAUNCH();
+}
+
+void kkt_rhs(Ctx& c, Vec& out) {
+    require(out.ctx == &c && out.prec == FWI_C128, "kkt_rhs: complex128 vector of this state required");
+    CK(cudaMemsetAsync(out.d.p, 0, out.d.bytes(), c.stream));
+    if (c.ndata)
+        kkt_rhs_scatter<<<(c.K + 127) / 128, 128, 0, c.stream>>>(c.K, c.n, c.recv_offset.p,
+                                                                 c.recv_node.p, c.w.p, c.r.p,
+                                                                 c.du_of(out.d.p));
+    if (!c.drop)
+        kkt_rhs_ds<<<grid_blocks(c.n, 256, 4 * sm_count()), 256, 0, c.stream>>>(
+            c.n, -c.eps, c.s.p, c.ds_of(out.d.p));
+    CK_LAUNCH();
+}
+
+}  // namespace fwi_b200

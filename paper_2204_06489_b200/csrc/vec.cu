@@ -1,0 +1,229 @@
+// vec.cu — K5: Krylov vector algebra on flat KKT vectors.
+//
+// Reference: KktVector dot/norm/axpy/scal (src/kkt.cpp:15-39) over
+// vec.hpp:16-58, and the GMRES vector passes (include/fwi/krylov.hpp:181-237).
+// By F4 a KKT vector is a flat array of 4Kn+n doubles and the KKT
+// inner product is the plain real dot product of that array, so every
+// operation here is real BLAS-1 on one contiguous buffer.
+//
+// Reductions are deterministic: a fixed grid (reduce_blocks()), fixed
+// per-thread strides, a fixed shuffle tree, and the last CTA to finish sums
+// the per-CTA partials in index order. Element-wise updates keep the
+// reference's rounding (no FMA: y + (a*x) rounded twice).
+#include "ctx.cuh"
+
+namespace fwi_b200 {
+
+namespace {
+
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// block sum in a fixed order; result valid in thread 0
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (wid == 0) {
+        r = lane < (blockDim.x >> 5) ? sh[lane] : 0.0;
+        r = warp_sum(r);
+    }
+    __syncthreads();
+    return r;
+}
+
+// Combine per-CTA partials: the last CTA (ticket) sums them in index order.
+__device__ __forceinline__ void finish_reduction(double part, double* partials, unsigned* ticket,
+                                                 double* out) {
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = part;
+        __threadfence();
+        const unsigned t = atomicAdd(ticket, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    __shared__ double sh[32];
+    double v = 0.0;
+    for (int i = threadIdx.x; i < gridDim.x; i += blockDim.x) v += __ldcg(partials + i);
+    v = block_sum(v, sh);
+    if (threadIdx.x == 0) {
+        *out = v;
+        *ticket = 0u;
+    }
+}
+
+__global__ void __launch_bounds__(kRedThreads) dot_kernel(const double2* __restrict__ x,
+                                                          const double2* __restrict__ y, int64_t m,
+                                                          double* partials, unsigned* ticket,
+                                                          double* out) {
+    __shared__ double sh[32];
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const double2 a = x[i], b = y[i];
+        acc += a.x * b.x + a.y * b.y;
+    }
+    acc = block_sum(acc, sh);
+    finish_reduction(acc, partials, ticket, out);
+}
+
+__global__ void axpy_kernel(double a, const double2* __restrict__ x, double2* __restrict__ y, int64_t m) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const double2 xv = x[i];
+        double2 yv = y[i];
+        yv.x = __dadd_rn(yv.x, __dmul_rn(a, xv.x));
+        yv.y = __dadd_rn(yv.y, __dmul_rn(a, xv.y));
+        y[i] = yv;
+    }
+}
+
+__global__ void scal_kernel(double a, double2* __restrict__ x, int64_t m) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        double2 v = x[i];
+        v.x = __dmul_rn(a, v.x);
+        v.y = __dmul_rn(a, v.y);
+        x[i] = v;
+    }
+}
+
+// MGS step (krylov.hpp:183-186), fused: w -= h_{i-1} v_{i-1} (h read from
+// device memory, no host round trip), then h_i = <v_i, w> (or <w, w> when
+// vnext is null, for ||w||).
+__global__ void __launch_bounds__(kRedThreads) mgs_kernel(double2* __restrict__ w,
+                                                          const double2* __restrict__ vprev,
+                                                          const double* __restrict__ hprev,
+                                                          const double2* __restrict__ vnext, int64_t m,
+                                                          double* partials, unsigned* ticket,
+                                                          double* out) {
+    __shared__ double sh[32];
+    const double nh = vprev ? -*hprev : 0.0;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        double2 wv = w[i];
+        if (vprev) {
+            const double2 pv = vprev[i];
+            wv.x = __dadd_rn(wv.x, __dmul_rn(nh, pv.x));
+            wv.y = __dadd_rn(wv.y, __dmul_rn(nh, pv.y));
+            w[i] = wv;
+        }
+        const double2 nv = vnext ? vnext[i] : wv;
+        acc += nv.x * wv.x + nv.y * wv.y;
+    }
+    acc = block_sum(acc, sh);
+    finish_reduction(acc, partials, ticket, out);
+}
+
+struct MultiAxpyArgs {
+    const double2* v[64];
+};
+
+// x_cand = x + sum_i y_i v_i with the reference's sequential rounding
+// (krylov.hpp:231-232: one axpy per basis vector, in order).
+__global__ void multi_axpy_kernel(double2* __restrict__ out, const double2* __restrict__ x,
+                                  MultiAxpyArgs args, const double* __restrict__ y, int mvec,
+                                  int64_t m) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        double2 acc = x ? x[i] : make_double2(0.0, 0.0);
+        for (int j = 0; j < mvec; ++j) {
+            const double yj = y[j];
+            const double2 v = args.v[j][i];
+            acc.x = __dadd_rn(acc.x, __dmul_rn(yj, v.x));
+            acc.y = __dadd_rn(acc.y, __dmul_rn(yj, v.y));
+        }
+        out[i] = acc;
+    }
+}
+
+// ||b - ax||^2 without materialising the residual (krylov.hpp:234-237)
+__global__ void __launch_bounds__(kRedThreads) sub_norm2_kernel(const double2* __restrict__ b,
+                                                                const double2* __restrict__ ax, int64_t m,
+                                                                double* partials, unsigned* ticket,
+                                                                double* out) {
+    __shared__ double sh[32];
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const double2 bv = b[i], av = ax[i];
+        const double rx = __dsub_rn(bv.x, av.x), ry = __dsub_rn(bv.y, av.y);
+        acc += rx * rx + ry * ry;
+    }
+    acc = block_sum(acc, sh);
+    finish_reduction(acc, partials, ticket, out);
+}
+
+}  // namespace
+
+int reduce_blocks() { return 2 * sm_count(); }
+
+static int ew_blocks(int64_t m) { return grid_blocks(m, 256, 16 * sm_count()); }
+
+void dev_dot_async(cudaStream_t st, const double* x, const double* y, double* out_dev,
+                   double* partials, unsigned* ticket, int64_t len) {
+    dot_kernel<<<reduce_blocks(), kRedThreads, 0, st>>>(reinterpret_cast<const double2*>(x),
+                                                        reinterpret_cast<const double2*>(y), len / 2,
+                                                        partials, ticket, out_dev);
+    CK_LAUNCH();
+}
+
+double dev_dot(Ctx* c, cudaStream_t st, const double* x, const double* y, int64_t len) {
+    dev_dot_async(st, x, y, c->red_out.p, c->red_partials.p, c->red_ticket.p, len);
+    double h = 0.0;
+    CK(cudaMemcpyAsync(&h, c->red_out.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return h;
+}
+
+void dev_axpy(cudaStream_t st, double a, const double* x, double* y, int64_t len) {
+    axpy_kernel<<<ew_blocks(len / 2), 256, 0, st>>>(a, reinterpret_cast<const double2*>(x),
+                                                    reinterpret_cast<double2*>(y), len / 2);
+    CK_LAUNCH();
+}
+
+void dev_scal(cudaStream_t st, double a, double* x, int64_t len) {
+    scal_kernel<<<ew_blocks(len / 2), 256, 0, st>>>(a, reinterpret_cast<double2*>(x), len / 2);
+    CK_LAUNCH();
+}
+
+void dev_mgs_step(cudaStream_t st, double* w, const double* vprev, const double* hprev_dev,
+                  const double* vnext, double* h_out_dev, double* partials, unsigned* ticket,
+                  int64_t len) {
+    mgs_kernel<<<reduce_blocks(), kRedThreads, 0, st>>>(
+        reinterpret_cast<double2*>(w), reinterpret_cast<const double2*>(vprev), hprev_dev,
+        reinterpret_cast<const double2*>(vnext), len / 2, partials, ticket, h_out_dev);
+    CK_LAUNCH();
+}
+
+void dev_multi_axpy(cudaStream_t st, double* out, const double* x, const double* const* v,
+                    const double* y_dev, int m, int64_t len) {
+    MultiAxpyArgs a{};
+    require(m <= 64, "gmres: restart larger than 63 is not supported by the fused update");
+    for (int i = 0; i < m; ++i) a.v[i] = reinterpret_cast<const double2*>(v[i]);
+    multi_axpy_kernel<<<ew_blocks(len / 2), 256, 0, st>>>(reinterpret_cast<double2*>(out),
+                                                          reinterpret_cast<const double2*>(x), a,
+                                                          y_dev, m, len / 2);
+    CK_LAUNCH();
+}
+
+void dev_sub_norm2(cudaStream_t st, const double* b, const double* ax, double* out_dev,
+                   double* partials, unsigned* ticket, int64_t len) {
+    sub_norm2_kernel<<<reduce_blocks(), kRedThreads, 0, st>>>(
+        reinterpret_cast<const double2*>(b), reinterpret_cast<const double2*>(ax), len / 2, partials,
+        ticket, out_dev);
+    CK_LAUNCH();
+}
+
+}  // namespace fwi_b200

@@ -1,0 +1,323 @@
+"""GPU parity: the CUDA path (libfwi_b200.so through the C ABI) against the
+reference CPU implementation run on the same seeded inputs.
+
+The checker here is the unmodified reference core (oracle/_ref, built from
+/root/reference/proj/src by oracle/Makefile) driven through its own API.
+Tolerances are the north star's: complex128 operator applies bit-exact where
+the arithmetic order is reproduced (kkt_apply, kkt_rhs, ILU preconditioner),
+<= 1e-12 relative L2 otherwise; GMRES residual histories <= 1e-8 relative per
+iteration.
+"""
+import numpy as np
+import pytest
+
+import pyoracle as po
+from paper_2204_06489_b200 import _abi
+from paper_2204_06489_b200 import api as fw
+from paper_2204_06489_b200.problem import (c1_problem, c2_problem, no_receiver_instance, random_kkt,
+                                           small_problem, standard_instance)
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def pair_direct(p, ilu_level=-1, exact=False):
+    """Reference and device states built from identical inputs (u and r given)."""
+    ref = po.Ref(p, full=False, exact=exact, ilu_level=ilu_level)
+    dev = fw.GnState(p, exact=exact, ilu_level=ilu_level)
+    return ref, dev
+
+
+@pytest.fixture(scope="module")
+def c1():
+    p = c1_problem()
+    p.d_obs = po.ref_simulate(p)
+    ref = po.Ref(p, full=True, exact=True, ilu_level=4)
+    # identical linearisation point on the device: upload the reference's u and r
+    q = c1_problem()
+    q.u, q.r = ref.u(), ref.residual()
+    dev = fw.GnState(q, exact=True, ilu_level=4)
+    return p, ref, dev
+
+
+PROBLEMS = [
+    lambda: small_problem(),
+    lambda: small_problem(nx=31, nz=23, n_pml=4, K=4, R=7, duplicate_receiver=True,
+                          weight_mode=_abi.FWI_WEIGHT_OFFSET, seed=3),
+    lambda: small_problem(nx=17, nz=29, n_pml=2, K=2, R=3, seed=11),  # nz > nx: row lines
+]
+
+
+@pytest.mark.parametrize("mk", PROBLEMS)
+def test_stencil_bitwise_equals_reference_csr(mk):
+    p = mk()
+    ref, dev = pair_direct(p)
+    rp, ci, va = ref.csr()
+    d, e, s = dev.stencil()
+    nx = p.grid.nx
+    for i in range(p.n):
+        for q in range(rp[i], rp[i + 1]):
+            j = ci[q]
+            want = va[q]
+            got = d[i] if j == i else e[i] if j == i + 1 else s[i] if j == i + nx else \
+                e[j] if j == i - 1 else s[j]
+            assert got == want, (i, j, got, want)
+
+
+@pytest.mark.parametrize("mk", PROBLEMS)
+def test_kkt_apply_bit_exact_small(mk):
+    p = mk()
+    ref, dev = pair_direct(p)
+    for seed in range(3):
+        x = random_kkt(p, 100 + seed)
+        want = ref.kkt_apply(x)
+        got = fw.kkt_apply(dev, fw.KktVector.from_host(dev, x)).to_host()
+        assert np.array_equal(got, want), rel(got, want)
+
+
+def test_kkt_apply_zero_and_unit_model_vector():
+    """tests/test_kkt.cpp:48-69 restated: M 0 = 0; xi = (0, e_m, 0) -> (0, eps e_m, -P e_m)."""
+    p = standard_instance()
+    p.d_obs = po.ref_simulate(p)
+    ref = po.Ref(p, full=True)
+    q = standard_instance()
+    q.u, q.r = ref.u(), ref.residual()
+    dev = fw.GnState(q, exact=False)
+    z = np.zeros(p.vec_len)
+    assert np.all(fw.kkt_apply(dev, fw.KktVector.from_host(dev, z)).to_host() == 0.0)
+    node = p.grid.index(5, 5)
+    n, K = p.n, p.K
+    x = z.copy()
+    x[2 * K * n + node] = 1.0
+    out = fw.kkt_apply(dev, fw.KktVector.from_host(dev, x)).to_host()
+    assert np.all(out[: 2 * K * n] == 0.0)
+    ds = out[2 * K * n: 2 * K * n + n]
+    assert ds[node] == p.epsilon and np.count_nonzero(ds) == 1
+    lam = out[2 * K * n + n:].view(np.complex128).reshape(K, n)
+    u = ref.u().reshape(K, n)
+    w2 = ref.omega ** 2
+    for k in range(K):
+        assert lam[k, node] == -(w2 * u[k, node])
+        assert np.count_nonzero(lam[k]) == 1
+
+
+def test_kkt_apply_c1_bit_exact(c1):
+    p, ref, dev = c1
+    x = random_kkt(p, 7)
+    want = ref.kkt_apply(x)
+    got = fw.kkt_apply(dev, fw.KktVector.from_host(dev, x)).to_host()
+    assert np.array_equal(got, want), rel(got, want)
+
+
+def test_kkt_apply_c2_parity():
+    """BASELINE config 2 at full size: 1e-12 gate (bit-exact expected)."""
+    p = c2_problem()
+    ref, dev = pair_direct(p)
+    x = random_kkt(p, 11)
+    want = ref.kkt_apply(x)
+    got = fw.kkt_apply(dev, fw.KktVector.from_host(dev, x)).to_host()
+    assert rel(got, want) <= 1e-12
+    assert np.array_equal(got, want)
+
+
+def test_kkt_rhs_exact(c1):
+    p, ref, dev = c1
+    assert np.array_equal(fw.kkt_rhs(dev).to_host(), ref.kkt_rhs())
+    dev.set_drop_reg_term(False)
+    ref.set_drop(False)
+    try:
+        assert np.array_equal(fw.kkt_rhs(dev).to_host(), ref.kkt_rhs())
+    finally:
+        dev.set_drop_reg_term(True)
+        ref.set_drop(True)
+
+
+def test_operator_symmetric_in_real_inner_product(c1):
+    """tests/test_kkt.cpp:81-90: <M xi, eta> = <M eta, xi>."""
+    p, ref, dev = c1
+    for s in range(3):
+        xi = fw.KktVector.from_host(dev, random_kkt(p, 300 + s))
+        eta = fw.KktVector.from_host(dev, random_kkt(p, 800 + s))
+        lhs = fw.dot(fw.kkt_apply(dev, xi), eta)
+        rhs = fw.dot(fw.kkt_apply(dev, eta), xi)
+        assert abs(lhs - rhs) <= 1e-12 * max(1.0, abs(lhs))
+
+
+def test_vector_ops_match_reference_formulas(c1):
+    p, ref, dev = c1
+    a, b = random_kkt(p, 1), random_kkt(p, 2)
+    va, vb = fw.KktVector.from_host(dev, a), fw.KktVector.from_host(dev, b)
+    assert abs(fw.dot(va, vb) - a @ b) <= 1e-12 * np.linalg.norm(a) * np.linalg.norm(b)
+    assert abs(fw.norm(va) - np.linalg.norm(a)) <= 1e-13 * np.linalg.norm(a)
+    fw.axpy(-0.37, va, vb)
+    assert np.array_equal(vb.to_host(), b + (-0.37) * a)
+    fw.scal(1.5, va)
+    assert np.array_equal(va.to_host(), 1.5 * a)
+
+
+def test_ilu_precond_bit_exact(c1):
+    p, ref, dev = c1
+    for s in range(2):
+        x = random_kkt(p, 40 + s)
+        want = ref.precond_apply(x, _abi.FWI_PRECOND_ILU)
+        got = fw.precond_apply(dev, fw.KktVector.from_host(dev, x), fw.PrecondMode.ilu).to_host()
+        assert np.array_equal(got, want), rel(got, want)
+
+
+@pytest.mark.parametrize("level", [0, 1, 3])
+@pytest.mark.parametrize("mk", PROBLEMS)
+def test_ilu_solves_bit_exact_small(mk, level):
+    p = mk()
+    ref, dev = pair_direct(p, ilu_level=level)
+    rng = np.random.default_rng(level)
+    b = rng.standard_normal(p.n) + 1j * rng.standard_normal(p.n)
+    for adj in (False, True):
+        want = ref.solve(b, _abi.FWI_PRECOND_ILU, adj)
+        got = dev.solve(b, fw.PrecondMode.ilu, adj)
+        assert np.array_equal(got, want), (adj, rel(got, want))
+
+
+@pytest.mark.parametrize("mk", PROBLEMS)
+def test_exact_block_solve_matches_reference_lu(mk):
+    p = mk()
+    ref, dev = pair_direct(p, exact=True)
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal(p.n) + 1j * rng.standard_normal(p.n)
+    for adj in (False, True):
+        want = ref.solve(b, _abi.FWI_PRECOND_EXACT, adj)
+        got = dev.solve(b, fw.PrecondMode.exact, adj)
+        assert rel(got, want) <= 1e-11, (adj, rel(got, want))
+
+
+def test_exact_precond_c1(c1):
+    p, ref, dev = c1
+    x = random_kkt(p, 9)
+    want = ref.precond_apply(x, _abi.FWI_PRECOND_EXACT)
+    got = fw.precond_apply(dev, fw.KktVector.from_host(dev, x), fw.PrecondMode.exact).to_host()
+    assert rel(got, want) <= 1e-10, rel(got, want)
+
+
+def test_precond_cost_contract(c1):
+    """tests/test_kkt.cpp:153-159: one exact precond_apply = 2K solve pairs."""
+    p, ref, dev = c1
+    dev.reset_solve_count(fw.PrecondMode.exact)
+    fw.precond_apply(dev, fw.KktVector.from_host(dev, random_kkt(p, 1)), fw.PrecondMode.exact)
+    assert dev.solve_count(fw.PrecondMode.exact) == 2 * p.K
+
+
+def test_exact_precond_inverts_operator_without_receivers():
+    """tests/test_kkt.cpp:132-140."""
+    p = no_receiver_instance()
+    dev = fw.GnState(p, exact=True)
+    for s in range(3):
+        x = random_kkt(p, 71 + s)
+        xi = fw.KktVector.from_host(dev, x)
+        back = fw.precond_apply(dev, fw.kkt_apply(dev, xi), fw.PrecondMode.exact).to_host()
+        assert rel(back, x) < 1e-10
+
+
+def test_forward_fields_match_reference(c1):
+    p, ref, _ = c1
+    dev = fw.GnState(p, exact=True)  # u by the device's own exact forward solves
+    assert rel(dev.u(), ref.u()) < 1e-10
+    assert rel(dev.residual(), ref.residual()) < 1e-8
+
+
+@pytest.mark.parametrize("mode", [fw.PrecondMode.exact, fw.PrecondMode.ilu])
+def test_fsgn_residual_history_c1(c1, mode):
+    """Residual histories agree to 1e-8 per iteration (north-star gate)."""
+    p, ref, dev = c1
+    maxit = 50 if mode == fw.PrecondMode.ilu else 30
+    ds_r, log_r = ref.fsgn(int(mode), 30, 0.0, maxit, 0)
+    ds_d, log_d = fw.fsgn_gmres_step(dev, fw.FsgnOptions(mode=mode, restart=30, tol=0.0, maxit=maxit,
+                                                         ecg_stride=0))
+    rr, rd = np.array(log_r.residuals()), np.array(log_d.residuals())
+    assert len(rr) == len(rd)
+    dev_rel = np.abs(rd - rr) / rr
+    print("max history deviation", dev_rel.max(), "per-iter", dev_rel)
+    assert dev_rel.max() <= 1e-8
+
+
+def test_fsgn_converges_c1(c1):
+    p, ref, dev = c1
+    ds_r, log_r = ref.fsgn(_abi.FWI_PRECOND_EXACT, 30, 1e-3, 60, 0)
+    ds_d, log_d = fw.fsgn_gmres_step(dev, fw.FsgnOptions(tol=1e-3, maxit=60, ecg_stride=0))
+    assert log_d.converged and log_d.iterations() == log_r.iterations()
+    assert rel(ds_d, ds_r) < 1e-6
+
+
+def test_zero_receivers_converge_in_one_iteration():
+    """tests/test_kkt.cpp:179-189."""
+    p = no_receiver_instance()
+    dev = fw.GnState(p, exact=True)
+    ds, log = fw.fsgn_gmres_step(dev, fw.FsgnOptions(tol=1e-10, maxit=30))
+    assert log.converged and log.iterations() == 1 and log.final_residual() < 1e-10
+
+
+def test_c64_apply_deviation():
+    p = c2_problem()
+    ref = po.Ref(p, full=False, exact=False)
+    dev = fw.GnState(p, exact=False, c64=True)
+    x = random_kkt(p, 11)
+    want = ref.kkt_apply(x)
+    got = fw.kkt_apply(dev, fw.KktVector.from_host(dev, x.astype(np.float32), _abi.FWI_C64)).to_host()
+    err = rel(got.astype(np.float64), want)
+    print("complex64 apply relative L2 deviation", err)
+    assert err < 1e-5
+
+
+# ---- generic GMRES known answers (tests/test_krylov.cpp:63-125, real systems)
+
+def test_gmres_identity_one_iteration():
+    b = np.array([1.0, 2.0, 3.0, -1.0])
+    x, log = fw.gmres(lambda v: v, lambda v: v, b, 5, 1e-12, 20)
+    assert log.converged and log.iterations() == 1 and rel(x, b) < 1e-13
+
+
+def test_gmres_exact_inverse_preconditioner():
+    m = np.array([[2.0, 0.5], [-1.0, 3.0]])
+    mi = np.linalg.inv(m)
+    x, log = fw.gmres(lambda v: m @ v, lambda v: mi @ v, np.array([1.0, 0.5]), 5, 1e-10, 20)
+    assert log.converged and log.iterations() == 1 and log.final_residual() < 1e-10
+
+
+def test_gmres_4x4_by_iteration_4():
+    m = np.array([[2, 1, 0, 1], [0, 3, 1, 0], [1, 0, 4, 1], [0, -1, 0, 5.0]])
+    x0 = np.array([1.0, -2.0, 3.0, 2.0])
+    x, log = fw.gmres(lambda v: m @ v, lambda v: v, m @ x0, 4, 1e-12, 4)
+    assert log.converged and log.iterations() <= 4 and rel(x, x0) < 1e-10
+
+
+def test_gmres_stagnation_on_nilpotent():
+    m = np.array([[0.0, 1.0], [0.0, 0.0]])
+    x, log = fw.gmres(lambda v: m @ v, lambda v: v, np.array([1.0, 0.0]), 2, 1e-12, 8)
+    assert not log.converged and log.stagnated
+
+
+def test_gmres_observer_stops():
+    m = np.array([[4, 1, 0, 0], [1, 3, 1, 0], [0, 1, 5, 0], [0, 0, 0, 2.0]])
+    calls = []
+    x, log = fw.gmres(lambda v: m @ v, lambda v: v, np.array([1.0, 2, 3, 1]), 3, 1e-14, 50,
+                      observer=lambda it, x: calls.append(it) or len(calls) >= 2)
+    assert len(calls) == 2 and log.iterations() == 2 and not log.converged
+
+
+def test_gmres_zero_rhs():
+    x, log = fw.gmres(lambda v: v, lambda v: v, np.zeros(4), 3, 1e-12, 9)
+    assert log.converged and log.iterations() == 0 and np.all(x == 0)
+
+
+def test_invalid_arguments_raise():
+    with pytest.raises(fw.InvalidArgument):
+        fw.gmres(lambda v: v, lambda v: v, np.ones(2), 0, 1e-12, 9)
+    p = small_problem()
+    dev = fw.GnState(p, exact=False)
+    with pytest.raises(fw.InvalidArgument):
+        fw.precond_apply(dev, fw.KktVector(dev), fw.PrecondMode.ilu)
+    bad = small_problem()
+    bad.epsilon = 0.0
+    with pytest.raises(fw.InvalidArgument):
+        fw.GnState(bad)
