@@ -4,6 +4,7 @@
 // and the data residual.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "ctx.cuh"
@@ -98,6 +99,8 @@ int sm_count() {
 Ctx::~Ctx() {
     if (exact) exact_free(exact);
     if (ilu) ilu_free(ilu);
+    for (auto*& p : kplan)
+        if (p) kkt_plan_free(p);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -161,6 +164,7 @@ Ctx* ctx_create(const fwi_state_desc& d) {
     c->ds_stride = (n + 31) / 32 * 32;
     c->vec_len = 4 * int64_t(c->K) * n + c->ds_stride;
     c->precision_mask = d.precision_mask;
+    if (const char* v = std::getenv("FWI_KKT_KERNEL")) c->kkt_variant = std::string(v) == "plain" ? 1 : 0;
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     cudaStream_t st = c->stream;
 

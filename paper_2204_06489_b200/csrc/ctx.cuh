@@ -23,6 +23,7 @@ namespace fwi_b200 {
 
 struct ExactFactor;  // exact.cu
 struct IluFactor;    // ilu.cu
+struct KktPlan;      // kkt_tma.cu
 
 struct Ctx {
     // geometry / scalars
@@ -55,6 +56,8 @@ struct Ctx {
     ExactFactor* exact = nullptr;  // owned (exact_free)
     IluFactor* ilu = nullptr;      // owned (ilu_free)
     int64_t solve_count[2] = {0, 0};
+    KktPlan* kplan[2] = {nullptr, nullptr};  // TMA apply plans (c128, c64), built lazily
+    int kkt_variant = 0;                      // 0: TMA persistent kernel, 1: plain kernel (FWI_KKT_KERNEL=plain)
     // host copy of the stencil for the ILU factorisation (lazily)
     std::vector<double> h_s;
 
@@ -90,6 +93,8 @@ void stencil_to_host(const Ctx& c, double* diag, double* east, double* south);
 void kkt_apply(Ctx& c, const Vec& xi, Vec& out);
 void kkt_rhs(Ctx& c, Vec& out);
 void kkt_apply_raw(Ctx& c, const double* xi, double* out);  // c128 flat device buffers
+bool kkt_apply_tma(Ctx& c, bool f32, const void* xi, void* out);
+void kkt_plan_free(KktPlan*);
 
 // ---- vec.cu  (flat device arrays of len doubles; deterministic reductions)
 double dev_dot(Ctx* c, cudaStream_t st, const double* x, const double* y, int64_t len);

@@ -18,56 +18,12 @@
 // and A^H lambda is a gather with conjugated coefficients in ascending row
 // order — the same summation order as the reference's column scatter, so the
 // complex128 result is bit-identical to the reference.
+#include "arith.cuh"
 #include "ctx.cuh"
 
 namespace fwi_b200 {
 
 namespace {
-
-// complex128: reference-faithful rounding (no FMA), see common.cuh
-struct F64 {
-    using T = double2;
-    using R = double;
-    static __device__ __forceinline__ T zero() { return make_double2(0.0, 0.0); }
-    static __device__ __forceinline__ T add(T a, T b) { return cadd(a, b); }
-    static __device__ __forceinline__ T sub(T a, T b) { return csub(a, b); }
-    static __device__ __forceinline__ T mul(T a, T b) { return cmul(a, b); }
-    static __device__ __forceinline__ T mulc(T a, T b) { return cmulc(a, b); }
-    static __device__ __forceinline__ T rm(R r, T a) { return rmul(r, a); }
-    static __device__ __forceinline__ R radd(R a, R b) { return __dadd_rn(a, b); }
-    static __device__ __forceinline__ R rmulr(R a, R b) { return __dmul_rn(a, b); }
-    static __device__ __forceinline__ R rsub(R a, R b) { return __dsub_rn(a, b); }
-    // Re(w2 * conj(u) * z) exactly as std::real(w2 * std::conj(u) * z)
-    static __device__ __forceinline__ R re_pconj(R w2, T u, T z) {
-        const R a = __dmul_rn(u.x, w2), b = __dmul_rn(-u.y, w2);
-        return __dsub_rn(__dmul_rn(a, z.x), __dmul_rn(b, z.y));
-    }
-    // (w2 * u) * v
-    static __device__ __forceinline__ T pmul(R w2, T u, R v) {
-        return make_double2(__dmul_rn(__dmul_rn(w2, u.x), v), __dmul_rn(__dmul_rn(w2, u.y), v));
-    }
-};
-
-// complex64: plain fast arithmetic (reported separately with its deviation)
-struct F32 {
-    using T = float2;
-    using R = float;
-    static __device__ __forceinline__ T zero() { return make_float2(0.f, 0.f); }
-    static __device__ __forceinline__ T add(T a, T b) { return make_float2(a.x + b.x, a.y + b.y); }
-    static __device__ __forceinline__ T sub(T a, T b) { return make_float2(a.x - b.x, a.y - b.y); }
-    static __device__ __forceinline__ T mul(T a, T b) {
-        return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-    }
-    static __device__ __forceinline__ T mulc(T a, T b) {
-        return make_float2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
-    }
-    static __device__ __forceinline__ T rm(R r, T a) { return make_float2(r * a.x, r * a.y); }
-    static __device__ __forceinline__ R radd(R a, R b) { return a + b; }
-    static __device__ __forceinline__ R rmulr(R a, R b) { return a * b; }
-    static __device__ __forceinline__ R rsub(R a, R b) { return a - b; }
-    static __device__ __forceinline__ R re_pconj(R w2, T u, T z) { return w2 * (u.x * z.x + u.y * z.y); }
-    static __device__ __forceinline__ T pmul(R w2, T u, R v) { return make_float2(w2 * u.x * v, w2 * u.y * v); }
-};
 
 template <class A>
 __global__ void __launch_bounds__(256) kkt_apply_kernel(
@@ -166,6 +122,7 @@ __global__ void kkt_rhs_ds(int64_t n, double neg_eps, const double* __restrict__
 }  // namespace
 
 void kkt_apply_raw(Ctx& c, const double* xi, double* out) {
+    if (c.kkt_variant == 0 && kkt_apply_tma(c, false, xi, out)) return;
     dim3 blk(32, 8), grd((c.nx + 31) / 32, (c.nz + 7) / 8);
     double* x = const_cast<double*>(xi);
     kkt_apply_kernel<F64><<<grd, blk, 0, c.stream>>>(
@@ -184,6 +141,7 @@ void kkt_apply(Ctx& c, const Vec& xi, Vec& out) {
         return;
     }
     require(c.u32.p != nullptr, "kkt_apply: context was created without the complex64 copy");
+    if (c.kkt_variant == 0 && kkt_apply_tma(c, true, xi.f.p, out.f.p)) return;
     dim3 blk(32, 8), grd((c.nx + 31) / 32, (c.nz + 7) / 8);
     const int64_t kn2 = 2 * int64_t(c.K) * c.n;
     float* x = const_cast<float*>(xi.f.p);

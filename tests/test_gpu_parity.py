@@ -123,6 +123,19 @@ def test_kkt_apply_c2_parity():
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("variant", ["plain", "tma"])
+@pytest.mark.parametrize("mk", PROBLEMS + [lambda: c2_problem(K=5, R=17)])
+def test_kkt_apply_kernel_variants_bit_exact(mk, variant, monkeypatch):
+    """Both K1 kernels (TMA-pipelined persistent, plain) reproduce the reference."""
+    monkeypatch.setenv("FWI_KKT_KERNEL", variant)
+    p = mk()
+    ref, dev = pair_direct(p)
+    x = random_kkt(p, 5)
+    want = ref.kkt_apply(x)
+    got = fw.kkt_apply(dev, fw.KktVector.from_host(dev, x)).to_host()
+    assert np.array_equal(got, want), rel(got, want)
+
+
 def test_kkt_rhs_exact(c1):
     p, ref, dev = c1
     assert np.array_equal(fw.kkt_rhs(dev).to_host(), ref.kkt_rhs())
