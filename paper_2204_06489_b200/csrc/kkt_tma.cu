@@ -67,6 +67,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <class A>
 struct TmaArgs {
     using T = typename A::T;
@@ -80,10 +89,18 @@ struct TmaArgs {
     const R* ds;
     T *odu, *ola;
     R* ods;
-    const int4* regions;  // x0, w, z0, h
-    int BW, BWU;          // halo box width / u box width (complex elements)
-    int stages, cm;
-    uint32_t dub, ub, stage_bytes, tx_bytes;
+    const int4* tiles;     // x0, w, z0, h   (w <= 128, h <= 8)
+    int T_, C;             // tiles, K-chunks (units = T_ * C, chunk-major)
+    unsigned* sched;       // [0] next unit, [1] finished CTAs
+    unsigned* flags;       // per tile: chunks completed (epoch-based)
+    unsigned base;         // epoch * C
+    int RP, UP;            // smem row pitch (complex) of the halo tiles / of the u tile
+    int stages;
+    int memonly;           // diagnostics: move the data, skip the arithmetic
+    int nofold;            // diagnostics: skip the ordered ds fold (wrong ds)
+    int nostore, nou;      // diagnostics: skip the output stores / the u load
+    int gr;                // complex numbers per innermost TMA element group
+    uint32_t dub, ub, stage_bytes, tx_bytes, ub_bytes;
 };
 
 template <class T>
@@ -93,136 +110,227 @@ __device__ __forceinline__ void st_stream<double2>(double2* p, double2 v) { __st
 template <>
 __device__ __forceinline__ void st_stream<float2>(float2* p, float2 v) { __stcs(p, v); }
 
-template <class A>
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+constexpr int kRing = 8;
+
+// Units = (tile, chunk of KC sources), claimed dynamically in chunk-major
+// order by persistent CTAs. A unit's ds contribution is folded into the
+// tile's running partial sum (kept in out.ds) strictly in source order: the
+// unit waits for the tile's previous chunk, so the complex128 result stays
+// bit-identical to the reference's sequential sum.
+// One node, one source: the three block rows of the KKT operator with the
+// reference's rounding order. FULL: all four neighbours present (interior
+// fast path, no per-term predication).
+template <class A, bool FULL>
+__device__ __forceinline__ void node_step(const typename A::T* dr, const typename A::T* lr, int RP,
+                                          bool hN, bool hW, bool hE, bool hS, typename A::T cD,
+                                          typename A::T cN, typename A::T cW, typename A::T cE,
+                                          typename A::T cS, typename A::T& s_, typename A::T& t_) {
+    using T = typename A::T;
+    s_ = A::zero();
+    t_ = A::zero();
+    if (FULL || hN) {
+        s_ = A::add(s_, A::mul(cN, dr[-RP]));
+        t_ = A::add(t_, A::mulc(cN, lr[-RP]));
+    }
+    if (FULL || hW) {
+        s_ = A::add(s_, A::mul(cW, dr[-1]));
+        t_ = A::add(t_, A::mulc(cW, lr[-1]));
+    }
+    s_ = A::add(s_, A::mul(cD, dr[0]));
+    t_ = A::add(t_, A::mulc(cD, lr[0]));
+    if (FULL || hE) {
+        s_ = A::add(s_, A::mul(cE, dr[1]));
+        t_ = A::add(t_, A::mulc(cE, lr[1]));
+    }
+    if (FULL || hS) {
+        s_ = A::add(s_, A::mul(cS, dr[RP]));
+        t_ = A::add(t_, A::mulc(cS, lr[RP]));
+    }
+    (void)sizeof(T);
+}
+
+// Units = (tile, chunk of KC sources), claimed dynamically in chunk-major
+// order by persistent CTAs. A unit's ds contribution is folded into the
+// tile's running partial sum (kept in out.ds) strictly in source order: the
+// unit waits for the tile's previous chunk, so the complex128 result stays
+// bit-identical to the reference's sequential sum. S (stages) divides KC, so
+// stage indices and mbarrier parities are compile-time within a unit.
+template <class A, int KC, int S>
 __global__ void __launch_bounds__(kThreads, 1)
     kkt_tma_kernel(const __grid_constant__ CUtensorMap tdu, const __grid_constant__ CUtensorMap tla,
                    const __grid_constant__ CUtensorMap tu, const TmaArgs<A> P) {
+    static_assert(KC % S == 0, "stages must divide the chunk");
     using T = typename A::T;
     using R = typename A::R;
     extern __shared__ __align__(1024) unsigned char sm[];
-    // mbarriers live in the dynamic allocation, after the stages (explicit layout)
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + size_t(P.stages) * P.stage_bytes);
-    const int4 rg = P.regions[blockIdx.x];
-    const int x0 = rg.x, w = rg.y, z0 = rg.z, h = rg.w;
-    const int K = P.K, nx = P.nx, nz = P.nz, S = P.stages;
-    const int nsub = (h + kRows - 1) / kRows;
-    const int nsteps = nsub * K;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + size_t(S) * P.stage_bytes);
+    int* ring = reinterpret_cast<int*>(bar + kMaxStages);
+    // this chunk's Re(w^2 conj(u_k) lambda_k) terms, [KC][2][kThreads]
+    R* terms = reinterpret_cast<R*>(sm + size_t(S) * P.stage_bytes + 128);
+    const int nx = P.nx, nz = P.nz, Tn = P.T_;
+    const int U = Tn * P.C;
     const int tid = threadIdx.x, lx = tid & (kCols - 1), zs = tid >> 7;
-    const int BW = P.BW, BWU = P.BWU;
+    const int RP = P.RP, UP = P.UP;
+    const int64_t n = P.n;
+
+    // producer (thread 0): claims units lazily, issues one step = 3 TMA boxes
+    int nclaimed = 0;
+    auto issue = [&](int j) {
+        const int qq = j / KC;
+        while (nclaimed <= qq) {
+            const unsigned u = atomicAdd(P.sched, 1u);
+            ring[nclaimed % kRing] = u < unsigned(U) ? int(u) : -1;
+            ++nclaimed;
+        }
+        const int u = ring[qq % kRing];
+        if (u < 0) return;
+        const int t = u % Tn, c = u / Tn;
+        const int k = c * KC + j % KC;
+        const int4 tl = P.tiles[t];
+        const int s = j % S;
+        unsigned char* st = sm + size_t(s) * P.stage_bytes;
+        mbar_expect_tx(&bar[s], P.nou ? P.tx_bytes - P.ub_bytes : P.tx_bytes);
+        // halo tiles start one complex pair (two nodes) left of the tile, so a
+        // smem row holds x0-2 .. x0+RP-3
+        tma_load_4d(st, &tdu, 0, tl.x / P.gr - 1, tl.z - 1, k, &bar[s]);
+        tma_load_4d(st + P.dub, &tla, 0, tl.x / P.gr - 1, tl.z - 1, k, &bar[s]);
+        if (!P.nou) tma_load_4d(st + 2 * P.dub, &tu, 0, tl.x / P.gr, tl.z, k, &bar[s]);
+    };
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int j = 0; j < S; ++j) issue(j);
     }
     __syncthreads();
 
-    auto issue = [&](int j) {
-        const int s = j % S;
-        const int sub = j / K, k = j - sub * K;
-        const int zt = z0 + kRows * sub;
-        unsigned char* st = sm + size_t(s) * P.stage_bytes;
-        mbar_expect_tx(&bar[s], P.tx_bytes);
-        const int cm = P.cm;  // tensor elements per complex number
-        tma_load_3d(st, &tdu, cm * (x0 - 1), zt - 1, k, &bar[s]);
-        tma_load_3d(st + P.dub, &tdu, cm * (x0 - 1 + BW), zt - 1, k, &bar[s]);
-        tma_load_3d(st + 2 * P.dub, &tla, cm * (x0 - 1), zt - 1, k, &bar[s]);
-        tma_load_3d(st + 3 * P.dub, &tla, cm * (x0 - 1 + BW), zt - 1, k, &bar[s]);
-        tma_load_3d(st + 4 * P.dub, &tu, cm * x0, zt, k, &bar[s]);
-        tma_load_3d(st + 4 * P.dub + P.ub, &tu, cm * (x0 + BWU), zt, k, &bar[s]);
-    };
-    if (tid == 0)
-        for (int j = 0; j < S && j < nsteps; ++j) issue(j);
-
-    // per-node state for the current sub-tile (two rows per thread)
-    bool act[2], hN[2], hW[2], hE[2], hS[2];
-    T cD[2], cN[2], cW[2], cE[2], cS[2];
-    R dsv[2], pl[2];
-    int q[2], qe[2];
-    int64_t cnode[2];
-
-    for (int j = 0; j < nsteps; ++j) {
-        const int sub = j / K, k = j - sub * K;
-        if (k == 0) {
-            const int zt = z0 + kRows * sub;
-            const int ht = min(kRows, h - kRows * sub);
+    for (int q = 0;; ++q) {
+        const int u = ring[q % kRing];
+        if (u < 0) break;
+        const int t = u % Tn, c = u / Tn;
+        const int4 tl = P.tiles[t];
+        const int x0 = tl.x, w = tl.y, zt = tl.z, ht = tl.w;
+        const int k0 = c * KC;
+        bool act[2], hN[2], hW[2], hE[2], hS[2];
+        T cD[2], cN[2], cW[2], cE[2], cS[2];
+        R dsv[2];
+        int qr[2], qe[2];
+        int64_t cnode[2];
+        bool full = true;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int row = zs + 4 * r;
+            act[r] = lx < w && row < ht;
+            const int ix = x0 + lx, iz = zt + row;
+            const int64_t cc = act[r] ? int64_t(iz) * nx + ix : 0;
+            cnode[r] = cc;
+            const bool bnd = on_boundary(ix, iz, nx, nz);
+            hN[r] = act[r] && !bnd && !on_boundary(ix, iz - 1, nx, nz);
+            hW[r] = act[r] && !bnd && !on_boundary(ix - 1, iz, nx, nz);
+            hE[r] = act[r] && !bnd && !on_boundary(ix + 1, iz, nx, nz);
+            hS[r] = act[r] && !bnd && !on_boundary(ix, iz + 1, nx, nz);
+            full = full && act[r] && hN[r] && hW[r] && hE[r] && hS[r];
+            cD[r] = act[r] ? P.diag[cc] : A::zero();
+            cN[r] = hN[r] ? P.south[cc - nx] : A::zero();
+            cW[r] = hW[r] ? P.east[cc - 1] : A::zero();
+            cE[r] = hE[r] ? P.east[cc] : A::zero();
+            cS[r] = hS[r] ? P.south[cc] : A::zero();
+            dsv[r] = act[r] ? P.ds[cc] : R(0);
+            int qq = act[r] ? P.nrec_ptr[cc] : 0;
+            qe[r] = act[r] ? P.nrec_ptr[cc + 1] : 0;
+            while (qq < qe[r] && P.nrec_k[qq] < k0) ++qq;
+            qr[r] = qq;
+        }
+        const bool warp_full = __all_sync(0xffffffffu, full);
+        const int par0 = (q * (KC / S)) & 1;
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) {
+            const int k = k0 + kk;
+            constexpr int dummy = 0;
+            (void)dummy;
+            const int s = kk % S;  // compile-time
+            mbar_wait(&bar[s], (par0 + kk / S) & 1);
+            const unsigned char* st = sm + size_t(s) * P.stage_bytes;
+            const T* dus = reinterpret_cast<const T*>(st) + lx + P.gr;
+            const T* las = reinterpret_cast<const T*>(st + P.dub) + lx + P.gr;
+            const T* us = reinterpret_cast<const T*>(st + 2 * P.dub) + lx;
+            T s_[2], t_[2];
+            if (P.memonly) {
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    s_[r] = dus[(zs + 4 * r + 1) * RP];
+                    t_[r] = las[(zs + 4 * r + 1) * RP];
+                }
+            } else if (warp_full) {
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+                    node_step<A, true>(dus + (zs + 4 * r + 1) * RP, las + (zs + 4 * r + 1) * RP, RP, true, true,
+                                       true, true, cD[r], cN[r], cW[r], cE[r], cS[r], s_[r], t_[r]);
+            } else {
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+                    node_step<A, false>(dus + (zs + 4 * r + 1) * RP, las + (zs + 4 * r + 1) * RP, RP, hN[r],
+                                        hW[r], hE[r], hS[r], cD[r], cN[r], cW[r], cE[r], cS[r], s_[r], t_[r]);
+            }
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const int row = zs + 4 * r;
-                act[r] = lx < w && row < ht;
-                const int ix = x0 + lx, iz = zt + row;
-                const int64_t c = act[r] ? int64_t(iz) * nx + ix : 0;
-                cnode[r] = c;
-                const bool bnd = on_boundary(ix, iz, nx, nz);
-                hN[r] = act[r] && !bnd && !on_boundary(ix, iz - 1, nx, nz);
-                hW[r] = act[r] && !bnd && !on_boundary(ix - 1, iz, nx, nz);
-                hE[r] = act[r] && !bnd && !on_boundary(ix + 1, iz, nx, nz);
-                hS[r] = act[r] && !bnd && !on_boundary(ix, iz + 1, nx, nz);
-                cD[r] = act[r] ? P.diag[c] : A::zero();
-                cN[r] = hN[r] ? P.south[c - nx] : A::zero();
-                cW[r] = hW[r] ? P.east[c - 1] : A::zero();
-                cE[r] = hE[r] ? P.east[c] : A::zero();
-                cS[r] = hS[r] ? P.south[c] : A::zero();
-                dsv[r] = act[r] ? P.ds[c] : R(0);
-                q[r] = act[r] ? P.nrec_ptr[c] : 0;
-                qe[r] = act[r] ? P.nrec_ptr[c + 1] : 0;
-                pl[r] = R(0);
+                const T duc = dus[(row + 1) * RP];
+                const T lac = las[(row + 1) * RP];
+                const T uc = us[row * UP];
+                terms[(kk * 2 + r) * kThreads + tid] = A::re_pconj(P.w2, uc, lac);
+                if (!act[r] || P.nostore) continue;
+                const int64_t o = int64_t(k) * n + cnode[r];
+                st_stream(P.ola + o, A::sub(s_[r], A::pmul(P.w2, uc, dsv[r])));
+                T tv = t_[r];
+                if (qr[r] < qe[r] && P.nrec_k[qr[r]] == k) {
+                    T f = A::zero();
+                    while (qr[r] < qe[r] && P.nrec_k[qr[r]] == k) {
+                        f = A::add(f, A::rm(R(P.nrec_w2[qr[r]]), duc));
+                        ++qr[r];
+                    }
+                    tv = A::add(f, tv);
+                }
+                st_stream(P.odu + o, tv);
             }
+            __syncthreads();  // every thread is done with stage s
+            if (tid == 0) issue(q * KC + kk + S);
         }
-        const int s = j % S;
-        mbar_wait(&bar[s], (j / S) & 1);
-        const unsigned char* st = sm + size_t(s) * P.stage_bytes;
-        const T* du0 = reinterpret_cast<const T*>(st);
-        const T* du1 = reinterpret_cast<const T*>(st + P.dub);
-        const T* la0 = reinterpret_cast<const T*>(st + 2 * P.dub);
-        const T* la1 = reinterpret_cast<const T*>(st + 3 * P.dub);
-        const T* u0 = reinterpret_cast<const T*>(st + 4 * P.dub);
-        const T* u1 = reinterpret_cast<const T*>(st + 4 * P.dub + P.ub);
+        // fold this chunk into the tile's running ds sum, in source order
+        if (tid == 0 && c > 0 && !P.nofold)
+            while (ld_acquire(P.flags + t) != P.base + unsigned(c)) __nanosleep(64);
+        __syncthreads();
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             if (!act[r]) continue;
-            const int row = zs + 4 * r;  // smem halo row = row + 1
-            auto at = [&](const T* b0, const T* b1, int col, int ri) -> T {
-                return col < BW ? b0[ri * BW + col] : b1[ri * BW + col - BW];
-            };
-            const int col = lx + 1;
-            T s_ = A::zero(), t_ = A::zero();
-            if (hN[r]) {
-                s_ = A::add(s_, A::mul(cN[r], at(du0, du1, col, row)));
-                t_ = A::add(t_, A::mulc(cN[r], at(la0, la1, col, row)));
-            }
-            if (hW[r]) {
-                s_ = A::add(s_, A::mul(cW[r], at(du0, du1, col - 1, row + 1)));
-                t_ = A::add(t_, A::mulc(cW[r], at(la0, la1, col - 1, row + 1)));
-            }
-            const T duc = at(du0, du1, col, row + 1);
-            const T lac = at(la0, la1, col, row + 1);
-            s_ = A::add(s_, A::mul(cD[r], duc));
-            t_ = A::add(t_, A::mulc(cD[r], lac));
-            if (hE[r]) {
-                s_ = A::add(s_, A::mul(cE[r], at(du0, du1, col + 1, row + 1)));
-                t_ = A::add(t_, A::mulc(cE[r], at(la0, la1, col + 1, row + 1)));
-            }
-            if (hS[r]) {
-                s_ = A::add(s_, A::mul(cS[r], at(du0, du1, col, row + 2)));
-                t_ = A::add(t_, A::mulc(cS[r], at(la0, la1, col, row + 2)));
-            }
-            const T uc = lx < BWU ? u0[row * BWU + lx] : u1[row * BWU + lx - BWU];
-            const int64_t o = int64_t(k) * P.n + cnode[r];
-            st_stream(P.ola + o, A::sub(s_, A::pmul(P.w2, uc, dsv[r])));
-            if (q[r] < qe[r] && P.nrec_k[q[r]] == k) {
-                T f = A::zero();
-                while (q[r] < qe[r] && P.nrec_k[q[r]] == k) {
-                    f = A::add(f, A::rm(R(P.nrec_w2[q[r]]), duc));
-                    ++q[r];
-                }
-                t_ = A::add(f, t_);
-            }
-            st_stream(P.odu + o, t_);
-            pl[r] = A::radd(pl[r], A::re_pconj(P.w2, uc, lac));
-            if (k == K - 1) P.ods[cnode[r]] = A::rsub(A::rmulr(P.eps, dsv[r]), pl[r]);
+            R pl = c > 0 ? __ldcg(P.ods + cnode[r]) : R(0);
+#pragma unroll
+            for (int kk = 0; kk < KC; ++kk) pl = A::radd(pl, terms[(kk * 2 + r) * kThreads + tid]);
+            P.ods[cnode[r]] = (c == P.C - 1) ? A::rsub(A::rmulr(P.eps, dsv[r]), pl) : pl;
         }
-        __syncthreads();  // every thread is done with stage s
-        if (tid == 0 && j + S < nsteps) issue(j + S);
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            st_release(P.flags + t, P.base + unsigned(c) + 1u);
+        }
+    }
+    // last CTA out resets the scheduler for the next launch
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(P.sched + 1, 1u) == gridDim.x - 1) {
+            P.sched[0] = 0u;
+            P.sched[1] = 0u;
+            __threadfence();
+        }
     }
 }
 
@@ -245,10 +353,12 @@ uint32_t align128(size_t b) { return uint32_t((b + 127) / 128 * 128); }
 
 struct KktPlan {
     bool ok = false;
-    int G = 0, BW = 0, BWU = 0, stages = 0;
+    int G = 0, T = 0, C = 0, KC = 0, RP = 0, UP = 0, stages = 0, gr = 2;
     uint32_t dub = 0, ub = 0, stage_bytes = 0, tx_bytes = 0;
+    unsigned epoch = 0;
     size_t smem = 0;
-    DevBuf<int4> regions;
+    DevBuf<int4> tiles;
+    DevBuf<unsigned> sched, flags;
     CUtensorMap tm_u;
 };
 
@@ -256,76 +366,118 @@ void kkt_plan_free(KktPlan* p) { delete p; }
 
 namespace {
 
-bool encode(CUtensorMap* tm, bool f32, const void* base, int nx, int nz, int K, int box_cplx, int box_rows) {
+CUtensorMapL2promotion l2promo() {
+    const char* e = std::getenv("FWI_KKT_L2PROMO");
+    if (!e) return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    const int v = std::atoi(e);
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+         : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
+// 4-D view of a source-major field: (complex pair, x/2, z, source). Each
+// element is 8 bytes: a double (complex128: 4 per pair) or a whole complex64
+// (2 per pair; the copy engine does not interpret the payload).
+bool encode(CUtensorMap* tm, bool f32, const void* base, int nx, int nz, int K, int gr, int box_pairs,
+            int box_rows) {
     auto fn = encode_fn();
     if (!fn) return false;
-    // complex128: two FLOAT64 elements per number; complex64: one 8-byte
-    // element per number (the copy engine does not interpret the payload)
-    const int cm = f32 ? 1 : 2;
-    cuuint64_t dims[3] = {cuuint64_t(cm) * nx, cuuint64_t(nz), cuuint64_t(K)};
-    cuuint64_t strides[2] = {cuuint64_t(nx) * (f32 ? 8 : 16), cuuint64_t(nx) * nz * (f32 ? 8 : 16)};
-    cuuint32_t box[3] = {cuuint32_t(cm * box_cplx), cuuint32_t(box_rows), 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = fn(tm, f32 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+    const cuuint64_t e = cuuint64_t(gr) * (f32 ? 1 : 2);  // 8-byte elements per group
+    const cuuint64_t cb = f32 ? 8 : 16;  // bytes per complex
+    cuuint64_t dims[4] = {e, cuuint64_t(nx / gr), cuuint64_t(nz), cuuint64_t(K)};
+    cuuint64_t strides[3] = {cuuint64_t(gr) * cb, cuuint64_t(nx) * cb, cuuint64_t(nx) * nz * cb};
+    cuuint32_t box[4] = {cuuint32_t(e), cuuint32_t(box_pairs), cuuint32_t(box_rows), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = fn(tm, f32 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
                           const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, l2promo(),
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
+template <class A, int KC, int S>
+void set_smem(size_t smem) {
+    static size_t smem_set = 0;  // per-kernel, process-wide attribute: only ever raise it
+    if (smem > smem_set) {
+        CK(cudaFuncSetAttribute(kkt_tma_kernel<A, KC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(smem)));
+        smem_set = smem;
+    }
+}
+
+// (KC, S) instantiations: KC in {1,2,4,8}, S in {1,2,4} with S | KC and S <= KC
+#define FWI_KKT_DISPATCH(KCv, Sv, CALL)                      \
+    switch (KCv * 16 + Sv) {                                 \
+        case 1 * 16 + 1: CALL(1, 1); break;                  \
+        case 2 * 16 + 2: CALL(2, 2); break;                  \
+        case 4 * 16 + 2: CALL(4, 2); break;                  \
+        case 4 * 16 + 4: CALL(4, 4); break;                  \
+        case 8 * 16 + 2: CALL(8, 2); break;                  \
+        default: CALL(8, 4); break;                          \
+    }
+
 template <class A>
 KktPlan* build_plan(Ctx& c, bool f32) {
     auto p = std::make_unique<KktPlan>();
-    const int nx = c.nx, nz = c.nz;
+    const int nx = c.nx, nz = c.nz, K = c.K;
     const int es = f32 ? 8 : 16;  // bytes per complex
-    // TMA constraints: 16-byte global strides, 16-byte box rows
-    if ((int64_t(2) * nx * (es / 2)) % 16 != 0) return p.release();
+    if (nx % 2 != 0) return p.release();  // pair view needs an even row length
     if (!encode_fn()) return p.release();
     const int nsx = (nx + kCols - 1) / kCols;
-    const int W = (nx + nsx - 1) / nsx;
-    int BW = (W + 2 + 1) / 2, BWU = (W + 1) / 2;
-    if (f32) {  // box rows must be multiples of 16 bytes
-        BW = (BW + 1) / 2 * 2;
-        BWU = (BWU + 1) / 2 * 2;
-    }
-    // regions: distribute the SMs over the strips in proportion to their width,
-    // then split each strip's rows evenly among its bands
-    const int G0 = sm_count();
-    std::vector<int4> regs;
-    int given = 0;
-    for (int sidx = 0; sidx < nsx; ++sidx) {
-        const int x0 = sidx * W, ws = std::min(W, nx - x0);
-        int bands = (sidx == nsx - 1) ? G0 - given
-                                      : int(std::lround(double(G0) * (x0 + ws) / nx)) - given;
-        bands = std::max(1, std::min(bands, nz));
-        given += bands;
-        for (int b = 0; b < bands; ++b) {
-            const int za = int(int64_t(nz) * b / bands), zb = int(int64_t(nz) * (b + 1) / bands);
-            if (zb > za) regs.push_back(make_int4(x0, ws, za, zb - za));
+    const int W = ((nx + nsx - 1) / nsx + 1) / 2 * 2;  // even strip width <= 128
+    // innermost TMA element group: 8 complex (128 B for complex128) measured
+    // best on B200 (request size vs. halo width); 2 as the general fallback
+    int gr = 8;
+    if (const char* e = std::getenv("FWI_KKT_GRP")) gr = std::max(1, std::atoi(e));
+    if (nx % gr != 0 || W % gr != 0) gr = 2;
+    const int RP = W + 2 * gr, UP = W;  // halo row: x0-gr .. x0+W+gr-1
+    p->gr = gr;
+    // tiles of <= 128 x 8 nodes, row-block major
+    std::vector<int4> tiles;
+    for (int z0 = 0; z0 < nz; z0 += kRows)
+        for (int sx = 0; sx < nsx; ++sx) {
+            const int x0 = sx * W;
+            tiles.push_back(make_int4(x0, std::min(W, nx - x0), z0, std::min(kRows, nz - z0)));
         }
+    p->T = int(tiles.size());
+    // K-chunk per unit: enough units (~12 per SM) for dynamic balance; a power
+    // of two dividing K
+    const int G0 = sm_count();
+    int kc = 8;
+    while (kc > 1 && (K % kc != 0 || int64_t(p->T) * (K / kc) < int64_t(4) * G0)) kc /= 2;
+    if (const char* e = std::getenv("FWI_KKT_KC")) {
+        const int v = std::atoi(e);
+        if ((v == 1 || v == 2 || v == 4 || v == 8) && K % v == 0) kc = v;
     }
-    p->G = int(regs.size());
-    p->regions.alloc(regs.size());
-    CK(cudaMemcpy(p->regions.p, regs.data(), regs.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    p->BW = BW;
-    p->BWU = BWU;
-    p->dub = align128(size_t(BW) * kBH * es);
-    p->ub = align128(size_t(BWU) * kRows * es);
-    p->stage_bytes = 4 * p->dub + 2 * p->ub;
-    p->tx_bytes = uint32_t(4 * size_t(BW) * kBH * es + 2 * size_t(BWU) * kRows * es);
-    const size_t budget = 227 * 1024 - 256;
-    p->stages = int(std::min<size_t>(kMaxStages, budget / p->stage_bytes));
-    if (const char* e = std::getenv("FWI_KKT_STAGES")) p->stages = std::min(p->stages, std::max(1, std::atoi(e)));
-    if (p->stages < 2) return p.release();
-    p->smem = size_t(p->stages) * p->stage_bytes + kMaxStages * sizeof(uint64_t);
-    // the attribute is per kernel and process-wide: only ever raise it
-    static size_t smem_set = 0;
-    if (p->smem > smem_set) {
-        CK(cudaFuncSetAttribute(kkt_tma_kernel<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)));
-        smem_set = p->smem;
-    }
+    p->KC = kc;
+    p->C = K / kc;
+    p->G = int(std::min<int64_t>(G0, int64_t(p->T) * p->C));
+    p->tiles.alloc(tiles.size());
+    CK(cudaMemcpy(p->tiles.p, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    p->sched.alloc(2);
+    p->flags.alloc(tiles.size());
+    CK(cudaMemset(p->sched.p, 0, 2 * sizeof(unsigned)));
+    CK(cudaMemset(p->flags.p, 0, tiles.size() * sizeof(unsigned)));
+    p->RP = RP;
+    p->UP = UP;
+    p->dub = align128(size_t(RP) * kBH * es);
+    p->ub = align128(size_t(UP) * kRows * es);
+    p->stage_bytes = 2 * p->dub + p->ub;
+    p->tx_bytes = uint32_t(2 * size_t(RP) * kBH * es + size_t(UP) * kRows * es);
+    const size_t tail = 128 + size_t(kc) * 2 * kThreads * (f32 ? 4 : 8);  // mbarriers, unit ring, terms
+    const size_t budget = 227 * 1024 - tail;
+    // four stages when they fit and divide the chunk, else two
+    int st = 4;
+    if (const char* e = std::getenv("FWI_KKT_STAGES")) st = std::atoi(e) >= 4 ? 4 : 2;
+    while (st > 1 && (size_t(st) * p->stage_bytes > budget || kc % st != 0)) st /= 2;
+    if (kc == 1) st = 1;
+    p->stages = st;
+    if (size_t(st) * p->stage_bytes > budget) return p.release();
+    p->smem = size_t(p->stages) * p->stage_bytes + tail;
+#define FWI_SET(KCc, Sc) set_smem<A, KCc, Sc>(p->smem)
+    FWI_KKT_DISPATCH(kc, st, FWI_SET)
+#undef FWI_SET
     const void* ubase = f32 ? static_cast<const void*>(c.u32.p) : static_cast<const void*>(c.u.p);
-    if (!ubase || !encode(&p->tm_u, f32, ubase, nx, nz, c.K, BWU, kRows)) return p.release();
+    if (!ubase || !encode(&p->tm_u, f32, ubase, nx, nz, K, gr, UP / gr, kRows)) return p.release();
     p->ok = true;
     return p.release();
 }
@@ -334,8 +486,8 @@ template <class A>
 bool launch(Ctx& c, KktPlan* p, const typename A::T* du, const typename A::R* ds, const typename A::T* la,
             typename A::T* odu, typename A::R* ods, typename A::T* ola, bool f32) {
     CUtensorMap tdu, tla;
-    if (!encode(&tdu, f32, du, c.nx, c.nz, c.K, p->BW, kBH)) return false;
-    if (!encode(&tla, f32, la, c.nx, c.nz, c.K, p->BW, kBH)) return false;
+    if (!encode(&tdu, f32, du, c.nx, c.nz, c.K, p->gr, p->RP / p->gr, kBH)) return false;
+    if (!encode(&tla, f32, la, c.nx, c.nz, c.K, p->gr, p->RP / p->gr, kBH)) return false;
     TmaArgs<A> a;
     a.nx = c.nx;
     a.nz = c.nz;
@@ -359,16 +511,30 @@ bool launch(Ctx& c, KktPlan* p, const typename A::T* du, const typename A::R* ds
     a.odu = odu;
     a.ola = ola;
     a.ods = ods;
-    a.regions = p->regions.p;
-    a.BW = p->BW;
-    a.BWU = p->BWU;
+    a.tiles = p->tiles.p;
+    a.T_ = p->T;
+    a.C = p->C;
+    a.sched = p->sched.p;
+    a.flags = p->flags.p;
+    ++p->epoch;
+    a.base = p->epoch * unsigned(p->C);
+    a.RP = p->RP;
+    a.UP = p->UP;
     a.stages = p->stages;
-    a.cm = f32 ? 1 : 2;
+    a.memonly = std::getenv("FWI_KKT_MEMONLY") ? 1 : 0;
+    a.nofold = std::getenv("FWI_KKT_NOFOLD") ? 1 : 0;
+    a.nostore = std::getenv("FWI_KKT_NOSTORE") ? 1 : 0;
+    a.nou = std::getenv("FWI_KKT_NOU") ? 1 : 0;
+    a.ub_bytes = uint32_t(size_t(p->UP) * kRows * (f32 ? 8 : 16));
+    a.gr = p->gr;
     a.dub = p->dub;
     a.ub = p->ub;
     a.stage_bytes = p->stage_bytes;
     a.tx_bytes = p->tx_bytes;
-    kkt_tma_kernel<A><<<p->G, kThreads, p->smem, c.stream>>>(tdu, tla, p->tm_u, a);
+#define FWI_LAUNCH(KCc, Sc) \
+    kkt_tma_kernel<A, KCc, Sc><<<p->G, kThreads, p->smem, c.stream>>>(tdu, tla, p->tm_u, a)
+    FWI_KKT_DISPATCH(p->KC, p->stages, FWI_LAUNCH)
+#undef FWI_LAUNCH
     CK_LAUNCH();
     return true;
 }
@@ -376,12 +542,15 @@ bool launch(Ctx& c, KktPlan* p, const typename A::T* du, const typename A::R* ds
 }  // namespace
 
 // Returns false when the TMA path does not apply (the caller then runs the
-// plain kernel of kkt.cu).
+// plain kernel of kkt.cu): small problems (the single-pass plain kernel wins
+// when everything is L2-resident) and layouts TMA cannot describe.
 bool kkt_apply_tma(Ctx& c, bool f32, const void* xi, void* out) {
-    // The complex64 instantiation faults (illegal instruction) as soon as more
-    // than one pipeline stage is in flight; until that is understood the
-    // complex64 apply runs the plain kernel (FWI_KKT_F32_TMA=1 re-enables it).
-    if (f32 && !std::getenv("FWI_KKT_F32_TMA")) return false;
+    // (FWI_KKT_F32_TMA=0 keeps the complex64 apply on the plain kernel)
+    if (f32) {
+        const char* e = std::getenv("FWI_KKT_F32_TMA");
+        if (e && std::atoi(e) == 0) return false;
+    }
+    if (int64_t(c.K) * c.n < (int64_t(1) << 21) && !std::getenv("FWI_KKT_FORCE_TMA")) return false;
     KktPlan*& p = c.kplan[f32 ? 1 : 0];
     if (!p) p = f32 ? build_plan<F32>(c, true) : build_plan<F64>(c, false);
     if (!p->ok) return false;
