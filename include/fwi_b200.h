@@ -203,6 +203,11 @@ int fwi_dev_vec_device_ptr(const fwi_dev_vec* v, void** out);
 
 /* ---- the hot path ------------------------------------------------------- */
 int fwi_dev_kkt_apply(fwi_dev_ctx* ctx, const fwi_dev_vec* xi, fwi_dev_vec* out);
+/* kkt_apply on HOST flat buffers (4Kn+n doubles each), the reference's own
+ * value-in/value-out signature: source chunks stream H2D, are applied as they
+ * land and stream back D2H on separate copy engines. Pinned host memory
+ * (fwi_host_register) gives full PCIe rate. Bit-identical to fwi_dev_kkt_apply. */
+int fwi_dev_kkt_apply_host(fwi_dev_ctx* ctx, const double* xi_host, double* out_host);
 int fwi_dev_kkt_rhs(fwi_dev_ctx* ctx, fwi_dev_vec* out);
 int fwi_dev_precond_apply(fwi_dev_ctx* ctx, int mode, const fwi_dev_vec* v, fwi_dev_vec* out);
 /* fsgn_gmres_step: returns delta_s (n doubles) and the convergence log. */

@@ -127,6 +127,7 @@ def lib() -> C.CDLL:
                 "fwi_dev_vec_device_ptr": [_vp, C.POINTER(_vp)],
                 "fwi_dev_kkt_apply": [_vp, _vp, _vp],
                 "fwi_dev_kkt_rhs": [_vp, _vp],
+                "fwi_dev_kkt_apply_host": [_vp, _dp, _dp],
                 "fwi_dev_precond_apply": [_vp, C.c_int, _vp, _vp],
                 "fwi_dev_fsgn_gmres_step": [_vp, C.c_void_p, _dp, C.c_void_p],
                 "fwi_dev_gmres_generic": [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, _vp, _vp, _vp,
@@ -363,6 +364,15 @@ def scal(a: float, x: KktVector) -> None:
 def kkt_apply(state: GnState, xi: KktVector, out: KktVector | None = None) -> KktVector:
     out = KktVector(state, xi.precision) if out is None else out
     _check(lib().fwi_dev_kkt_apply(state.h, xi.h, out.h))
+    return out
+
+
+def kkt_apply_host(state: GnState, xi: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+    """kkt_apply on host arrays (flat 4Kn+n doubles), streamed through the GPU
+    with copy/compute overlap (fwi_dev_kkt_apply_host)."""
+    xi = np.ascontiguousarray(xi, np.float64)
+    out = np.empty(state.vec_len) if out is None else out
+    _check(lib().fwi_dev_kkt_apply_host(state.h, _p(xi), _p(out)))
     return out
 
 

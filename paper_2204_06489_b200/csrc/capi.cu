@@ -365,6 +365,15 @@ int fwi_dev_kkt_apply(fwi_dev_ctx* ctx, const fwi_dev_vec* xi, fwi_dev_vec* out)
     });
 }
 
+int fwi_dev_kkt_apply_host(fwi_dev_ctx* ctx, const double* xi_host, double* out_host) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(xi_host, "xi");
+        need(out_host, "out");
+        kkt_apply_host(*ctx->c, xi_host, out_host);
+    });
+}
+
 int fwi_dev_kkt_rhs(fwi_dev_ctx* ctx, fwi_dev_vec* out) {
     return guard([&] {
         need(ctx, "ctx");

@@ -101,6 +101,12 @@ Ctx::~Ctx() {
     if (ilu) ilu_free(ilu);
     for (auto*& p : kplan)
         if (p) kkt_plan_free(p);
+    for (auto& e : ev_in)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : ev_out)
+        if (e) cudaEventDestroy(e);
+    if (s_h2d) cudaStreamDestroy(s_h2d);
+    if (s_d2h) cudaStreamDestroy(s_d2h);
     if (stream) cudaStreamDestroy(stream);
 }
 

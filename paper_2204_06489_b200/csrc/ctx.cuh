@@ -67,6 +67,11 @@ struct Ctx {
     DevBuf<double> red_out;       // scalar results
     DevBuf<double2> work_a, work_b, work_c;  // K*n complex scratch (precond)
     DevBuf<double> work_ds;
+    // pipelined host-buffer apply (kkt_apply_host)
+    static constexpr int kMaxChunks = 16;
+    DevBuf<double> hx, hy, hpl;
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_in[kMaxChunks] = {}, ev_out[kMaxChunks] = {};
 
     ~Ctx();
     double2* du_of(double* base) const { return reinterpret_cast<double2*>(base); }
@@ -94,6 +99,7 @@ void kkt_apply(Ctx& c, const Vec& xi, Vec& out);
 void kkt_rhs(Ctx& c, Vec& out);
 void kkt_apply_raw(Ctx& c, const double* xi, double* out);  // c128 flat device buffers
 bool kkt_apply_tma(Ctx& c, bool f32, const void* xi, void* out);
+void kkt_apply_host(Ctx& c, const double* in, double* out);
 void kkt_plan_free(KktPlan*);
 
 // ---- vec.cu  (flat device arrays of len doubles; deterministic reductions)

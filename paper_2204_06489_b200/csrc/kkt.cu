@@ -21,6 +21,8 @@
 #include "arith.cuh"
 #include "ctx.cuh"
 
+#include <algorithm>
+
 namespace fwi_b200 {
 
 namespace {
@@ -33,7 +35,11 @@ __global__ void __launch_bounds__(256) kkt_apply_kernel(
     const int* __restrict__ nrec_ptr, const int* __restrict__ nrec_k,
     const double* __restrict__ nrec_w2, const typename A::T* __restrict__ du,
     const typename A::R* __restrict__ ds, const typename A::T* __restrict__ la,
-    typename A::T* __restrict__ odu, typename A::R* __restrict__ ods, typename A::T* __restrict__ ola) {
+    typename A::T* __restrict__ odu, typename A::R* __restrict__ ods, typename A::T* __restrict__ ola,
+    int k0, int k1, typename A::R* __restrict__ plbuf) {
+    // Sources [k0, k1) only (the pipelined host-buffer apply streams source
+    // chunks); the ds row's running sum continues from plbuf when k0 > 0 and
+    // is written back to plbuf unless the chunk ends at K.
     using T = typename A::T;
     using R = typename A::R;
     const int ix = blockIdx.x * blockDim.x + threadIdx.x;
@@ -53,8 +59,9 @@ __global__ void __launch_bounds__(256) kkt_apply_kernel(
     const R dsv = ds[c];
     int q = nrec_ptr[c];
     const int qe = nrec_ptr[c + 1];
-    R pl = R(0);
-    for (int k = 0; k < K; ++k) {
+    while (q < qe && nrec_k[q] < k0) ++q;
+    R pl = k0 > 0 ? plbuf[c] : R(0);
+    for (int k = k0; k < k1; ++k) {
         const int64_t o = int64_t(k) * n + c;
         // row 3: A du - P ds (ascending column order: -nx, -1, 0, +1, +nx)
         T s = A::zero();
@@ -94,7 +101,10 @@ __global__ void __launch_bounds__(256) kkt_apply_kernel(
         // row 2 partial sum, sources in order
         pl = A::radd(pl, A::re_pconj(w2, uc, lac));
     }
-    ods[c] = A::rsub(A::rmulr(eps, dsv), pl);
+    if (k1 == K)
+        ods[c] = A::rsub(A::rmulr(eps, dsv), pl);
+    else
+        plbuf[c] = pl;
 }
 
 // kkt_rhs (src/kkt.cpp:98-112): b = (Q^H W^T W r scattered per source,
@@ -128,8 +138,61 @@ void kkt_apply_raw(Ctx& c, const double* xi, double* out) {
     kkt_apply_kernel<F64><<<grd, blk, 0, c.stream>>>(
         c.nx, c.nz, c.K, c.n, c.w2, c.eps, c.diag.p, c.east.p, c.south.p, c.u.p, c.nrec_ptr.p,
         c.nrec_k.p, c.nrec_w2.p, c.du_of(x), c.ds_of(x), c.la_of(x), c.du_of(out), c.ds_of(out),
-        c.la_of(out));
+        c.la_of(out), 0, c.K, nullptr);
     CK_LAUNCH();
+}
+
+// kkt_apply on host buffers (the reference's own signature,
+// src/kkt.cpp:78): the flat input is streamed in source chunks on one copy
+// stream, each chunk is applied as soon as it lands, and its output block
+// streams back on a second copy stream, so H2D, compute and D2H overlap. The
+// ds row's K-sum is carried across chunks in source order (bit-exact).
+void kkt_apply_host(Ctx& c, const double* in, double* out) {
+    const int K = c.K;
+    const int64_t n = c.n, kn2 = 2 * int64_t(K) * n;
+    if (!c.hx.p) {
+        c.hx.alloc(c.vec_len);
+        c.hy.alloc(c.vec_len);
+        c.hpl.alloc(c.ds_stride);
+        CK(cudaMemset(c.hx.p, 0, c.hx.bytes()));
+        CK(cudaMemset(c.hy.p, 0, c.hy.bytes()));
+        CK(cudaStreamCreateWithFlags(&c.s_h2d, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c.s_d2h, cudaStreamNonBlocking));
+        for (int i = 0; i < Ctx::kMaxChunks; ++i) {
+            CK(cudaEventCreateWithFlags(&c.ev_in[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c.ev_out[i], cudaEventDisableTiming));
+        }
+    }
+    const int nch = std::min(K, Ctx::kMaxChunks);
+    double* x = c.hx.p;
+    double* y = c.hy.p;
+    const size_t cb = sizeof(double2);
+    const int64_t dev_la = kn2 + c.ds_stride, host_la = kn2 + n;
+    // the previous call's D2H must be done before this call reuses y (stream order)
+    CK(cudaMemcpyAsync(c.ds_of(x), in + kn2, n * sizeof(double), cudaMemcpyHostToDevice, c.s_h2d));
+    dim3 blk(32, 8), grd((c.nx + 31) / 32, (c.nz + 7) / 8);
+    for (int ch = 0; ch < nch; ++ch) {
+        const int k0 = int(int64_t(K) * ch / nch), k1 = int(int64_t(K) * (ch + 1) / nch);
+        const size_t off = size_t(k0) * n, cnt = size_t(k1 - k0) * n;
+        CK(cudaMemcpyAsync(c.du_of(x) + off, in + 2 * off, cnt * cb, cudaMemcpyHostToDevice, c.s_h2d));
+        CK(cudaMemcpyAsync(c.la_of(x) + off, in + host_la + 2 * off, cnt * cb, cudaMemcpyHostToDevice,
+                           c.s_h2d));
+        CK(cudaEventRecord(c.ev_in[ch], c.s_h2d));
+        CK(cudaStreamWaitEvent(c.stream, c.ev_in[ch], 0));
+        kkt_apply_kernel<F64><<<grd, blk, 0, c.stream>>>(
+            c.nx, c.nz, K, n, c.w2, c.eps, c.diag.p, c.east.p, c.south.p, c.u.p, c.nrec_ptr.p, c.nrec_k.p,
+            c.nrec_w2.p, c.du_of(x), c.ds_of(x), c.la_of(x), c.du_of(y), c.ds_of(y), c.la_of(y), k0, k1,
+            c.hpl.p);
+        CK_LAUNCH();
+        CK(cudaEventRecord(c.ev_out[ch], c.stream));
+        CK(cudaStreamWaitEvent(c.s_d2h, c.ev_out[ch], 0));
+        CK(cudaMemcpyAsync(out + 2 * off, c.du_of(y) + off, cnt * cb, cudaMemcpyDeviceToHost, c.s_d2h));
+        CK(cudaMemcpyAsync(out + host_la + 2 * off, c.la_of(y) + off, cnt * cb, cudaMemcpyDeviceToHost,
+                           c.s_d2h));
+    }
+    CK(cudaMemcpyAsync(out + kn2, c.ds_of(y), n * sizeof(double), cudaMemcpyDeviceToHost, c.s_d2h));
+    CK(cudaStreamSynchronize(c.s_d2h));
+    (void)dev_la;
 }
 
 void kkt_apply(Ctx& c, const Vec& xi, Vec& out) {
@@ -150,7 +213,7 @@ void kkt_apply(Ctx& c, const Vec& xi, Vec& out) {
         c.nx, c.nz, c.K, c.n, float(c.w2), float(c.eps), c.diag32.p, c.east32.p, c.south32.p,
         c.u32.p, c.nrec_ptr.p, c.nrec_k.p, c.nrec_w2.p, reinterpret_cast<float2*>(x), x + kn2,
         reinterpret_cast<float2*>(x + kn2 + c.ds_stride), reinterpret_cast<float2*>(o), o + kn2,
-        reinterpret_cast<float2*>(o + kn2 + c.ds_stride));
+        reinterpret_cast<float2*>(o + kn2 + c.ds_stride), 0, c.K, nullptr);
     CK_LAUNCH();
 }
 

@@ -334,3 +334,13 @@ def test_invalid_arguments_raise():
     bad.epsilon = 0.0
     with pytest.raises(fw.InvalidArgument):
         fw.GnState(bad)
+
+
+@pytest.mark.parametrize("mk", [lambda: small_problem(), lambda: c2_problem(K=11, R=9)])
+def test_kkt_apply_host_pipelined_bit_exact(mk):
+    """fwi_dev_kkt_apply_host (chunked H2D/compute/D2H) equals the reference."""
+    p = mk()
+    ref, dev = pair_direct(p)
+    for seed in (3, 4):
+        x = random_kkt(p, seed)
+        assert np.array_equal(fw.kkt_apply_host(dev, x), ref.kkt_apply(x))
