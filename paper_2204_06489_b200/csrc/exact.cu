@@ -22,6 +22,7 @@
 // A^{-H} b = conj(A^{-1} conj(b)). Storage: L * nb^2 complex128
 // (C1: 8.4 MB, C3: 100 MB, C5: 34 GB), read twice per solve.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ctx.cuh"
 
@@ -30,14 +31,16 @@ namespace fwi_b200 {
 struct ExactFactor {
     int L = 0, nb = 0;
     bool col_lines = true;  // lines are grid columns (fixed ix) when nz <= nx
-    DevBuf<double2> GT;     // L x nb x nb, GT[i][j][m] = G_i[m][j]
+    int gp = 0;             // row pitch of G (nb + 1: padded against smem bank conflicts)
+    DevBuf<double2> G;      // L x nb x gp, G[i][m][j] = (S_i^{-1})[m][j]
     DevBuf<double2> coup;   // L x nb, coupling line i -> i+1 at position m
     DevBuf<double2> work;   // nb x nb scratch (global-memory inversion)
+    DevBuf<double2> ybuf;   // forward-sweep results of the cluster sweep
     DevBuf<int> status;
 };
 
 void exact_free(ExactFactor* f) { delete f; }
-int64_t exact_bytes(const ExactFactor* f) { return f ? int64_t(f->GT.bytes() + f->coup.bytes()) : 0; }
+int64_t exact_bytes(const ExactFactor* f) { return f ? int64_t(f->G.bytes() + f->coup.bytes()) : 0; }
 
 namespace {
 
@@ -68,7 +71,7 @@ template <bool SMEM>
 __global__ void __launch_bounds__(512) line_factor_kernel(
     bool col_lines, int nx, int nb, int line, const double2* __restrict__ diag,
     const double2* __restrict__ east, const double2* __restrict__ south,
-    const double2* __restrict__ coup, const double2* __restrict__ GTprev, double2* __restrict__ GTout,
+    const double2* __restrict__ coup, const double2* __restrict__ Gprev, double2* __restrict__ Gout, int gp,
     double2* gwork, int* status) {
     extern __shared__ double2 dsm[];
     double2* prow = dsm;
@@ -83,23 +86,24 @@ __global__ void __launch_bounds__(512) line_factor_kernel(
     const int64_t nn = int64_t(nb) * nb;
 
     // ---- S_i = T_i - E_{i-1} G_{i-1} E_{i-1}
-    for (int64_t t = tid; t < nn; t += nt) {
-        const int a = int(t / nb), b = int(t % nb);
-        double2 v = make_double2(0.0, 0.0);
-        const int64_t na = line_node(col_lines, nx, line, a);
-        if (a == b) v = diag[na];
-        else if (b == a + 1) v = col_lines ? south[na] : east[na];
-        else if (a == b + 1) v = col_lines ? south[line_node(col_lines, nx, line, b)]
-                                           : east[line_node(col_lines, nx, line, b)];
-        if (line > 0) {
-            const double2 ea = coup[int64_t(line - 1) * nb + a], eb = coup[int64_t(line - 1) * nb + b];
-            const double2 g = GTprev[int64_t(b) * nb + a];  // G_{i-1}[a][b]
-            const double2 t2 = fmul(fmul(ea, g), eb);
-            v.x -= t2.x;
-            v.y -= t2.y;
+    const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+    for (int a = wid; a < nb; a += nw)
+        for (int b = lane; b < nb; b += 32) {
+            double2 v = make_double2(0.0, 0.0);
+            const int64_t na = line_node(col_lines, nx, line, a);
+            if (a == b) v = diag[na];
+            else if (b == a + 1) v = col_lines ? south[na] : east[na];
+            else if (a == b + 1) v = col_lines ? south[line_node(col_lines, nx, line, b)]
+                                               : east[line_node(col_lines, nx, line, b)];
+            if (line > 0) {
+                const double2 ea = coup[int64_t(line - 1) * nb + a], eb = coup[int64_t(line - 1) * nb + b];
+                const double2 g = Gprev[int64_t(a) * gp + b];  // G_{i-1}[a][b]
+                const double2 t2 = fmul(fmul(ea, g), eb);
+                v.x -= t2.x;
+                v.y -= t2.y;
+            }
+            A[a * nb + b] = v;
         }
-        A[t] = v;
-    }
     __syncthreads();
 
     // ---- Gauss-Jordan inversion with row pivoting
@@ -154,15 +158,16 @@ __global__ void __launch_bounds__(512) line_factor_kernel(
             pcol[j] = (j == k) ? make_double2(0.0, 0.0) : A[int64_t(j) * nb + k];
         }
         __syncthreads();
-        for (int64_t t = tid; t < nn; t += nt) {
-            const int r = int(t / nb), j = int(t % nb);
+        for (int r = wid; r < nb; r += nw) {
             if (r == k) continue;
             const double2 f = pcol[r];
-            double2 v = (j == k) ? make_double2(0.0, 0.0) : A[t];
-            const double2 pr = prow[j];
-            v.x -= f.x * pr.x - f.y * pr.y;
-            v.y -= f.x * pr.y + f.y * pr.x;
-            A[t] = v;
+            for (int j = lane; j < nb; j += 32) {
+                double2 v = (j == k) ? make_double2(0.0, 0.0) : A[r * nb + j];
+                const double2 pr = prow[j];
+                v.x -= f.x * pr.x - f.y * pr.y;
+                v.y -= f.x * pr.y + f.y * pr.x;
+                A[r * nb + j] = v;
+            }
         }
         __syncthreads();
     }
@@ -177,11 +182,8 @@ __global__ void __launch_bounds__(512) line_factor_kernel(
             }
         __syncthreads();
     }
-    // GT[j][m] = G[m][j]
-    for (int64_t t = tid; t < nn; t += nt) {
-        const int m = int(t / nb), j = int(t % nb);
-        GTout[int64_t(j) * nb + m] = A[t];
-    }
+    for (int m = wid; m < nb; m += nw)
+        for (int j = lane; j < nb; j += 32) Gout[int64_t(m) * gp + j] = A[m * nb + j];
 }
 
 // source-major b_k[node]  ->  line-major W[i][k][m] (optionally conjugated)
@@ -257,7 +259,7 @@ __global__ void scatter_lines(bool col_lines, int nx, int nz, int L, int nb, int
 // dimension (S = 256/nb when nb <= 256), partial sums combined in fixed order.
 template <int KG>
 __global__ void __launch_bounds__(256) sweep_kernel(int L, int nb, int nrhs,
-                                                    const double2* __restrict__ GT,
+                                                    const double2* __restrict__ GT, int gp,
                                                     const double2* __restrict__ coup, double2* W) {
     extern __shared__ double2 sm[];
     double2* wv = sm;                 // KG x nb   operand
@@ -282,7 +284,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(int L, int nb, int nrhs,
             const int j0 = my_s * seg, j1 = min(nb, j0 + seg);
 #pragma unroll 4
             for (int j = j0; j < j1; ++j) {
-                const double2 g = __ldg(G + int64_t(j) * nb + m0);
+                const double2 g = __ldg(G + int64_t(m0) * gp + j);
 #pragma unroll
                 for (int k = 0; k < KG; ++k) {
                     const double2 w = wv[k * nb + j];
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(int L, int nb, int nrhs,
             wv[k * nb + m] = b;
         }
         __syncthreads();
-        matvec(GT + int64_t(i) * nn, false, i);
+        matvec(GT + int64_t(i) * nb * gp, false, i);
     }
     // backward: x_i = y_i - G_i E_i x_{i+1}; yv holds x_{i+1}
     for (int i = L - 2; i >= 0; --i) {
@@ -361,8 +363,295 @@ __global__ void __launch_bounds__(256) sweep_kernel(int L, int nb, int nrhs,
             yv[k * nb + m] = W[(int64_t(i) * nrhs + k0 + k) * nb + m];
         }
         __syncthreads();
-        matvec(GT + int64_t(i) * nn, true, i);
+        matvec(GT + int64_t(i) * nb * gp, true, i);
     }
+}
+
+// ---------------------------------------------------------------------------
+// Cluster sweep: one thread-block cluster of CS CTAs carries a group of KG
+// right-hand sides through all lines. CTA r owns rows [r*R, (r+1)*R) of every
+// G_i; per line it computes its slab of y_i = G_i w and pushes it into the
+// double-buffered full-vector copy of every CTA of the cluster through
+// distributed shared memory, followed by one cluster barrier. The next line's
+// G slab, coupling row and right-hand-side block are prefetched with bulk
+// async copies (cp.async.bulk + mbarrier) while the current line computes.
+// ---------------------------------------------------------------------------
+struct SweepArgs {
+    int L, nb, nrhs, gp, R;
+    const double2* G;
+    const double2* coup;
+    double2* W;   // line-major RHS in, solution out
+    double2* Y;   // line-major forward-sweep results (separate: W is still being read)
+    uint32_t off_e, off_b, stage_bytes, off_y, off_w, off_part, off_bar;
+    int nseg, nst;  // inner-dimension segments, pipeline stages (2..4)
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_init(uint64_t* b) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
+            smem_addr(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(b))
+                 : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t map_rank(uint32_t local_addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster(uint32_t addr, double2 v) {
+    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
+}
+// remote store that completes 16 bytes on the receiver's mbarrier (no fence)
+__device__ __forceinline__ void st_async16(uint32_t addr, double2 v, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(addr),
+                 "d"(v.x), "d"(v.y), "r"(remote_bar)
+                 : "memory");
+}
+
+template <int KG, int CS>
+__global__ void __launch_bounds__(256) sweep_cluster_kernel(const SweepArgs a) {
+    extern __shared__ __align__(128) unsigned char csm[];
+    const int tid = threadIdx.x;
+    const uint32_t rank = cluster_rank();
+    const int grp = blockIdx.x / CS;
+    const int nb = a.nb, L = a.L, R = a.R, gp = a.gp, nrhs = a.nrhs;
+    const int nbp = nb + 1;
+    const int k0 = grp * KG;
+    const int kc = min(KG, nrhs - k0);
+    const int r0 = int(rank) * R;
+    const int rows = max(0, min(nb, r0 + R) - r0);
+    double2* yfull = reinterpret_cast<double2*>(csm + a.off_y);  // [2][KG][nbp]
+    double2* wv = reinterpret_cast<double2*>(csm + a.off_w);     // [KG][nbp]
+    double2* part = reinterpret_cast<double2*>(csm + a.off_part);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(csm + a.off_bar);
+    const int O = R * KG;  // outputs (row, rhs) per CTA
+    const int nsteps = 2 * L - 1;
+
+    // step s: forward line s (s < L), backward line 2L-2-s (s >= L)
+    auto line_of = [&](int st) { return st < L ? st : 2 * L - 2 - st; };
+    auto issue = [&](int st) {
+        if (st >= nsteps) return;
+        const int sb = st % a.nst;
+        unsigned char* buf = csm + sb * a.stage_bytes;
+        const int i = line_of(st);
+        const bool fwd = st < L;
+        const uint32_t gbytes = uint32_t(rows) * gp * sizeof(double2);
+        const bool has_e = fwd ? i > 0 : true;
+        const uint32_t ebytes = has_e ? uint32_t(nb) * sizeof(double2) : 0u;
+        const uint32_t bbytes = fwd ? uint32_t(kc) * nb * sizeof(double2) : 0u;
+        bar_expect(&bar[sb], gbytes + ebytes + bbytes);
+        if (gbytes) bulk_g2s(buf, a.G + (int64_t(i) * nb + r0) * gp, gbytes, &bar[sb]);
+        if (ebytes) bulk_g2s(buf + a.off_e, a.coup + int64_t(fwd ? i - 1 : i) * nb, ebytes, &bar[sb]);
+        if (bbytes) bulk_g2s(buf + a.off_b, a.W + (int64_t(i) * nrhs + k0) * nb, bbytes, &bar[sb]);
+    };
+    uint64_t* rbar = bar + 4;  // receive barriers of the two y buffers
+    const uint32_t recv_bytes = uint32_t(kc) * nb * sizeof(double2);
+    if (tid == 0) {
+        for (int q = 0; q < a.nst; ++q) bar_init(&bar[q]);
+        bar_init(&rbar[0]);
+        bar_init(&rbar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int q = 0; q < a.nst; ++q) issue(q);
+    }
+    __syncthreads();
+    cluster_sync_all();  // peers' barriers are initialised before any remote arrive
+
+    for (int st = 0; st < nsteps; ++st) {
+        const int i = line_of(st);
+        const bool fwd = st < L;
+        const unsigned char* buf = csm + (st % a.nst) * a.stage_bytes;
+        const double2* Gs = reinterpret_cast<const double2*>(buf);
+        const double2* es = reinterpret_cast<const double2*>(buf + a.off_e);
+        const double2* bs = reinterpret_cast<const double2*>(buf + a.off_b);
+        bar_wait(&bar[st % a.nst], (st / a.nst) & 1);
+        // arm this step's receive buffer, then wait for all slabs of step st-1
+        if (tid == 0 && st + 1 < nsteps) bar_expect(&rbar[st & 1], recv_bytes);
+        if (st > 0) bar_wait(&rbar[(st - 1) & 1], ((st - 1) >> 1) & 1);
+        const double2* yprev = yfull + ((st + 1) & 1) * KG * nbp;  // written at step st-1
+        // w = b_i - E_{i-1} y_{i-1}  (forward)  |  w = E_i x_{i+1}  (backward)
+        for (int t = tid; t < KG * nb; t += blockDim.x) {
+            const int k = t / nb, m = t - k * nb;
+            double2 v = make_double2(0.0, 0.0);
+            if (k < kc) {
+                if (fwd) {
+                    v = bs[k * nb + m];
+                    if (i > 0) {
+                        const double2 e = es[m], y = yprev[k * nbp + m];
+                        v.x -= e.x * y.x - e.y * y.y;
+                        v.y -= e.x * y.y + e.y * y.x;
+                    }
+                } else {
+                    const double2 e = es[m], x = yprev[k * nbp + m];
+                    v = make_double2(e.x * x.x - e.y * x.y, e.x * x.y + e.y * x.x);
+                }
+            }
+            wv[k * nbp + m] = v;
+        }
+        __syncthreads();
+        // slab matvec: output o = (row, rhs), segments of the inner dimension
+        const int seglen = (nb + a.nseg - 1) / a.nseg;
+        for (int t = tid; t < O * a.nseg; t += blockDim.x) {
+            const int o = t % O, seg = t / O;
+            const int row = o / KG, k = o - row * KG;
+            double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+            if (row < rows) {
+                const double2* g = Gs + row * gp;
+                const double2* w = wv + k * nbp;
+                const int j0 = seg * seglen, j1 = min(nb, j0 + seglen);
+                int j = j0;
+                for (; j + 1 < j1; j += 2) {  // two independent accumulator chains
+                    const double2 g0 = g[j], x0 = w[j], g1 = g[j + 1], x1 = w[j + 1];
+                    acc.x += g0.x * x0.x - g0.y * x0.y;
+                    acc.y += g0.x * x0.y + g0.y * x0.x;
+                    acc2.x += g1.x * x1.x - g1.y * x1.y;
+                    acc2.y += g1.x * x1.y + g1.y * x1.x;
+                }
+                if (j < j1) {
+                    const double2 g0 = g[j], x0 = w[j];
+                    acc.x += g0.x * x0.x - g0.y * x0.y;
+                    acc.y += g0.x * x0.y + g0.y * x0.x;
+                }
+            }
+            part[seg * O + o] = make_double2(acc.x + acc2.x, acc.y + acc2.y);
+        }
+        __syncthreads();
+        double2* ynext_local = yfull + (st & 1) * KG * nbp;
+        for (int o = tid; o < O; o += blockDim.x) {
+            const int row = o / KG, k = o - row * KG;
+            if (row >= rows || k >= kc) continue;
+            double2 v = make_double2(0.0, 0.0);
+            for (int sg = 0; sg < a.nseg; ++sg) {
+                const double2 pv = part[sg * O + o];
+                v.x += pv.x;
+                v.y += pv.y;
+            }
+            const int64_t gi = (int64_t(i) * nrhs + k0 + k) * nb + r0 + row;
+            if (fwd) {
+                a.Y[gi] = v;
+            } else {
+                const double2 y = a.Y[gi];  // y_i from the forward sweep
+                v = make_double2(y.x - v.x, y.y - v.y);
+                a.W[gi] = v;
+            }
+            if (fwd && i == L - 1) a.W[gi] = v;  // x_{L-1} = y_{L-1}
+            if (st + 1 < nsteps) {  // the last step's slabs have no consumer
+                const uint32_t la = smem_addr(ynext_local + k * nbp + r0 + row);
+                const uint32_t lb = smem_addr(&rbar[st & 1]);
+#pragma unroll
+                for (int q = 0; q < CS; ++q) st_async16(map_rank(la, uint32_t(q)), v, map_rank(lb, uint32_t(q)));
+            }
+        }
+        __syncthreads();  // stage (st % nst) and the partials are free
+        if (tid == 0) issue(st + a.nst);
+    }
+    cluster_sync_all();  // no CTA leaves while peers may still address its shared memory
+}
+
+struct ClusterPlan {
+    bool ok = false;
+    int KG = 0, CS = 0, R = 0, nseg = 0;
+    SweepArgs a{};
+    size_t smem = 0;
+};
+
+template <int KG, int CS>
+bool cluster_launch(const ClusterPlan& cp, int nrhs, cudaStream_t st) {
+    static size_t set = 0;
+    if (cp.smem > set) {
+        if (cudaFuncSetAttribute(sweep_cluster_kernel<KG, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(cp.smem)) != cudaSuccess)
+            return false;
+        if (CS > 8 && cudaFuncSetAttribute(sweep_cluster_kernel<KG, CS>,
+                                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+            return false;
+        set = cp.smem;
+    }
+    const int groups = (nrhs + KG - 1) / KG;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(groups * CS);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = cp.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SweepArgs a = cp.a;
+    a.nrhs = nrhs;
+    CK(cudaLaunchKernelEx(&cfg, sweep_cluster_kernel<KG, CS>, a));
+    return true;
+}
+
+uint32_t al128(size_t b) { return uint32_t((b + 127) / 128 * 128); }
+
+// pick (KG, CS) whose shared-memory footprint fits; nb <= 256 only
+bool cluster_plan(int nb, int L, int gp, int nrhs, ClusterPlan& cp) {
+    const int cands[][2] = {{8, 8}, {4, 8}, {8, 16}, {4, 16}, {2, 16}, {1, 16}};
+    for (const auto& c : cands) {
+        const int KG = c[0], CS = c[1];
+        if (KG > 1 && nrhs < KG && KG != 8) continue;
+        const int R = (nb + CS - 1) / CS;
+        const int O = R * KG;
+        const int nseg = std::max(1, std::min(8, 256 / std::max(O, 1)));
+        SweepArgs a{};
+        a.L = L;
+        a.nb = nb;
+        a.gp = gp;
+        a.R = R;
+        a.nseg = nseg;
+        const size_t gbytes = size_t(R) * gp * sizeof(double2);
+        a.off_e = al128(gbytes);
+        a.off_b = a.off_e + al128(size_t(nb) * sizeof(double2));
+        a.stage_bytes = a.off_b + al128(size_t(KG) * nb * sizeof(double2));
+        const size_t rest = al128(size_t(2) * KG * (nb + 1) * sizeof(double2)) +
+                            al128(size_t(KG) * (nb + 1) * sizeof(double2)) +
+                            al128(size_t(nseg) * O * sizeof(double2)) + 128;
+        a.nst = 4;
+        while (a.nst > 2 && size_t(a.nst) * a.stage_bytes + rest > 220 * 1024) --a.nst;
+        a.off_y = a.nst * a.stage_bytes;
+        a.off_w = a.off_y + al128(size_t(2) * KG * (nb + 1) * sizeof(double2));
+        a.off_part = a.off_w + al128(size_t(KG) * (nb + 1) * sizeof(double2));
+        a.off_bar = a.off_part + al128(size_t(nseg) * O * sizeof(double2));
+        const size_t smem = a.off_bar + 128;
+        if (smem <= 220 * 1024) {
+            cp.ok = true;
+            cp.KG = KG;
+            cp.CS = CS;
+            cp.R = R;
+            cp.nseg = nseg;
+            cp.a = a;
+            cp.smem = smem;
+            return true;
+        }
+    }
+    return false;
 }
 
 constexpr int kSweepKG = 2;
@@ -381,7 +670,8 @@ void exact_factor(Ctx& c) {
     f->L = f->col_lines ? c.nx : c.nz;
     const int nb = f->nb, L = f->L;
     require(nb <= 2048, "exact block factorisation: line length above 2048 is not supported");
-    f->GT.alloc(size_t(L) * nb * nb);
+    f->gp = nb + 1;
+    f->G.alloc(size_t(L) * nb * f->gp);
     f->coup.alloc(size_t(L) * nb);
     f->status.alloc(1);
     CK(cudaMemsetAsync(f->status.p, 0, sizeof(int), c.stream));
@@ -399,15 +689,15 @@ void exact_factor(Ctx& c) {
         CK(cudaFuncSetAttribute(line_factor_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm)));
     const int64_t nn = int64_t(nb) * nb;
     for (int i = 0; i < L; ++i) {
-        const double2* prev = i > 0 ? f->GT.p + (i - 1) * nn : nullptr;
+        const double2* prev = i > 0 ? f->G.p + (i - 1) * int64_t(nb) * f->gp : nullptr;
         if (smem)
             line_factor_kernel<true><<<1, threads, shm, c.stream>>>(
                 f->col_lines, c.nx, nb, i, c.diag.p, c.east.p, c.south.p, f->coup.p, prev,
-                f->GT.p + i * nn, nullptr, f->status.p);
+                f->G.p + i * int64_t(nb) * f->gp, f->gp, nullptr, f->status.p);
         else
             line_factor_kernel<false><<<1, threads, shm, c.stream>>>(
                 f->col_lines, c.nx, nb, i, c.diag.p, c.east.p, c.south.p, f->coup.p, prev,
-                f->GT.p + i * nn, f->work.p, f->status.p);
+                f->G.p + i * int64_t(nb) * f->gp, f->gp, f->work.p, f->status.p);
         CK_LAUNCH();
     }
     int st = 0;
@@ -442,9 +732,31 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
                           : dim3((f.nb + 31) / 32, (f.L + 31) / 32, nrhs);
     gather_lines<<<tg, tb, 0, c.stream>>>(f.col_lines, c.nx, c.nz, f.L, f.nb, nrhs, adjoint, b, W);
     CK_LAUNCH();
-    sweep_kernel<kSweepKG><<<(nrhs + kSweepKG - 1) / kSweepKG, 256, sweep_smem(f.nb), c.stream>>>(
-        f.L, f.nb, nrhs, f.GT.p, f.coup.p, W);
-    CK_LAUNCH();
+    bool done = false;
+    if (!std::getenv("FWI_EXACT_LEGACY")) {
+        ClusterPlan cp;
+        if (cluster_plan(f.nb, f.L, f.gp, nrhs, cp)) {
+            cp.a.G = f.G.p;
+            cp.a.coup = f.coup.p;
+            cp.a.W = W;
+            if (f.ybuf.count < size_t(nrhs) * c.n) const_cast<ExactFactor&>(f).ybuf.alloc(size_t(nrhs) * c.n);
+            cp.a.Y = f.ybuf.p;
+            switch (cp.KG * 100 + cp.CS) {
+                case 808: done = cluster_launch<8, 8>(cp, nrhs, c.stream); break;
+                case 408: done = cluster_launch<4, 8>(cp, nrhs, c.stream); break;
+                case 816: done = cluster_launch<8, 16>(cp, nrhs, c.stream); break;
+                case 416: done = cluster_launch<4, 16>(cp, nrhs, c.stream); break;
+                case 216: done = cluster_launch<2, 16>(cp, nrhs, c.stream); break;
+                case 116: done = cluster_launch<1, 16>(cp, nrhs, c.stream); break;
+                default: break;
+            }
+        }
+    }
+    if (!done) {
+        sweep_kernel<kSweepKG><<<(nrhs + kSweepKG - 1) / kSweepKG, 256, sweep_smem(f.nb), c.stream>>>(
+            f.L, f.nb, nrhs, f.G.p, f.gp, f.coup.p, W);
+        CK_LAUNCH();
+    }
     scatter_lines<<<tg, tb, 0, c.stream>>>(f.col_lines, c.nx, c.nz, f.L, f.nb, nrhs, adjoint, W, x);
     CK_LAUNCH();
     c.solve_count[FWI_PRECOND_EXACT] += nrhs;
