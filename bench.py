@@ -217,15 +217,20 @@ def run_ours(args):
         s1 = fw.GnState(q, exact=True, ilu_level=4)
         for mode in (fw.PrecondMode.exact, fw.PrecondMode.ilu):
             fw.fsgn_gmres_step(s1, fw.FsgnOptions(mode=mode, tol=1e-3, maxit=3, ecg_stride=0))
-            t0 = time.perf_counter()
-            ds, log = fw.fsgn_gmres_step(s1, fw.FsgnOptions(mode=mode, restart=30, tol=1e-3, maxit=60,
-                                                            ecg_stride=0))
-            tw = time.perf_counter() - t0
+            runs = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                ds, log = fw.fsgn_gmres_step(s1, fw.FsgnOptions(mode=mode, restart=30, tol=1e-3, maxit=60,
+                                                                ecg_stride=0))
+                runs.append((log.entries[-1].wall_time, time.perf_counter() - t0, log))
+            runs.sort(key=lambda r: r[0])
+            wt, tw, log = runs[1]
             it = log.iterations()
-            krylov[mode.name] = {"iterations": it, "converged": log.converged,
+            krylov[mode.name] = {"config": "C1 128x64, K=8, 5 Hz, eps=1e10, tol 1e-3, restart 30, maxit 60",
+                                 "iterations": it, "converged": log.converged,
                                  "final_residual": log.final_residual(),
-                                 "iters_per_s": it / log.entries[-1].wall_time,
-                                 "step_wall_s": tw}
+                                 "iters_per_s": it / wt, "solve_wall_s": wt, "step_wall_s": tw,
+                                 "timing": "median of 3 solves, ConvergenceLog wall time"}
         s1.close()
 
     cpu = None

@@ -14,6 +14,7 @@
 // a group of sources, and each (row, source) item evaluates its row in the
 // reference's entry order (bit-faithful), with a CTA barrier between levels.
 #include <algorithm>
+#include <cstdlib>
 #include <complex>
 #include <queue>
 
@@ -26,7 +27,12 @@ using cplx = std::complex<double>;
 struct Sweep {          // one triangular sweep in CSR form + its level schedule
     DevBuf<int> ptr, idx, lvl_ptr, lvl_rows;
     DevBuf<double2> val;
+    // the same entries regrouped in level order: row lvl_rows[r] owns
+    // entries [rstart[r], rstart[r+1]) of (lidx, lval), in the row's own order
+    DevBuf<int> rstart, lidx;
+    DevBuf<double2> lval;
     int nlev = 0;
+    int ecap = 0, rcap = 0;  // max entries / rows of one level
 };
 
 struct IluFactor {
@@ -113,6 +119,32 @@ void upload_sweep(Sweep& s, int n, const std::vector<int>& ptr, const std::vecto
     up(s.idx, idx);
     up(s.lvl_ptr, lp);
     up(s.lvl_rows, rows);
+    {
+        std::vector<int> rst(n + 1, 0), li;
+        std::vector<cplx> lv;
+        li.reserve(idx.size());
+        lv.reserve(val.size());
+        for (int r = 0; r < n; ++r) {
+            const int i = rows[r];
+            for (int q = ptr[i]; q < ptr[i + 1]; ++q) {
+                li.push_back(idx[q]);
+                lv.push_back(val[q]);
+            }
+            rst[r + 1] = int(li.size());
+        }
+        up(s.rstart, rst);
+        s.ecap = s.rcap = 1;
+        for (int l = 0; l < s.nlev; ++l) {
+            s.rcap = std::max(s.rcap, lp[l + 1] - lp[l]);
+            s.ecap = std::max(s.ecap, rst[lp[l + 1]] - rst[lp[l]]);
+        }
+        s.ecap = (s.ecap + 1) / 2 * 2;
+        up(s.lidx, li);
+        s.lval.alloc(std::max<size_t>(lv.size(), 1));
+        if (!lv.empty())
+            CK(cudaMemcpyAsync(s.lval.p, lv.data(), lv.size() * sizeof(cplx), cudaMemcpyHostToDevice, st));
+        bytes += int64_t(lv.size() * sizeof(cplx));
+    }
     s.val.alloc(std::max<size_t>(val.size(), 1));
     if (!val.empty())
         CK(cudaMemcpyAsync(s.val.p, val.data(), val.size() * sizeof(cplx), cudaMemcpyHostToDevice, st));
@@ -185,8 +217,117 @@ __global__ void __launch_bounds__(256) ilu_sweep_kernel(int64_t n, int nrhs, int
     }
 }
 
+// Shared-memory variant (n * 16 B fits): one CTA per right-hand side keeps
+// its whole vector in shared memory. The rows of each level and their entries
+// are contiguous in the level-ordered arrays; they are staged into a ring of
+// shared-memory buffers with cp.async three levels ahead, so the dependency
+// chain of a level only touches shared memory.
+constexpr int kLvlBuf = 4;
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int* __restrict__ lvl_ptr,
+                                                     const int* __restrict__ lvl_rows,
+                                                     const int* __restrict__ rstart,
+                                                     const int* __restrict__ idx,
+                                                     const double2* __restrict__ val, double2* x, int ecap,
+                                                     int rcap) {
+    extern __shared__ __align__(16) double2 xs[];
+    double2* vb = xs + n;                                     // [kLvlBuf][ecap]
+    int* ib = reinterpret_cast<int*>(vb + size_t(kLvlBuf) * ecap);  // [kLvlBuf][ecap]
+    int* rib = ib + kLvlBuf * ecap;                           // [kLvlBuf][rcap] row ids
+    int* rpb = rib + kLvlBuf * rcap;                          // [kLvlBuf][rcap + 1] entry starts
+    double2* xk = x + int64_t(blockIdx.x) * n;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    auto prefetch = [&](int l) {
+        if (l < nlev) {
+            const int b = l % kLvlBuf;
+            const int r0 = lvl_ptr[l], r1 = lvl_ptr[l + 1];
+            const int e0 = rstart[r0], e1 = rstart[r1];
+            for (int t = tid; t < e1 - e0; t += nt) {
+                cp_async16(vb + b * ecap + t, val + e0 + t);
+                cp_async4(ib + b * ecap + t, idx + e0 + t);
+            }
+            for (int t = tid; t < r1 - r0; t += nt) cp_async4(rib + b * rcap + t, lvl_rows + r0 + t);
+            for (int t = tid; t <= r1 - r0; t += nt) cp_async4(rpb + b * (rcap + 1) + t, rstart + r0 + t);
+        }
+        cp_commit();  // (possibly empty) group per level keeps the counting uniform
+    };
+    for (int i = tid; i < n; i += nt) xs[i] = xk[i];
+#pragma unroll
+    for (int l = 0; l < kLvlBuf - 1; ++l) prefetch(l);
+    for (int l = 0; l < nlev; ++l) {
+        cp_wait<kLvlBuf - 2>();
+        __syncthreads();
+        const int b = l % kLvlBuf;
+        const int nrow = lvl_ptr[l + 1] - lvl_ptr[l];
+        const int* rp = rpb + b * (rcap + 1);
+        const int e0 = rp[0];
+        const double2* vl = vb + b * ecap;
+        const int* il = ib + b * ecap;
+        for (int t = tid; t < nrow; t += nt) {
+            const int i = rib[b * rcap + t];
+            const int p0 = rp[t] - e0, p1 = rp[t + 1] - e0;
+            double2 s = xs[i];
+            if (KIND == kLfwd || KIND == kLtbwd) {
+                for (int p = p0; p < p1; ++p) {
+                    const double2 xv = xs[il[p]];
+                    s = csub(s, KIND == kLfwd ? cmul(vl[p], xv) : cmulc(vl[p], xv));
+                }
+                xs[i] = s;
+            } else if (KIND == kUbwd) {
+                for (int p = p0 + 1; p < p1; ++p) s = csub(s, cmul(vl[p], xs[il[p]]));
+                xs[i] = cdiv(s, vl[p0]);
+            } else {
+                double2 dg = make_double2(0.0, 0.0);
+                for (int p = p0; p < p1; ++p) {
+                    const int k = il[p];
+                    if (k == i)
+                        dg = vl[p];
+                    else
+                        s = csub(s, cmulc(vl[p], xs[k]));
+                }
+                xs[i] = cdiv(s, make_double2(dg.x, -dg.y));
+            }
+        }
+        __syncthreads();
+        prefetch(l + kLvlBuf - 1);
+    }
+    cp_wait<0>();
+    for (int t = tid; t < n; t += nt) xk[t] = xs[t];
+}
+
 template <int KIND>
 void run_sweep(const Sweep& s, int64_t n, int nrhs, double2* x, cudaStream_t st) {
+    const size_t smem = size_t(n) * sizeof(double2) + size_t(kLvlBuf) * s.ecap * (sizeof(double2) + 4) +
+                        size_t(kLvlBuf) * (2 * s.rcap + 1) * 4 + 64;
+    if (smem <= 220 * 1024 && !std::getenv("FWI_ILU_GLOBAL")) {
+        static size_t set = 0;
+        if (smem > set) {
+            CK(cudaFuncSetAttribute(ilu_sweep_smem<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            set = smem;
+        }
+        ilu_sweep_smem<KIND><<<nrhs, 256, smem, st>>>(int(n), s.nlev, s.lvl_ptr.p, s.lvl_rows.p, s.rstart.p,
+                                                     s.lidx.p, s.lval.p, x, s.ecap, s.rcap);
+        CK_LAUNCH();
+        return;
+    }
     const int kg = 1;
     ilu_sweep_kernel<KIND><<<(nrhs + kg - 1) / kg, 256, 0, st>>>(n, nrhs, kg, s.nlev, s.lvl_ptr.p,
                                                                 s.lvl_rows.p, s.ptr.p, s.idx.p,
