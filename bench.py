@@ -126,6 +126,17 @@ def barrier_max(t, ws):
     return float(x.item())
 
 
+def barrier_max_cpu(t, ws):
+    """Max over ranks of a host time on an initialised (gloo) process group."""
+    if ws == 1:
+        return t
+    import torch
+    import torch.distributed as dist
+    x = torch.tensor([t], dtype=torch.float64)
+    dist.all_reduce(x, op=dist.ReduceOp.MAX)
+    return float(x.item())
+
+
 def load_traffic():
     try:
         with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
