@@ -1,0 +1,239 @@
+// fwi_b200/kkt.hpp — header-only C++ mirror of the reference's KKT/Krylov API
+// (namespace fwi in /root/reference/proj/include/fwi/{kkt,krylov,lu,ilu}.hpp)
+// on top of the plain C ABI in fwi_b200.h. Same names, argument meaning,
+// defaults and exception types; the objects live on the GPU.
+//
+//   reference (CPU)                          this header (B200)
+//   fwi::GnState  make_gn_state(...)         fwi::gpu::GnState(desc)
+//   fwi::KktVector                           fwi::gpu::KktVector (one flat device buffer)
+//   dot / norm / axpy / scal                 same names, same semantics
+//   kkt_apply(state, xi)                     kkt_apply(state, xi)
+//   kkt_rhs(state)                           kkt_rhs(state)
+//   precond_apply(state, v, mode)            precond_apply(state, v, mode)
+//   fsgn_gmres_step(state, options)          fsgn_gmres_step(state, options)
+//   SingularPivotError / ZeroPivotError      same, with .index
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "fwi_b200.h"
+
+namespace fwi::gpu {
+
+struct SingularPivotError : std::runtime_error {
+    int index;
+    SingularPivotError(const std::string& m, int i) : std::runtime_error(m), index(i) {}
+};
+struct ZeroPivotError : std::runtime_error {
+    int index;
+    ZeroPivotError(const std::string& m, int i) : std::runtime_error(m), index(i) {}
+};
+struct DeviceError : std::runtime_error {
+    int code;
+    DeviceError(const std::string& m, int c) : std::runtime_error(m), code(c) {}
+};
+
+inline void check(int code) {
+    if (code == FWI_OK) return;
+    const std::string msg = fwi_dev_last_error();
+    switch (code) {
+        case FWI_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case FWI_ERR_SINGULAR_PIVOT: throw SingularPivotError(msg, fwi_dev_last_error_index());
+        case FWI_ERR_ZERO_PIVOT: throw ZeroPivotError(msg, fwi_dev_last_error_index());
+        default: throw DeviceError(msg, code);
+    }
+}
+
+enum class PrecondMode { exact = FWI_PRECOND_EXACT, ilu = FWI_PRECOND_ILU };
+
+// fwi::GnState on the device (make_gn_state, src/reduced_space.cpp:40-86)
+class GnState {
+public:
+    explicit GnState(const fwi_state_desc& d) { check(fwi_dev_ctx_create(&d, &h_)); }
+    GnState(const GnState&) = delete;
+    GnState& operator=(const GnState&) = delete;
+    GnState(GnState&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+    ~GnState() {
+        if (h_) fwi_dev_ctx_destroy(h_);
+    }
+    fwi_dev_ctx* handle() const { return h_; }
+    fwi_state_info info() const {
+        fwi_state_info i{};
+        check(fwi_dev_ctx_info(h_, &i));
+        return i;
+    }
+    int model_size() const { return info().n; }
+    int num_sources() const { return info().num_sources; }
+    void set_epsilon(double e) { check(fwi_dev_ctx_set_epsilon(h_, e)); }
+    void set_drop_reg_term(bool d) { check(fwi_dev_ctx_set_drop_reg_term(h_, d ? 1 : 0)); }
+    void factor_ilu(int level, double diag_shift = 0.0) { check(fwi_dev_factor_ilu(h_, level, diag_shift)); }
+    std::int64_t solve_count(PrecondMode m = PrecondMode::exact) const {
+        return fwi_dev_solve_count(h_, int(m));
+    }
+    void reset_solve_count(PrecondMode m = PrecondMode::exact) { fwi_dev_reset_solve_count(h_, int(m)); }
+    // LuFactors::solve / IluFactors::solve for one RHS
+    std::vector<std::complex<double>> solve(const std::vector<std::complex<double>>& b,
+                                            PrecondMode m = PrecondMode::exact, bool adjoint = false) {
+        std::vector<std::complex<double>> x(b.size());
+        check(fwi_dev_solve(h_, int(m), adjoint ? 1 : 0, 1, reinterpret_cast<const double*>(b.data()),
+                            reinterpret_cast<double*>(x.data())));
+        return x;
+    }
+
+private:
+    fwi_dev_ctx* h_ = nullptr;
+};
+
+// fwi::KktVector on the device: one flat buffer [du_0..du_{K-1} | ds | la_0..la_{K-1}]
+class KktVector {
+public:
+    static KktVector zeros(GnState& s, int precision = FWI_C128) { return KktVector(s, precision); }
+    KktVector(GnState& s, int precision = FWI_C128) : state_(&s) {
+        check(fwi_dev_vec_create(s.handle(), precision, &h_));
+    }
+    KktVector(const KktVector& o) : state_(o.state_) {
+        check(fwi_dev_vec_create(state_->handle(), FWI_C128, &h_));
+        check(fwi_dev_vec_copy(h_, o.h_));
+    }
+    KktVector& operator=(const KktVector& o) {
+        if (this != &o) check(fwi_dev_vec_copy(h_, o.h_));
+        return *this;
+    }
+    KktVector(KktVector&& o) noexcept : state_(o.state_), h_(std::exchange(o.h_, nullptr)) {}
+    ~KktVector() {
+        if (h_) fwi_dev_vec_destroy(h_);
+    }
+    fwi_dev_vec* handle() const { return h_; }
+    GnState& state() const { return *state_; }
+    void upload(const std::vector<double>& flat) { check(fwi_dev_vec_upload(h_, flat.data())); }
+    std::vector<double> download() const {
+        std::vector<double> f(size_t(state_->info().vec_doubles));
+        check(fwi_dev_vec_download(h_, f.data()));
+        return f;
+    }
+    // any type with the reference KktVector's members (du, ds, lambda)
+    template <class RefKkt>
+    void upload_from(const RefKkt& v) {
+        std::vector<double> f;
+        for (const auto& b : v.du) append(f, b);
+        f.insert(f.end(), v.ds.begin(), v.ds.end());
+        for (const auto& b : v.lambda) append(f, b);
+        upload(f);
+    }
+    template <class RefKkt>
+    void download_into(RefKkt& v) const {
+        const std::vector<double> f = download();
+        size_t o = 0;
+        for (auto& b : v.du) o = take(f, o, b);
+        for (auto& d : v.ds) d = f[o++];
+        for (auto& b : v.lambda) o = take(f, o, b);
+    }
+
+private:
+    template <class C>
+    static void append(std::vector<double>& f, const C& b) {
+        for (const auto& z : b) {
+            f.push_back(z.real());
+            f.push_back(z.imag());
+        }
+    }
+    template <class C>
+    static size_t take(const std::vector<double>& f, size_t o, C& b) {
+        for (auto& z : b) {
+            z = {f[o], f[o + 1]};
+            o += 2;
+        }
+        return o;
+    }
+    GnState* state_;
+    fwi_dev_vec* h_ = nullptr;
+};
+
+inline double dot(const KktVector& x, const KktVector& y) {
+    double r = 0;
+    check(fwi_dev_vec_dot(x.handle(), y.handle(), &r));
+    return r;
+}
+inline double norm(const KktVector& x) {
+    double r = 0;
+    check(fwi_dev_vec_norm(x.handle(), &r));
+    return r;
+}
+inline void axpy(double a, const KktVector& x, KktVector& y) { check(fwi_dev_vec_axpy(a, x.handle(), y.handle())); }
+inline void scal(double a, KktVector& x) { check(fwi_dev_vec_scal(a, x.handle())); }
+
+inline KktVector kkt_apply(GnState& s, const KktVector& xi) {
+    KktVector out(s);
+    check(fwi_dev_kkt_apply(s.handle(), xi.handle(), out.handle()));
+    return out;
+}
+inline KktVector kkt_rhs(GnState& s) {
+    KktVector out(s);
+    check(fwi_dev_kkt_rhs(s.handle(), out.handle()));
+    return out;
+}
+inline KktVector precond_apply(GnState& s, const KktVector& v, PrecondMode mode) {
+    KktVector out(s);
+    check(fwi_dev_precond_apply(s.handle(), int(mode), v.handle(), out.handle()));
+    return out;
+}
+
+// fwi::FsgnOptions (include/fwi/kkt.hpp:47-57), same defaults
+struct FsgnOptions {
+    PrecondMode mode = PrecondMode::exact;
+    int restart = 30;
+    double tol = 1e-10;
+    int maxit = 30;
+    int ecg_stride = 1;
+    double ecg_stop_tol = 0.0;
+};
+
+// fwi::ConvergenceLog (include/fwi/krylov.hpp:17-33)
+struct ConvergenceLog {
+    struct Entry {
+        int iteration = 0;
+        double residual_norm = 0.0;
+        std::optional<double> normal_residual;
+        std::optional<double> precond_residual;
+        double wall_time = 0.0;
+    };
+    std::vector<Entry> entries;
+    bool converged = false;
+    bool stagnated = false;
+    int iterations() const { return entries.empty() ? 0 : entries.back().iteration; }
+    double final_residual() const { return entries.empty() ? 0.0 : entries.back().residual_norm; }
+};
+
+struct StepResult {
+    std::vector<double> delta_s;
+    ConvergenceLog log;
+};
+
+inline StepResult fsgn_gmres_step(GnState& s, const FsgnOptions& o = {}) {
+    fwi_fsgn_options co{int(o.mode), o.restart, o.tol, o.maxit, o.ecg_stride, o.ecg_stop_tol};
+    std::vector<fwi_log_entry> buf(size_t(o.maxit) + 2);
+    fwi_convergence_log cl{buf.data(), int(buf.size()), 0, 0, 0};
+    StepResult r;
+    r.delta_s.resize(size_t(s.model_size()));
+    check(fwi_dev_fsgn_gmres_step(s.handle(), &co, r.delta_s.data(), &cl));
+    for (int i = 0; i < cl.count; ++i) {
+        ConvergenceLog::Entry e;
+        e.iteration = buf[i].iteration;
+        e.residual_norm = buf[i].residual_norm;
+        if (buf[i].has_normal_residual) e.normal_residual = buf[i].normal_residual;
+        if (buf[i].has_precond_residual) e.precond_residual = buf[i].precond_residual;
+        e.wall_time = buf[i].wall_time;
+        r.log.entries.push_back(e);
+    }
+    r.log.converged = cl.converged != 0;
+    r.log.stagnated = cl.stagnated != 0;
+    return r;
+}
+
+}  // namespace fwi::gpu

