@@ -214,6 +214,31 @@ int fwi_dev_precond_apply(fwi_dev_ctx* ctx, int mode, const fwi_dev_vec* v, fwi_
 int fwi_dev_fsgn_gmres_step(fwi_dev_ctx* ctx, const fwi_fsgn_options* opt, double* delta_s_host,
                             fwi_convergence_log* log);
 
+/* ---- Gauss-Newton step (the caller of the hot path, src/driver.cpp:65-127) --
+ * Linearise at desc->s (u computed on the device, r from desc->d_obs), solve
+ * the KKT system with fsgn_gmres_step, clamp s + ds to [1/v_max^2, 1/v_min^2],
+ * and re-solve at the updated model for the final misfit. */
+#define FWI_SOLVER_FSGN_EXACT 1
+#define FWI_SOLVER_FSGN_ILU 2
+typedef struct fwi_gn_options {
+    int solver;               /* FWI_SOLVER_FSGN_* (rsgn-cg is outside this path) */
+    int max_inner;            /* FwiConfig::max_inner */
+    double inner_tol;         /* FwiConfig::inner_tol */
+    int gmres_restart;
+    int ilu_level;
+    double ilu_diag_shift;
+    double v_min, v_max;      /* clamp bounds, m/s */
+    int ecg_stride;
+    double ecg_stop_tol;
+} fwi_gn_options;
+
+typedef struct fwi_gn_result {
+    double misfit_ini, misfit_fin, update_relnorm, wall_seconds;
+} fwi_gn_result;
+
+int fwi_dev_gn_step(const fwi_state_desc* desc, const fwi_gn_options* opt, double* s_out,
+                    fwi_gn_result* result, fwi_convergence_log* log);
+
 /* ---- generic GMRES over flat real device vectors ------------------------
  * The same restarted left-preconditioned GMRES core as fsgn_gmres_step
  * (krylov.hpp:128-269), with caller-supplied operators. Vectors are device

@@ -58,6 +58,22 @@ class FsgnOptions(C.Structure):
                 ("maxit", C.c_int), ("ecg_stride", C.c_int), ("ecg_stop_tol", C.c_double)]
 
 
+FWI_SOLVER_FSGN_EXACT = 1
+FWI_SOLVER_FSGN_ILU = 2
+
+
+class GnOptions(C.Structure):
+    _fields_ = [("solver", C.c_int), ("max_inner", C.c_int), ("inner_tol", C.c_double),
+                ("gmres_restart", C.c_int), ("ilu_level", C.c_int), ("ilu_diag_shift", C.c_double),
+                ("v_min", C.c_double), ("v_max", C.c_double), ("ecg_stride", C.c_int),
+                ("ecg_stop_tol", C.c_double)]
+
+
+class GnResult(C.Structure):
+    _fields_ = [("misfit_ini", C.c_double), ("misfit_fin", C.c_double), ("update_relnorm", C.c_double),
+                ("wall_seconds", C.c_double)]
+
+
 class LogEntry(C.Structure):
     _fields_ = [("iteration", C.c_int), ("has_precond_residual", C.c_int),
                 ("has_normal_residual", C.c_int), ("pad_", C.c_int),

@@ -128,6 +128,7 @@ def lib() -> C.CDLL:
                 "fwi_dev_kkt_apply": [_vp, _vp, _vp],
                 "fwi_dev_kkt_rhs": [_vp, _vp],
                 "fwi_dev_kkt_apply_host": [_vp, _dp, _dp],
+                "fwi_dev_gn_step": [C.c_void_p, C.c_void_p, _dp, C.c_void_p, C.c_void_p],
                 "fwi_dev_precond_apply": [_vp, C.c_int, _vp, _vp],
                 "fwi_dev_fsgn_gmres_step": [_vp, C.c_void_p, _dp, C.c_void_p],
                 "fwi_dev_gmres_generic": [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, _vp, _vp, _vp,
@@ -429,6 +430,71 @@ def simulate(problem: Problem, s: np.ndarray | None = None) -> np.ndarray:
         return st.d_pred()
     finally:
         st.close()
+
+
+# ---------------------------------------------------------------------------
+# Gauss-Newton driver (src/driver.cpp:65-155)
+# ---------------------------------------------------------------------------
+@dataclass
+class FwiConfig:
+    """The fields of fwi::FwiConfig (include/fwi/driver.hpp:17-42) this path uses."""
+    solver: str = "fsgn-gmres-exact"
+    max_inner: int = 30
+    inner_tol: float = 1e-12
+    gmres_restart: int = 30
+    ilu_level: int = 4
+    ilu_diag_shift: float = 0.0
+    v_min: float = 300.0
+    v_max: float = 8000.0
+    ecg_stride: int = 0
+    ecg_stop_tol: float = 0.0
+
+
+@dataclass
+class GnStepResult:
+    freq_hz: float
+    epsilon: float
+    s: np.ndarray
+    log: ConvergenceLog
+    misfit_ini: float
+    misfit_fin: float
+    update_relnorm: float
+    wall_seconds: float
+
+
+def gn_step(problem: Problem, s: np.ndarray, freq_hz: float, epsilon: float, config: FwiConfig = FwiConfig()):
+    """fwi::gn_step: linearise at s, solve the KKT system on the device, clamp, re-solve.
+    problem.d_obs must hold the observed data at freq_hz."""
+    from dataclasses import replace
+    solver = {"fsgn-gmres-exact": _abi.FWI_SOLVER_FSGN_EXACT, "fsgn-gmres-ilu": _abi.FWI_SOLVER_FSGN_ILU}
+    if config.solver not in solver:
+        raise InvalidArgument(f"unknown inner solver '{config.solver}' on this path")
+    q = replace(problem, s=np.ascontiguousarray(s, np.float64), freq_hz=freq_hz, epsilon=epsilon, u=None, r=None)
+    d, keep = q.desc()
+    o = _abi.GnOptions(solver[config.solver], config.max_inner, config.inner_tol, config.gmres_restart,
+                       config.ilu_level, config.ilu_diag_shift, config.v_min, config.v_max, config.ecg_stride,
+                       config.ecg_stop_tol)
+    s_out = np.empty(problem.n)
+    res = _abi.GnResult()
+    lb = _abi.LogBuffer(config.max_inner + 2)
+    _check(lib().fwi_dev_gn_step(C.byref(d), C.byref(o), _p(s_out), C.byref(res), C.byref(lb.c)))
+    return GnStepResult(freq_hz, epsilon, s_out, lb.to_log(), res.misfit_ini, res.misfit_fin,
+                        res.update_relnorm, res.wall_seconds)
+
+
+def fwi_run(problem: Problem, observed: dict, s0: np.ndarray, epsilons: dict, config: FwiConfig = FwiConfig(),
+            steps_per_frequency: int = 1):
+    """fwi::fwi_run (src/driver.cpp:129-155): ascending frequencies, each consuming the
+    previous model; steps_per_frequency > 1 repeats gn_step (BASELINE configs 3-4)."""
+    from dataclasses import replace
+    report, s = [], np.asarray(s0, np.float64)
+    for f in sorted(observed):
+        q = replace(problem, d_obs=observed[f])
+        for _ in range(steps_per_frequency):
+            r = gn_step(q, s, f, epsilons[f], config)
+            report.append(r)
+            s = r.s
+    return report
 
 
 # ---------------------------------------------------------------------------

@@ -16,6 +16,8 @@ struct fwi_dev_vec {
 };
 
 namespace fwi_b200 {
+void gn_step(const fwi_state_desc& d0, const fwi_gn_options& o, double* s_out, fwi_gn_result* res,
+             fwi_convergence_log* log);
 void gmres_generic(int64_t n, fwi_op_cb apply, fwi_op_cb precond, fwi_observer_cb observer, void* user,
                    const double* b, double* x, int restart, double tol, int maxit,
                    fwi_convergence_log* log);
@@ -396,6 +398,17 @@ int fwi_dev_fsgn_gmres_step(fwi_dev_ctx* ctx, const fwi_fsgn_options* opt, doubl
         need(ctx, "ctx");
         need(opt, "options");
         fsgn_gmres_step(*ctx->c, *opt, ds, log);
+    });
+}
+
+int fwi_dev_gn_step(const fwi_state_desc* desc, const fwi_gn_options* opt, double* s_out,
+                    fwi_gn_result* result, fwi_convergence_log* log) {
+    return guard([&] {
+        need(desc, "desc");
+        need(opt, "options");
+        need(s_out, "s_out");
+        need(result, "result");
+        gn_step(*desc, *opt, s_out, result, log);
     });
 }
 

@@ -275,6 +275,63 @@ def c2_problem(seed: int = 2024, K: int = 64, R: int = 256) -> Problem:
                    u=u, r=r, name="C2")
 
 
+def layered_fault_velocity(nx: int, nz: int, seed: int, water_cells: int = 10, n_layers: int = 40,
+                           n_faults: int = 3, vmin: float = 1500.0, vmax: float = 4700.0,
+                           fault_throw=(5, 15)) -> np.ndarray:
+    """Marmousi-like synthetic section (BASELINE config 3): a water layer at 1500 m/s,
+    `n_layers` seeded dipping layers with velocities drawn from U(vmin, vmax) and
+    sorted to trend upward with depth, and `n_faults` seeded normal faults whose
+    hanging wall is shifted down by 5-15 cells. The reference has only layered and
+    lens generators (src/model_io.cpp:437-487), so this one is ours."""
+    rng = np.random.default_rng(seed)
+    depth = nz - water_cells
+    vel_layers = np.sort(rng.uniform(vmin, vmax, n_layers))
+    # interface depths (cells below the water) and per-interface dips (cells per column)
+    tops = np.sort(rng.uniform(0, depth, n_layers - 1))
+    dips = rng.uniform(-0.08, 0.08, n_layers - 1)
+    ix = np.arange(nx)[None, :]
+    iz = np.arange(depth)[:, None].astype(float)
+    # layer index at (z, x): number of interfaces above
+    layer = np.zeros((depth, nx), np.int64)
+    for t, d in zip(tops, dips):
+        layer += (iz >= t + d * (ix - nx / 2)).astype(np.int64)
+    v = vel_layers[np.clip(layer, 0, n_layers - 1)]
+    for _ in range(n_faults):  # normal faults: shift the hanging wall down
+        x0 = rng.uniform(0.15 * nx, 0.85 * nx)
+        slope = rng.uniform(0.4, 1.2) * (1 if rng.uniform() < 0.5 else -1)
+        throw = int(rng.integers(fault_throw[0], fault_throw[1] + 1))
+        hang = (ix - x0) * slope > iz - depth / 2 + 0 * ix  # one side of a dipping fault plane
+        hang = np.broadcast_to(hang, (depth, nx))
+        shifted = np.empty_like(v)
+        shifted[throw:] = v[:-throw]
+        shifted[:throw] = v[:1]
+        v = np.where(hang, shifted, v)
+    out = np.empty((nz, nx))
+    out[:water_cells] = 1500.0
+    out[water_cells:] = v
+    return out
+
+
+def c3_problem(freq_hz: float = 3.0, seed: int = 33, K: int = 48, R: int = 192, nx: int = 384, nz: int = 128,
+               h: float = 20.0, n_pml: int = 20) -> Problem:
+    """BASELINE config 3/4: 384x128, h=20 m, ⚑ 20-cell PML, 10-cell water layer, 40 seeded
+    dipping layers and 3 normal faults; 48 sources and 192 receivers on the top core
+    row; the start model is the truth smoothed with a 10-cell Gaussian; frequencies
+    3, 5, 7 Hz. ⚑ eps calibrated as in config 1 (1e10 with drop_reg_term)."""
+    g = Grid(nx, nz, h, n_pml)
+    vt = layered_fault_velocity(nx, nz, seed)
+    v0 = _gauss_smooth(vt, 10.0)
+    v0[:10] = 1500.0
+    g.sigma_max = pml_sigma_max(g, float(v0.mean()))
+    row = g.n_pml + 1
+    src = [(g.n_pml + 1 + int(round((k + 0.5) * (g.core_nx - 2) / K)), row) for k in range(K)]
+    rec = [(g.n_pml + 1 + (j * (g.core_nx - 2)) // R, row) for j in range(R)]
+    sv = Survey.shared(src, rec)
+    return Problem(grid=g, survey=sv, freq_hz=freq_hz, epsilon=1e10, drop_reg_term=True,
+                   s=(1.0 / v0 ** 2).ravel(), s_true=(1.0 / vt ** 2).ravel(), name="C3",
+                   meta={"v_true": vt, "v0": v0})
+
+
 def small_problem(nx=24, nz=18, n_pml=3, K=3, R=5, freq=6.0, h=20.0, seed=7, eps=1e-2,
                   duplicate_receiver=False, weight_mode=_abi.FWI_WEIGHT_IDENTITY) -> Problem:
     """Small desk-scale instance for parity tests (seconds on the CPU oracle)."""

@@ -344,3 +344,21 @@ def test_kkt_apply_host_pipelined_bit_exact(mk):
     for seed in (3, 4):
         x = random_kkt(p, seed)
         assert np.array_equal(fw.kkt_apply_host(dev, x), ref.kkt_apply(x))
+
+
+@pytest.mark.parametrize("solver,ilu", [(1, 4), (2, 4)])
+def test_gn_step_matches_reference_c1(solver, ilu):
+    """gn_step (src/driver.cpp:65-127): the Newton-updated model within 1e-6 relative L2
+    (north-star gate) and the misfits of the reference."""
+    p = c1_problem()
+    p.d_obs = po.ref_simulate(p)
+    s_ref, mi_ref, mf_ref, log_ref = po.ref_gn_step(p, solver=solver, max_inner=30, inner_tol=1e-12,
+                                                    restart=30, ilu_level=ilu)
+    cfg = fw.FwiConfig(solver="fsgn-gmres-exact" if solver == 1 else "fsgn-gmres-ilu", max_inner=30,
+                       inner_tol=1e-12, gmres_restart=30, ilu_level=ilu)
+    r = fw.gn_step(p, p.s, p.freq_hz, p.epsilon, cfg)
+    print("model rel dev", rel(r.s, s_ref), "misfits", r.misfit_ini, mi_ref, r.misfit_fin, mf_ref)
+    assert rel(r.s, s_ref) <= 1e-6
+    assert abs(r.misfit_ini - mi_ref) <= 1e-9 * mi_ref
+    assert abs(r.misfit_fin - mf_ref) <= 1e-6 * mf_ref
+    assert r.log.iterations() == log_ref.iterations()
