@@ -49,6 +49,7 @@ extern "C" {
 #define FWI_ERR_CUDA 4             /* CUDA runtime failure (no fallback exists) */
 #define FWI_ERR_NOT_SUPPORTED 5
 #define FWI_ERR_OUT_OF_MEMORY 6
+#define FWI_ERR_CG_BREAKDOWN 7       /* fwi::CgBreakdownError */
 
 /* fwi::PrecondMode (include/fwi/kkt.hpp:38) */
 #define FWI_PRECOND_EXACT 0
@@ -214,14 +215,21 @@ int fwi_dev_precond_apply(fwi_dev_ctx* ctx, int mode, const fwi_dev_vec* v, fwi_
 int fwi_dev_fsgn_gmres_step(fwi_dev_ctx* ctx, const fwi_fsgn_options* opt, double* delta_s_host,
                             fwi_convergence_log* log);
 
+/* rsgn_cg_step (src/reduced_space.cpp:163-170): CG on the reduced normal
+ * equations H ds = g with device Hessian actions (2K exact solves each) — the
+ * RSGN comparison path of the paper's Table 1. */
+int fwi_dev_rsgn_cg_step(fwi_dev_ctx* ctx, double tol, int maxit, double* delta_s_host,
+                         fwi_convergence_log* log);
+
 /* ---- Gauss-Newton step (the caller of the hot path, src/driver.cpp:65-127) --
  * Linearise at desc->s (u computed on the device, r from desc->d_obs), solve
  * the KKT system with fsgn_gmres_step, clamp s + ds to [1/v_max^2, 1/v_min^2],
  * and re-solve at the updated model for the final misfit. */
+#define FWI_SOLVER_RSGN_CG 0
 #define FWI_SOLVER_FSGN_EXACT 1
 #define FWI_SOLVER_FSGN_ILU 2
 typedef struct fwi_gn_options {
-    int solver;               /* FWI_SOLVER_FSGN_* (rsgn-cg is outside this path) */
+    int solver;               /* FWI_SOLVER_RSGN_CG / FWI_SOLVER_FSGN_EXACT / FWI_SOLVER_FSGN_ILU */
     int max_inner;            /* FwiConfig::max_inner */
     double inner_tol;         /* FwiConfig::inner_tol */
     int gmres_restart;

@@ -65,6 +65,7 @@ def ref_lib() -> C.CDLL:
             "ref_ilu_factor_status": [vp, C.c_int, C.c_double],
             "ref_kkt_apply_bench": [vp, _dp, C.c_int, C.c_int, _dp],
             "ref_ilu_export": [vp, _ip, _ip, _ip, _ip, _dp, _ip, _ip, _dp],
+            "ref_rsgn": [vp, C.c_double, C.c_int, _dp, C.c_void_p],
             "ref_gn_step": [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
                             C.c_double, C.c_double, _dp, _dp, _dp, C.c_void_p],
         }.items():
@@ -207,6 +208,12 @@ class Ref:
         ds = np.empty(self.n)
         lb = _abi.LogBuffer(maxit + 2)
         _ck(self.lib, self.lib.ref_fsgn(self.h, C.byref(o), _p(ds), C.byref(lb.c)))
+        return ds, lb.to_log()
+
+    def rsgn(self, tol, maxit):
+        ds = np.empty(self.n)
+        lb = _abi.LogBuffer(maxit + 2)
+        _ck(self.lib, self.lib.ref_rsgn(self.h, tol, maxit, _p(ds), C.byref(lb.c)))
         return ds, lb.to_log()
 
     def ilu_factors(self):

@@ -372,6 +372,17 @@ int ref_fsgn(void* h, const fwi_fsgn_options* o, double* ds_out, fwi_convergence
     }
 }
 
+int ref_rsgn(void* h, double tol, int maxit, double* ds_out, fwi_convergence_log* log) {
+    try {
+        const StepResult r = rsgn_cg_step(static_cast<RefCtx*>(h)->st, tol, maxit);
+        std::memcpy(ds_out, r.delta_s.data(), r.delta_s.size() * sizeof(double));
+        fill_log(r.log, log);
+        return FWI_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 // Forward data d = Q A(s)^{-1} f for the state's geometry at model s
 // (fixtures::simulate_blocks, tests/support/fixtures.hpp:12-23).
 int ref_simulate(const fwi_state_desc* d, double* d_out) {

@@ -69,6 +69,11 @@ class CudaError(FwiError):
     code = _abi.FWI_ERR_CUDA
 
 
+class CgBreakdownError(FwiError):
+    """fwi::CgBreakdownError (include/fwi/krylov.hpp:35-37)"""
+    code = 7
+
+
 class PrecondMode(enum.IntEnum):
     exact = _abi.FWI_PRECOND_EXACT
     ilu = _abi.FWI_PRECOND_ILU
@@ -129,6 +134,7 @@ def lib() -> C.CDLL:
                 "fwi_dev_kkt_rhs": [_vp, _vp],
                 "fwi_dev_kkt_apply_host": [_vp, _dp, _dp],
                 "fwi_dev_gn_step": [C.c_void_p, C.c_void_p, _dp, C.c_void_p, C.c_void_p],
+                "fwi_dev_rsgn_cg_step": [_vp, C.c_double, C.c_int, _dp, C.c_void_p],
                 "fwi_dev_precond_apply": [_vp, C.c_int, _vp, _vp],
                 "fwi_dev_fsgn_gmres_step": [_vp, C.c_void_p, _dp, C.c_void_p],
                 "fwi_dev_gmres_generic": [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, _vp, _vp, _vp,
@@ -170,6 +176,8 @@ def _check(code: int) -> None:
         raise ZeroPivotError(msg, idx)
     if code == _abi.FWI_ERR_CUDA:
         raise CudaError(msg)
+    if code == 7:
+        raise CgBreakdownError(msg)
     e = FwiError(f"[{code}] {msg}")
     e.code = code
     raise e
@@ -432,6 +440,14 @@ def simulate(problem: Problem, s: np.ndarray | None = None) -> np.ndarray:
         st.close()
 
 
+def rsgn_cg_step(state: GnState, tol: float, maxit: int):
+    """fwi::rsgn_cg_step (src/reduced_space.cpp:163-170) on the device."""
+    ds = np.empty(state.n)
+    lb = _abi.LogBuffer(maxit + 2)
+    _check(lib().fwi_dev_rsgn_cg_step(state.h, tol, maxit, _p(ds), C.byref(lb.c)))
+    return ds, lb.to_log()
+
+
 # ---------------------------------------------------------------------------
 # Gauss-Newton driver (src/driver.cpp:65-155)
 # ---------------------------------------------------------------------------
@@ -466,7 +482,8 @@ def gn_step(problem: Problem, s: np.ndarray, freq_hz: float, epsilon: float, con
     """fwi::gn_step: linearise at s, solve the KKT system on the device, clamp, re-solve.
     problem.d_obs must hold the observed data at freq_hz."""
     from dataclasses import replace
-    solver = {"fsgn-gmres-exact": _abi.FWI_SOLVER_FSGN_EXACT, "fsgn-gmres-ilu": _abi.FWI_SOLVER_FSGN_ILU}
+    solver = {"rsgn-cg": 0, "fsgn-gmres-exact": _abi.FWI_SOLVER_FSGN_EXACT,
+              "fsgn-gmres-ilu": _abi.FWI_SOLVER_FSGN_ILU}
     if config.solver not in solver:
         raise InvalidArgument(f"unknown inner solver '{config.solver}' on this path")
     q = replace(problem, s=np.ascontiguousarray(s, np.float64), freq_hz=freq_hz, epsilon=epsilon, u=None, r=None)

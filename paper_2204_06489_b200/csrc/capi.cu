@@ -16,6 +16,7 @@ struct fwi_dev_vec {
 };
 
 namespace fwi_b200 {
+void rsgn_cg_step(Ctx& c, double tol, int maxit, double* ds_host, fwi_convergence_log* log);
 void gn_step(const fwi_state_desc& d0, const fwi_gn_options& o, double* s_out, fwi_gn_result* res,
              fwi_convergence_log* log);
 void gmres_generic(int64_t n, fwi_op_cb apply, fwi_op_cb precond, fwi_observer_cb observer, void* user,
@@ -398,6 +399,13 @@ int fwi_dev_fsgn_gmres_step(fwi_dev_ctx* ctx, const fwi_fsgn_options* opt, doubl
         need(ctx, "ctx");
         need(opt, "options");
         fsgn_gmres_step(*ctx->c, *opt, ds, log);
+    });
+}
+
+int fwi_dev_rsgn_cg_step(fwi_dev_ctx* ctx, double tol, int maxit, double* ds, fwi_convergence_log* log) {
+    return guard([&] {
+        need(ctx, "ctx");
+        rsgn_cg_step(*ctx->c, tol, maxit, ds, log);
     });
 }
 

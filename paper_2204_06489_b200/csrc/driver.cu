@@ -14,6 +14,8 @@
 
 namespace fwi_b200 {
 
+void rsgn_cg_step(Ctx& c, double tol, int maxit, double* ds_host, fwi_convergence_log* log);
+
 namespace {
 
 // relative_misfit (src/forward.cpp:114-124)
@@ -39,8 +41,8 @@ std::vector<std::complex<double>> dpred_of(const Ctx& c) {
 
 void gn_step(const fwi_state_desc& d0, const fwi_gn_options& o, double* s_out, fwi_gn_result* res,
              fwi_convergence_log* log) {
-    require(o.solver == FWI_SOLVER_FSGN_EXACT || o.solver == FWI_SOLVER_FSGN_ILU,
-            "gn_step: only the fsgn-gmres solvers are on this path");
+    require(o.solver == FWI_SOLVER_RSGN_CG || o.solver == FWI_SOLVER_FSGN_EXACT || o.solver == FWI_SOLVER_FSGN_ILU,
+            "gn_step: unknown inner solver");
     require(o.max_inner >= 1, "FwiConfig: max_inner must be >= 1");
     require(o.v_min > 0.0 && o.v_max > o.v_min, "FwiConfig: need 0 < v_min < v_max");
     require(d0.d_obs != nullptr || d0.survey.recv_offset[d0.survey.num_sources] == 0,
@@ -65,7 +67,10 @@ void gn_step(const fwi_state_desc& d0, const fwi_gn_options& o, double* s_out, f
     fo.ecg_stride = o.ecg_stride;
     fo.ecg_stop_tol = o.ecg_stop_tol;
     std::vector<double> ds(n);
-    fsgn_gmres_step(*c, fo, ds.data(), log);
+    if (o.solver == FWI_SOLVER_RSGN_CG)
+        rsgn_cg_step(*c, o.inner_tol, o.max_inner, ds.data(), log);
+    else
+        fsgn_gmres_step(*c, fo, ds.data(), log);
     c.reset();
 
     // clamp (src/driver.cpp:108-113)

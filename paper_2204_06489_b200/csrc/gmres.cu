@@ -308,6 +308,61 @@ void fsgn_gmres_step(Ctx& c, const fwi_fsgn_options& o, double* ds_host, fwi_con
     fill_log(lg, log);
 }
 
+// rsgn_cg_step (src/reduced_space.cpp:163-170) over cg<RealVector>
+// (include/fwi/krylov.hpp:79-120): CG on H ds = g, H = Re(J^H W^T W J) + eps I.
+void rsgn_cg_step(Ctx& c, double tol, int maxit, double* ds_host, fwi_convergence_log* log) {
+    require(c.exact != nullptr, "rsgn_cg_step: state has no exact factorization");
+    const auto t0 = std::chrono::steady_clock::now();
+    const int64_t len = c.ds_stride;
+    cudaStream_t st = c.stream;
+    Scratch sc;
+    auto ddot = [&](const double* a, const double* b) {
+        dev_dot_async(st, a, b, sc.out.p, sc.partials.p, sc.ticket.p, len);
+        double h = 0;
+        CK(cudaMemcpyAsync(&h, sc.out.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return h;
+    };
+    DevBuf<double> g(len), x(len), r(len), p(len), ap(len);
+    for (auto* b : {&g, &x, &r, &p, &ap}) CK(cudaMemsetAsync(b->p, 0, b->bytes(), st));
+    reduced_gradient(c, g.p);
+    Log lg;
+    const double bnorm = std::sqrt(ddot(g.p, g.p));
+    if (bnorm == 0.0) {
+        lg.entries.push_back({0, 0.0, {}, {}, seconds_since(t0)});
+        lg.converged = true;
+    } else {
+        lg.entries.push_back({0, 1.0, {}, {}, seconds_since(t0)});
+        CK(cudaMemcpyAsync(r.p, g.p, len * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(p.p, g.p, len * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        double rho = ddot(r.p, r.p);
+        for (int it = 1; it <= maxit; ++it) {
+            reduced_hessian(c, p.p, ap.p);
+            const double pap = ddot(p.p, ap.p);
+            if (!(pap > 0.0))
+                throw FwiError(FWI_ERR_CG_BREAKDOWN, "cg: non-positive curvature, operator is not HPD");
+            const double alpha = rho / pap;
+            dev_axpy(st, alpha, p.p, x.p, len);
+            dev_axpy(st, -alpha, ap.p, r.p, len);
+            const double rn = std::sqrt(ddot(r.p, r.p)) / bnorm;
+            lg.entries.push_back({it, rn, {}, {}, seconds_since(t0)});
+            if (rn <= tol) {
+                lg.converged = true;
+                break;
+            }
+            const double rho_new = ddot(r.p, r.p);
+            const double beta = rho_new / rho;
+            rho = rho_new;
+            dev_scal(st, beta, p.p, len);
+            dev_axpy(st, 1.0, r.p, p.p, len);
+        }
+    }
+    for (auto& e : lg.entries) e.normal_residual = e.residual_norm;  // src/reduced_space.cpp:166-168
+    if (ds_host) CK(cudaMemcpyAsync(ds_host, x.p, c.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    fill_log(lg, log);
+}
+
 void gmres_generic(int64_t n, fwi_op_cb apply, fwi_op_cb precond, fwi_observer_cb observer, void* user,
                    const double* b, double* x, int restart, double tol, int maxit,
                    fwi_convergence_log* log) {

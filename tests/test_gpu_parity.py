@@ -362,3 +362,25 @@ def test_gn_step_matches_reference_c1(solver, ilu):
     assert abs(r.misfit_ini - mi_ref) <= 1e-9 * mi_ref
     assert abs(r.misfit_fin - mf_ref) <= 1e-6 * mf_ref
     assert r.log.iterations() == log_ref.iterations()
+
+
+def test_rsgn_cg_matches_reference_and_agrees_with_fsgn(c1):
+    """rsgn_cg_step on the device vs the reference (C1: the early CG iterations,
+    before CG's rounding sensitivity on this ill-conditioned system takes over),
+    and RSGN vs FSGN at tight tolerance on the standard instance
+    (tests/test_kkt.cpp:206-215)."""
+    p, ref, dev = c1
+    ds_r, log_r = ref.rsgn(1e-6, 8)
+    ds_d, log_d = fw.rsgn_cg_step(dev, 1e-6, 8)
+    rr, rd = np.array(log_r.residuals()), np.array(log_d.residuals())
+    assert len(rr) == len(rd) == 9
+    assert np.max(np.abs(rd - rr) / rr) <= 1e-8
+    assert rel(ds_d, ds_r) <= 1e-6
+    q = standard_instance()
+    q.d_obs = po.ref_simulate(q)
+    r0 = po.Ref(q, full=True)
+    q.u, q.r = r0.u(), r0.residual()
+    dv = fw.GnState(q, exact=True)
+    ds_cg, _ = fw.rsgn_cg_step(dv, 1e-12, 400)
+    ds_gm, _ = fw.fsgn_gmres_step(dv, fw.FsgnOptions(tol=1e-12, maxit=400, ecg_stride=0))
+    assert rel(ds_gm, ds_cg) < 1e-5
