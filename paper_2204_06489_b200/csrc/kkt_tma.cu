@@ -31,9 +31,18 @@ namespace fwi_b200 {
 
 namespace {
 
-constexpr int kThreads = 512;
-constexpr int kCols = 128;  // max strip width (columns per CTA)
-constexpr int kRows = 8;    // rows per sub-tile (4 slots x 2 rows per thread)
+#ifndef FWI_KKT_THREADS
+#define FWI_KKT_THREADS 512
+#endif
+#ifndef FWI_KKT_COLS
+#define FWI_KKT_COLS 128
+#endif
+constexpr int kThreads = FWI_KKT_THREADS;
+constexpr int kCols = FWI_KKT_COLS;                   // tile width (columns)
+constexpr int kSlots = kThreads / kCols;              // row slots (2 rows per thread)
+constexpr int kColShift = kCols == 256 ? 8 : kCols == 128 ? 7 : kCols == 64 ? 6 : 5;
+constexpr int kCtasPerSm = kThreads <= 256 ? 2 : 1;
+constexpr int kRows = 2 * kSlots;  // rows per tile
 constexpr int kBH = kRows + 2;
 constexpr int kMaxStages = 4;
 
@@ -165,7 +174,7 @@ __device__ __forceinline__ void node_step(const typename A::T* dr, const typenam
 // bit-identical to the reference's sequential sum. S (stages) divides KC, so
 // stage indices and mbarrier parities are compile-time within a unit.
 template <class A, int KC, int S>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
     kkt_tma_kernel(const __grid_constant__ CUtensorMap tdu, const __grid_constant__ CUtensorMap tla,
                    const __grid_constant__ CUtensorMap tu, const TmaArgs<A> P) {
     static_assert(KC % S == 0, "stages must divide the chunk");
@@ -178,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     R* terms = reinterpret_cast<R*>(sm + size_t(S) * P.stage_bytes + 128);
     const int nx = P.nx, nz = P.nz, Tn = P.T_;
     const int U = Tn * P.C;
-    const int tid = threadIdx.x, lx = tid & (kCols - 1), zs = tid >> 7;
+    const int tid = threadIdx.x, lx = tid & (kCols - 1), zs = tid >> kColShift;
     const int RP = P.RP, UP = P.UP;
     const int64_t n = P.n;
 
@@ -228,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         bool full = true;
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
-            const int row = zs + 4 * r;
+            const int row = zs + kSlots * r;
             act[r] = lx < w && row < ht;
             const int ix = x0 + lx, iz = zt + row;
             const int64_t cc = act[r] ? int64_t(iz) * nx + ix : 0;
@@ -267,23 +276,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (P.memonly) {
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
-                    s_[r] = dus[(zs + 4 * r + 1) * RP];
-                    t_[r] = las[(zs + 4 * r + 1) * RP];
+                    s_[r] = dus[(zs + kSlots * r + 1) * RP];
+                    t_[r] = las[(zs + kSlots * r + 1) * RP];
                 }
             } else if (warp_full) {
 #pragma unroll
                 for (int r = 0; r < 2; ++r)
-                    node_step<A, true>(dus + (zs + 4 * r + 1) * RP, las + (zs + 4 * r + 1) * RP, RP, true, true,
+                    node_step<A, true>(dus + (zs + kSlots * r + 1) * RP, las + (zs + kSlots * r + 1) * RP, RP, true, true,
                                        true, true, cD[r], cN[r], cW[r], cE[r], cS[r], s_[r], t_[r]);
             } else {
 #pragma unroll
                 for (int r = 0; r < 2; ++r)
-                    node_step<A, false>(dus + (zs + 4 * r + 1) * RP, las + (zs + 4 * r + 1) * RP, RP, hN[r],
+                    node_step<A, false>(dus + (zs + kSlots * r + 1) * RP, las + (zs + kSlots * r + 1) * RP, RP, hN[r],
                                         hW[r], hE[r], hS[r], cD[r], cN[r], cW[r], cE[r], cS[r], s_[r], t_[r]);
             }
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
-                const int row = zs + 4 * r;
+                const int row = zs + kSlots * r;
                 const T duc = dus[(row + 1) * RP];
                 const T lac = las[(row + 1) * RP];
                 const T uc = us[row * UP];
@@ -441,7 +450,7 @@ KktPlan* build_plan(Ctx& c, bool f32) {
     p->T = int(tiles.size());
     // K-chunk per unit: enough units (~12 per SM) for dynamic balance; a power
     // of two dividing K
-    const int G0 = sm_count();
+    const int G0 = sm_count() * kCtasPerSm;
     int kc = 8;
     while (kc > 1 && (K % kc != 0 || int64_t(p->T) * (K / kc) < int64_t(4) * G0)) kc /= 2;
     if (const char* e = std::getenv("FWI_KKT_KC")) {
@@ -464,7 +473,7 @@ KktPlan* build_plan(Ctx& c, bool f32) {
     p->stage_bytes = 2 * p->dub + p->ub;
     p->tx_bytes = uint32_t(2 * size_t(RP) * kBH * es + size_t(UP) * kRows * es);
     const size_t tail = 128 + size_t(kc) * 2 * kThreads * (f32 ? 4 : 8);  // mbarriers, unit ring, terms
-    const size_t budget = 227 * 1024 - tail;
+    const size_t budget = (kCtasPerSm == 1 ? 227 * 1024 : 113 * 1024) - tail;
     // four stages when they fit and divide the chunk, else two
     int st = 4;
     if (const char* e = std::getenv("FWI_KKT_STAGES")) st = std::atoi(e) >= 4 ? 4 : 2;
