@@ -23,6 +23,11 @@
 // (C1: 8.4 MB, C3: 100 MB, C5: 34 GB), read twice per solve.
 #include <algorithm>
 #include <cstdlib>
+#include <string>
+#include <array>
+#include <type_traits>
+#include <cstdio>
+#include <vector>
 
 #include "ctx.cuh"
 
@@ -571,6 +576,413 @@ __global__ void __launch_bounds__(256) sweep_cluster_kernel(const SweepArgs a) {
     cluster_sync_all();  // no CTA leaves while peers may still address its shared memory
 }
 
+uint32_t al128(size_t b) { return uint32_t((b + 127) / 128 * 128); }
+
+// ---------------------------------------------------------------------------
+// Warp-specialised cluster sweep (v2). A cluster of CS CTAs owns KG right-hand
+// sides; CTA `rank` owns rows [rank*R, rank*R+R) of every line block. Each
+// consumer warp owns KR right-hand sides: it builds its own w_k = b_i - E y_{i-1}
+// (or E_i x_{i+1}), multiplies the CTA's G slab with it (lane = (row, column
+// residue class), fixed-order shuffle reduction over the classes) and pushes its
+// slab of y_k to every peer with st.async, completing on a per-warp receive
+// mbarrier there. A warp only ever waits for its own right-hand sides' data, so
+// a line step needs no CTA barrier; the producer warp streams G slabs, coupling
+// rows and RHS blocks into a ring of stages released by per-stage "empty"
+// mbarriers. Per line step the critical path is: receive wake-up -> w -> matvec
+// -> butterfly -> st.async (DSMEM latency ~200 cycles).
+//
+// Shared-memory traffic per step (the bound at large KG): G is read once per
+// warp, i.e. KG/KR times, and each G element feeds KR complex MACs; columns are
+// dealt to lanes round-robin (j = cls + ncls*t) so a warp's G and w loads hit
+// distinct bank groups.
+// ---------------------------------------------------------------------------
+constexpr int kWMaxStages = 8;
+
+struct WSweepArgs {
+    int L, nb, nrhs, gp, R, Rp, nst;
+    const double2* G;
+    const double2* coup;
+    double2* W;
+    double2* Y;
+    uint32_t off_e, off_b, stage_bytes, off_y, off_w, off_bar;
+    unsigned long long* trace;  // diagnostics: per-step clock64 stamps of CTA 0 / warp 0, or null
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %clock64;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void bar_init_n(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+// producer-side wait: polls with a back-off so the spinning warp leaves the issue
+// slots of its sub-partition to the consumer warps on the critical path
+__device__ __forceinline__ void bar_wait_lazy(uint64_t* b, uint32_t parity) {
+    uint32_t done = 0;
+    for (;;) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_addr(b)), "r"(parity)
+            : "memory");
+        if (done) return;
+        __nanosleep(128);
+    }
+}
+
+__device__ __forceinline__ void cmac(double2& c, const double2 g, const double2 x) {
+    c.x = fma(g.x, x.x, c.x);
+    c.y = fma(g.x, x.y, c.y);
+    c.x = fma(-g.y, x.y, c.x);
+    c.y = fma(g.y, x.x, c.y);
+}
+
+template <int CS, int KG, int KR, bool TRACE, bool EVEN>
+__global__ void __launch_bounds__((KG / KR + 1) * 32) sweep_warp_kernel(const WSweepArgs a) {
+    constexpr int NW = KG / KR;  // consumer warps
+    extern __shared__ __align__(128) unsigned char wsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int grp = blockIdx.x / CS;
+    const int nb = a.nb, L = a.L, gp = a.gp, nrhs = a.nrhs, R = a.R, Rp = a.Rp;
+    const int S = a.nst, smask = a.nst - 1;  // power of two
+    const int nbp = nb + 1;
+    const int k0 = grp * KG;
+    const int kc = min(KG, nrhs - k0);
+    const int r0 = int(rank) * R;
+    const int rows = max(0, min(nb, r0 + R) - r0);
+    double2* yfull = reinterpret_cast<double2*>(wsm + a.off_y);  // [2][KG][nbp]
+    uint64_t* full = reinterpret_cast<uint64_t*>(wsm + a.off_bar);
+    uint64_t* empty = full + kWMaxStages;
+    uint64_t* rbar = empty + kWMaxStages;  // [2][NW]
+    const int nsteps = 2 * L - 1;
+
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < S; ++q) {
+            bar_init(&full[q]);
+            bar_init_n(&empty[q], NW);
+        }
+        for (int q = 0; q < 2 * NW; ++q) bar_init(&rbar[q]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    cluster_sync_all();  // peers' barriers exist before any remote arrive
+
+    if (warp == NW) {  // ---- producer
+        if (lane == 0) {
+            const uint32_t gbytes = uint32_t(rows) * gp * sizeof(double2);
+            const uint32_t ebytes = uint32_t(rows) * sizeof(double2);
+            const uint32_t bbytes = uint32_t(kc) * nb * sizeof(double2);
+            for (int st = 0; st < nsteps; ++st) {
+                const int sb = st & smask;
+                if (st >= S) bar_wait_lazy(&empty[sb], ((st - S) / S) & 1);
+                unsigned char* buf = wsm + sb * a.stage_bytes;
+                const bool fwd = st < L;
+                const int i = fwd ? st : 2 * L - 2 - st;
+                // coupling that scales this step's result before it is pushed: the next
+                // step uses E_i (forward, line i+1) or E_{i-1} (backward, line i-1)
+                const int cidx = st + 1 < L ? st : 2 * L - 3 - st;
+                const uint32_t eb = (st + 1 < nsteps) ? ebytes : 0u;
+                const uint32_t bb = fwd ? bbytes : 0u;
+                bar_expect(&full[sb], gbytes + eb + bb);
+                if (gbytes) bulk_g2s(buf, a.G + (int64_t(i) * nb + r0) * gp, gbytes, &full[sb]);
+                if (eb) bulk_g2s(buf + a.off_e, a.coup + int64_t(cidx) * nb + r0, eb, &full[sb]);
+                if (bb) bulk_g2s(buf + a.off_b, a.W + (int64_t(i) * nrhs + k0) * nb, bb, &full[sb]);
+            }
+        }
+    } else {  // ---- consumer warp: right-hand sides k0 + warp*KR + [0, KR)
+        const int w = warp;
+        const int kw = w * KR;                    // first local RHS of this warp
+        const int kr = max(0, min(KR, kc - kw));  // active RHS of this warp
+        const int ncls = 32 / Rp;
+        const int row = lane & (Rp - 1), cls = lane / Rp;
+        const bool has_row = row < rows;
+        const int nj = (nb - cls + ncls - 1) / ncls;  // columns j = cls + ncls*t of this lane
+        const bool tr = TRACE && blockIdx.x == 0 && w == 0 && lane == 0;
+        // per-lane constant addresses
+        const uint32_t rb_local0 = smem_addr(&rbar[w]), rb_local1 = smem_addr(&rbar[NW + w]);
+        const uint32_t y_local0 = smem_addr(yfull + kw * nbp + r0 + row);
+        const uint32_t y_buf_bytes = uint32_t(KG * nbp * sizeof(double2)), y_q_bytes = uint32_t(nbp * sizeof(double2));
+        const int pfirst = cls, pstep = ncls;  // the row's lanes share the pushes to the CS peers
+        double2* Yrow = a.Y + int64_t(k0 + kw) * nb + r0 + row;  // + i*nrhs*nb + q*nb
+        double2* Wrow = a.W + int64_t(k0 + kw) * nb + r0 + row;
+        const int64_t line_stride = int64_t(nrhs) * nb;
+        const uint32_t rbytes = uint32_t(kr * nb) * 16u;
+
+        // Received vectors are pre-scaled by the coupling (z = E y), so a step is
+        //   forward   y_i = G_i (b_i - z_{i-1}),   backward  x_i = y_i - G_i z'_{i+1},
+        // and the CTA scales its own rows of the result before pushing them.
+        // EVEN: every lane owns a row and nj is a multiple of 4 (no element guards).
+        int sb = 0;
+        uint32_t fph = 0;
+        auto step = [&](auto fwd_tag, auto first_tag, const int st, const int i) {
+            constexpr bool fwd = decltype(fwd_tag)::value;
+            constexpr bool first = decltype(first_tag)::value;
+            if (tr) a.trace[8 * st] = gtimer();
+            // backward: this thread wrote its rows of y_i itself in the forward sweep; load early
+            double2 yown[KR];
+            if (!fwd) {
+#pragma unroll
+                for (int q = 0; q < KR; ++q)
+                    yown[q] = (q < kr && has_row) ? Yrow[i * line_stride + q * nb] : make_double2(0.0, 0.0);
+            }
+            bar_wait(&full[sb], fph);
+            if (tr) a.trace[8 * st + 1] = gtimer();
+            const unsigned char* buf = wsm + sb * a.stage_bytes;
+            const double2* Gs = reinterpret_cast<const double2*>(buf);
+            const double2* es = reinterpret_cast<const double2*>(buf + a.off_e);
+            const double2* bs = reinterpret_cast<const double2*>(buf + a.off_b);
+            if (kr > 0) {
+                if (lane == 0 && st + 1 < nsteps)
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((st & 1) ? rb_local1
+                                                                                                    : rb_local0),
+                                 "r"(rbytes)
+                                 : "memory");
+                const double2* g = Gs + row * gp + cls;
+                const double2* z = yfull + (((st + 1) & 1) * KG + kw) * nbp + cls;
+                const double2* bq = bs + kw * nb + cls;
+                const double2 esc = has_row && st + 1 < nsteps ? es[row] : make_double2(0.0, 0.0);
+                if (!first) bar_wait(&rbar[((st - 1) & 1) * NW + w], ((st - 1) >> 1) & 1);
+                if (tr) a.trace[8 * st + 2] = gtimer();
+                if (tr) a.trace[8 * st + 3] = gtimer();
+                // w_j = b_j - z_j (forward) | b_j (first line) | z_j (backward)
+                auto wval = [&](int q, int j) {
+                    if constexpr (first) return bq[q * nb + j];
+                    if constexpr (!fwd) return z[q * nbp + j];
+                    const double2 b = bq[q * nb + j], zz = z[q * nbp + j];
+                    return make_double2(b.x - zz.x, b.y - zz.y);
+                };
+                double2 acc[KR][4];
+#pragma unroll
+                for (int q = 0; q < KR; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = make_double2(0.0, 0.0);
+                if constexpr (EVEN) {
+#pragma unroll 2
+                    for (int t = 0; t < nj; t += 4) {
+                        double2 g4[4], w4[4][KR];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            g4[u] = g[(t + u) * ncls];
+#pragma unroll
+                            for (int q = 0; q < KR; ++q) w4[u][q] = wval(q, (t + u) * ncls);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+#pragma unroll
+                            for (int q = 0; q < KR; ++q) cmac(acc[q][u], g4[u], w4[u][q]);
+                    }
+                } else if (has_row) {
+                    for (int t = 0; t < nj; ++t) {
+                        const double2 g0 = g[t * ncls];
+#pragma unroll
+                        for (int q = 0; q < KR; ++q) cmac(acc[q][0], g0, wval(q, t * ncls));
+                    }
+                }
+                double2 v[KR];
+#pragma unroll
+                for (int q = 0; q < KR; ++q) {
+                    v[q] = make_double2((acc[q][0].x + acc[q][2].x) + (acc[q][1].x + acc[q][3].x),
+                                        (acc[q][0].y + acc[q][2].y) + (acc[q][1].y + acc[q][3].y));
+                    for (int off = Rp; off < 32; off <<= 1) {  // fixed-order class reduction
+                        v[q].x += __shfl_xor_sync(0xffffffffu, v[q].x, off);
+                        v[q].y += __shfl_xor_sync(0xffffffffu, v[q].y, off);
+                    }
+                }
+                if (tr) a.trace[8 * st + 4] = gtimer();
+                if (has_row) {  // every class lane holds the row totals after the butterfly
+#pragma unroll
+                    for (int q = 0; q < KR; ++q) {
+                        if (q < kr) {
+                            if (!fwd) v[q] = make_double2(yown[q].x - v[q].x, yown[q].y - v[q].y);
+                            if (st + 1 < nsteps) {
+                                const double2 zo = make_double2(esc.x * v[q].x - esc.y * v[q].y,
+                                                                esc.x * v[q].y + esc.y * v[q].x);
+                                const uint32_t la = y_local0 + ((st & 1) ? y_buf_bytes : 0u) + q * y_q_bytes;
+                                const uint32_t lb = (st & 1) ? rb_local1 : rb_local0;
+                                for (int p = pfirst; p < CS; p += pstep)
+                                    st_async16(map_rank(la, uint32_t(p)), zo, map_rank(lb, uint32_t(p)));
+                            }
+                            if (cls == q % ncls) {
+                                const int64_t off = i * line_stride + q * nb;
+                                if (fwd) {
+                                    Yrow[off] = v[q];
+                                    if (i == L - 1) Wrow[off] = v[q];
+                                } else {
+                                    Wrow[off] = v[q];
+                                }
+                            }
+                        }
+                    }
+                }
+                if (tr) a.trace[8 * st + 5] = gtimer();
+            }
+            __syncwarp();
+            if (lane == 0) bar_arrive(&empty[sb]);
+            if (++sb == S) {
+                sb = 0;
+                fph ^= 1u;
+            }
+        };
+        step(std::true_type{}, std::true_type{}, 0, 0);
+        for (int st = 1; st < L; ++st) step(std::true_type{}, std::false_type{}, st, st);
+        for (int st = L; st < nsteps; ++st) step(std::false_type{}, std::false_type{}, st, 2 * L - 2 - st);
+    }
+    __syncthreads();
+    cluster_sync_all();
+}
+
+struct WarpPlan {
+    WSweepArgs a;
+    int CS = 0, KG = 0, KR = 0;
+    bool even = false;  // every lane owns a row and an equal multiple-of-4 column count
+    size_t smem = 0;
+    double est = 0;
+};
+
+bool warp_layout(int nb, int L, int gp, int nrhs, int CS, int KG, WarpPlan& p) {
+    const int R = (nb + CS - 1) / CS;
+    if (R > 32) return false;
+    int Rp = 1;
+    while (Rp < R) Rp <<= 1;
+    WSweepArgs& a = p.a;
+    a = WSweepArgs{};
+    a.L = L;
+    a.nb = nb;
+    a.nrhs = nrhs;
+    a.gp = gp;
+    a.R = R;
+    a.Rp = Rp;
+    const size_t gbytes = size_t(R) * gp * sizeof(double2);
+    a.off_e = al128(gbytes);
+    a.off_b = a.off_e + al128(size_t(R) * sizeof(double2));
+    a.stage_bytes = a.off_b + al128(size_t(KG) * nb * sizeof(double2));
+    const size_t yb = al128(size_t(2) * KG * (nb + 1) * sizeof(double2));
+    const size_t wb = 0;  // w is formed in registers
+    const char* ns = std::getenv("FWI_EXACT_STAGES");
+    a.nst = ns ? std::max(2, std::min(kWMaxStages, std::atoi(ns))) : kWMaxStages;
+    while (a.nst & (a.nst - 1)) --a.nst;  // power of two: the kernel masks the step index
+    while (a.nst > 2 && size_t(a.nst) * a.stage_bytes + yb + wb + 512 > 220 * 1024) a.nst /= 2;
+    a.off_y = a.nst * a.stage_bytes;
+    a.off_w = a.off_y + yb;
+    a.off_bar = a.off_w + wb;
+    p.smem = a.off_bar + 512;
+    p.CS = CS;
+    p.KG = KG;
+    p.KR = KG >= 4 ? 2 : 1;
+    p.even = (R == Rp) && (nb % CS == 0) && (nb % (4 * (32 / Rp)) == 0);
+    return p.smem <= 220 * 1024;
+}
+
+template <int CS, int KG, int KR, bool TRACE, bool EVEN>
+bool warp_prepare(const WarpPlan& p, int* max_clusters) {
+    auto kern = sweep_warp_kernel<CS, KG, KR, TRACE, EVEN>;
+    static size_t set = 0;
+    if (p.smem > set) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem)) != cudaSuccess)
+            return false;
+        if (CS > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+            return false;
+        set = p.smem;
+    }
+    if (max_clusters) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(CS);
+        cfg.blockDim = dim3((KG / KR + 1) * 32);
+        cfg.dynamicSmemBytes = p.smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
+            cudaGetLastError();
+            return false;
+        }
+        *max_clusters = n;
+    }
+    return true;
+}
+
+template <int CS, int KG, int KR, bool TRACE, bool EVEN>
+bool warp_launch(const WarpPlan& p, int nrhs, cudaStream_t st) {
+    if (!warp_prepare<CS, KG, KR, TRACE, EVEN>(p, nullptr)) return false;
+    const int groups = (nrhs + KG - 1) / KG;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(groups * CS);
+    cfg.blockDim = dim3((KG / KR + 1) * 32);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, sweep_warp_kernel<CS, KG, KR, TRACE, EVEN>, p.a));
+    return true;
+}
+
+#define FWI_WARP_VARIANTS(X) X(8, 8, 2) X(8, 4, 2) X(8, 2, 1) X(8, 1, 1) X(16, 8, 2) X(16, 4, 2) X(16, 2, 1) X(16, 1, 1)
+
+bool warp_dispatch_prepare(const WarpPlan& p, int* maxc) {
+#define X(cs, kg, kr) \
+    if (p.CS == cs && p.KG == kg)                                                        \
+        return p.even ? warp_prepare<cs, kg, kr, false, true>(p, maxc) : warp_prepare<cs, kg, kr, false, false>(p, maxc);
+    FWI_WARP_VARIANTS(X)
+#undef X
+    return false;
+}
+
+bool warp_dispatch_launch(const WarpPlan& p, int nrhs, cudaStream_t st) {
+#define X(cs, kg, kr) \
+    if (p.CS == cs && p.KG == kg)                                   \
+        return !p.even ? warp_launch<cs, kg, kr, false, false>(p, nrhs, st)                         \
+                       : (p.a.trace ? warp_launch<cs, kg, kr, true, true>(p, nrhs, st)                   \
+                                    : warp_launch<cs, kg, kr, false, true>(p, nrhs, st));
+    FWI_WARP_VARIANTS(X)
+#undef X
+    return false;
+}
+
+// Pick (CS, KG) by a model of one line step, fitted to clock64 traces of the
+// kernel on B200 (tools/sweep_trace.py): a consumer warp's step is bound by its
+// dependent instruction stream, ~1400 cycles of fixed work (barrier wake-ups,
+// butterfly, pushes, DSMEM flight) plus ~35 cycles per column element per RHS it
+// owns; clusters beyond the resident limit run in further waves.
+bool warp_plan(int nb, int L, int gp, int nrhs, WarpPlan& best) {
+    const char* ecs = std::getenv("FWI_EXACT_CS");
+    const char* ekg = std::getenv("FWI_EXACT_KG");
+    const int want_cs = ecs ? std::atoi(ecs) : 0, want_kg = ekg ? std::atoi(ekg) : 0;
+    bool found = false;
+    for (int cs : {16, 8})
+        for (int kg : {8, 4, 2, 1}) {
+            if ((want_cs && cs != want_cs) || (want_kg && kg != want_kg)) continue;
+            WarpPlan p;
+            if (!warp_layout(nb, L, gp, nrhs, cs, kg, p)) continue;
+            int maxc = 0;
+            if (!warp_dispatch_prepare(p, &maxc)) continue;
+            const int groups = (nrhs + kg - 1) / kg;
+            const int waves = (groups + maxc - 1) / maxc;
+            const int ncls = 32 / p.a.Rp;
+            const double per_lane = double((nb + ncls - 1) / ncls);
+            p.est = double(waves) * (2.0 * L - 1) * (1400.0 + 35.0 * per_lane * p.KR);
+            // ties go to fewer clusters (less G traffic through L2)
+            if (!found || p.est < best.est - 1e-9 || (p.est <= best.est + 1e-9 && kg > best.KG)) {
+                best = p;
+                found = true;
+            }
+        }
+    return found;
+}
+
 struct ClusterPlan {
     bool ok = false;
     int KG = 0, CS = 0, R = 0, nseg = 0;
@@ -608,8 +1020,6 @@ bool cluster_launch(const ClusterPlan& cp, int nrhs, cudaStream_t st) {
     CK(cudaLaunchKernelEx(&cfg, sweep_cluster_kernel<KG, CS>, a));
     return true;
 }
-
-uint32_t al128(size_t b) { return uint32_t((b + 127) / 128 * 128); }
 
 // pick (KG, CS) whose shared-memory footprint fits; nb <= 256 only
 bool cluster_plan(int nb, int L, int gp, int nrhs, ClusterPlan& cp) {
@@ -733,7 +1143,49 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
     gather_lines<<<tg, tb, 0, c.stream>>>(f.col_lines, c.nx, c.nz, f.L, f.nb, nrhs, adjoint, b, W);
     CK_LAUNCH();
     bool done = false;
-    if (!std::getenv("FWI_EXACT_LEGACY")) {
+    const char* sw = std::getenv("FWI_EXACT_SWEEP");  // "warp" (default) | "cta" | "legacy"
+    const std::string sweep = sw ? sw : "warp";
+    if (sweep == "warp") {
+        // plans are cached per (nb, L, nrhs): the model queries cluster occupancy
+        static std::vector<std::pair<std::array<int, 3>, WarpPlan>> cache;
+        const std::array<int, 3> key{f.nb, f.L, nrhs};
+        WarpPlan* wp = nullptr;
+        for (auto& e : cache)
+            if (e.first == key && !std::getenv("FWI_EXACT_CS") && !std::getenv("FWI_EXACT_KG")) wp = &e.second;
+        WarpPlan fresh;
+        if (!wp && warp_plan(f.nb, f.L, f.gp, nrhs, fresh)) {
+            cache.emplace_back(key, fresh);
+            wp = &cache.back().second;
+        }
+        if (wp) {
+            WarpPlan p = *wp;
+            p.a.G = f.G.p;
+            p.a.coup = f.coup.p;
+            p.a.W = W;
+            if (f.ybuf.count < size_t(nrhs) * c.n) const_cast<ExactFactor&>(f).ybuf.alloc(size_t(nrhs) * c.n);
+            p.a.Y = f.ybuf.p;
+            const char* tpath = std::getenv("FWI_SWEEP_TRACE");  // diagnostics only
+            DevBuf<unsigned long long> tbuf;
+            if (tpath) {
+                tbuf.alloc(size_t(8) * (2 * f.L - 1));
+                CK(cudaMemsetAsync(tbuf.p, 0, tbuf.count * 8, c.stream));
+                p.a.trace = tbuf.p;
+            }
+            done = warp_dispatch_launch(p, nrhs, c.stream);
+            if (tpath && done) {
+                std::vector<unsigned long long> h(tbuf.count);
+                CK(cudaMemcpyAsync(h.data(), tbuf.p, tbuf.count * 8, cudaMemcpyDeviceToHost, c.stream));
+                CK(cudaStreamSynchronize(c.stream));
+                if (FILE* fp = std::fopen(tpath, "ab")) {
+                    std::fwrite(h.data(), 8, h.size(), fp);
+                    std::fclose(fp);
+                }
+                std::fprintf(stderr, "[fwi] exact sweep plan CS=%d KG=%d KR=%d nst=%d smem=%zu est=%.0f\n", p.CS,
+                             p.KG, p.KR, p.a.nst, p.smem, p.est);
+            }
+        }
+    }
+    if (!done && sweep != "legacy") {
         ClusterPlan cp;
         if (cluster_plan(f.nb, f.L, f.gp, nrhs, cp)) {
             cp.a.G = f.G.p;
