@@ -332,6 +332,35 @@ def c3_problem(freq_hz: float = 3.0, seed: int = 33, K: int = 48, R: int = 192, 
                    meta={"v_true": vt, "v0": v0})
 
 
+def c5_problem(freq_hz: float = 10.0, seed: int = 55, K: int = 256, R: int = 1024, nx: int = 2048,
+               nz: int = 1024, h: float = 10.0, n_pml: int = 30, with_u: bool = False) -> Problem:
+    """BASELINE config 5: 2048x1024, h=10 m, 30-cell PML, 10 Hz, 256 surface sources and
+    1024 receivers on the top core row; the model is config 3's construction scaled to
+    this grid (water layer, dipping layers, fault throws and the start-model smoothing
+    all x8 in cells, i.e. the same depths in metres at half the spacing).
+    ⚑ eps as in config 1/3 (1e10, drop_reg_term). With `with_u`, u_k and r are seeded
+    CN(0,1) (8.6 GB of host memory) for apply-only measurements, as in config 2."""
+    g = Grid(nx, nz, h, n_pml)
+    sc = nz / 128.0
+    vt = layered_fault_velocity(nx, nz, seed, water_cells=int(round(10 * sc)),
+                                fault_throw=(int(round(5 * sc)), int(round(15 * sc))))
+    v0 = _gauss_smooth(vt, 10.0 * sc)
+    v0[:int(round(10 * sc))] = 1500.0
+    g.sigma_max = pml_sigma_max(g, float(v0.mean()))
+    row = g.n_pml + 1
+    src = [(g.n_pml + 1 + int(round((k + 0.5) * (g.core_nx - 2) / K)), row) for k in range(K)]
+    rec = [(g.n_pml + 1 + (j * (g.core_nx - 2)) // R, row) for j in range(R)]
+    sv = Survey.shared(src, rec)
+    u = r = None
+    if with_u:
+        rng = np.random.default_rng(seed + 1)
+        u = rng.standard_normal(2 * K * g.n).view(np.complex128)
+        r = rng.standard_normal(2 * sv.num_data).view(np.complex128)
+    return Problem(grid=g, survey=sv, freq_hz=freq_hz, epsilon=1e10, drop_reg_term=True,
+                   s=(1.0 / v0 ** 2).ravel(), s_true=(1.0 / vt ** 2).ravel(), u=u, r=r, name="C5",
+                   meta={"v_true": vt, "v0": v0})
+
+
 def small_problem(nx=24, nz=18, n_pml=3, K=3, R=5, freq=6.0, h=20.0, seed=7, eps=1e-2,
                   duplicate_receiver=False, weight_mode=_abi.FWI_WEIGHT_IDENTITY) -> Problem:
     """Small desk-scale instance for parity tests (seconds on the CPU oracle)."""
