@@ -215,6 +215,14 @@ int fwi_dev_precond_apply(fwi_dev_ctx* ctx, int mode, const fwi_dev_vec* v, fwi_
 int fwi_dev_fsgn_gmres_step(fwi_dev_ctx* ctx, const fwi_fsgn_options* opt, double* delta_s_host,
                             fwi_convergence_log* log);
 
+/* Reduced-space gradient and Gauss-Newton Hessian action (the RSGN / E_cg
+ * building blocks): g = Re(J^H W^T W r) - eps s (gradient, src/reduced_space.cpp:
+ * 141-152; K adjoint exact solves) and H v = Re(J^H W^T W J v) + eps v
+ * (hessian_apply, src/reduced_space.cpp:120-139; 2K exact solves). Host arrays of
+ * n doubles. */
+int fwi_dev_gradient(fwi_dev_ctx* ctx, double* g_host);
+int fwi_dev_hessian_apply(fwi_dev_ctx* ctx, const double* v_host, double* out_host);
+
 /* rsgn_cg_step (src/reduced_space.cpp:163-170): CG on the reduced normal
  * equations H ds = g with device Hessian actions (2K exact solves each) — the
  * RSGN comparison path of the paper's Table 1. */

@@ -135,6 +135,8 @@ def lib() -> C.CDLL:
                 "fwi_dev_kkt_apply_host": [_vp, _dp, _dp],
                 "fwi_dev_gn_step": [C.c_void_p, C.c_void_p, _dp, C.c_void_p, C.c_void_p],
                 "fwi_dev_rsgn_cg_step": [_vp, C.c_double, C.c_int, _dp, C.c_void_p],
+                "fwi_dev_gradient": [_vp, _dp],
+                "fwi_dev_hessian_apply": [_vp, _dp, _dp],
                 "fwi_dev_precond_apply": [_vp, C.c_int, _vp, _vp],
                 "fwi_dev_fsgn_gmres_step": [_vp, C.c_void_p, _dp, C.c_void_p],
                 "fwi_dev_gmres_generic": [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, _vp, _vp, _vp,
@@ -382,6 +384,21 @@ def kkt_apply_host(state: GnState, xi: np.ndarray, out: np.ndarray | None = None
     xi = np.ascontiguousarray(xi, np.float64)
     out = np.empty(state.vec_len) if out is None else out
     _check(lib().fwi_dev_kkt_apply_host(state.h, _p(xi), _p(out)))
+    return out
+
+
+def gradient(state: GnState) -> np.ndarray:
+    """fwi::gradient (src/reduced_space.cpp:141-152): Re(J^H W^T W r) - eps s."""
+    out = np.empty(state.n)
+    _check(lib().fwi_dev_gradient(state.h, _p(out)))
+    return out
+
+
+def hessian_apply(state: GnState, v: np.ndarray) -> np.ndarray:
+    """fwi::hessian_apply (src/reduced_space.cpp:120-139): Re(J^H W^T W J v) + eps v."""
+    v = np.ascontiguousarray(v, np.float64)
+    out = np.empty(state.n)
+    _check(lib().fwi_dev_hessian_apply(state.h, _p(v), _p(out)))
     return out
 
 

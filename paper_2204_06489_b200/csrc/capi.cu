@@ -17,6 +17,8 @@ struct fwi_dev_vec {
 
 namespace fwi_b200 {
 void rsgn_cg_step(Ctx& c, double tol, int maxit, double* ds_host, fwi_convergence_log* log);
+void reduced_gradient(Ctx& c, double* g_dev);
+void reduced_hessian(Ctx& c, const double* v_dev, double* out_dev);
 void gn_step(const fwi_state_desc& d0, const fwi_gn_options& o, double* s_out, fwi_gn_result* res,
              fwi_convergence_log* log);
 void gmres_generic(int64_t n, fwi_op_cb apply, fwi_op_cb precond, fwi_observer_cb observer, void* user,
@@ -116,7 +118,7 @@ int fwi_dev_ctx_info(const fwi_dev_ctx* ctx, fwi_state_info* o) {
         o->has_ilu = c.ilu != nullptr;
         o->vec_doubles = 4 * int64_t(c.K) * c.n + c.n;
         o->device_bytes = int64_t(c.diag.bytes() * 3 + c.u.bytes() + c.u32.bytes() + c.s.bytes() +
-                                  exact_bytes(c.exact) + c.work_a.bytes() * 3);
+                                  exact_bytes(c.exact) + c.work_a.bytes() + c.work_b.bytes() + c.work_c.bytes());
     });
 }
 
@@ -399,6 +401,34 @@ int fwi_dev_fsgn_gmres_step(fwi_dev_ctx* ctx, const fwi_fsgn_options* opt, doubl
         need(ctx, "ctx");
         need(opt, "options");
         fsgn_gmres_step(*ctx->c, *opt, ds, log);
+    });
+}
+
+int fwi_dev_gradient(fwi_dev_ctx* ctx, double* g_host) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(g_host, "g");
+        Ctx& c = *ctx->c;
+        require(c.exact != nullptr, "gradient: state has no exact factorization");
+        DevBuf<double> g(c.n);
+        reduced_gradient(c, g.p);
+        CK(cudaMemcpyAsync(g_host, g.p, c.n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int fwi_dev_hessian_apply(fwi_dev_ctx* ctx, const double* v_host, double* out_host) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(v_host, "v");
+        need(out_host, "out");
+        Ctx& c = *ctx->c;
+        require(c.exact != nullptr, "hessian_apply: state has no exact factorization");
+        DevBuf<double> v(c.n), h(c.n);
+        CK(cudaMemcpyAsync(v.p, v_host, c.n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+        reduced_hessian(c, v.p, h.p);
+        CK(cudaMemcpyAsync(out_host, h.p, c.n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
     });
 }
 

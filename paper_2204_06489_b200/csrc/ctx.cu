@@ -110,14 +110,12 @@ Ctx::~Ctx() {
     if (stream) cudaStreamDestroy(stream);
 }
 
-void Ctx::ensure_work() {
+void Ctx::ensure_work(unsigned which) {
     const size_t kn = size_t(K) * n;
-    if (work_a.count < kn) {
-        work_a.alloc(kn);
-        work_b.alloc(kn);
-        work_c.alloc(kn);
-        work_ds.alloc(ds_stride);
-    }
+    if ((which & kWorkA) && work_a.count < kn) work_a.alloc(kn);
+    if ((which & kWorkB) && work_b.count < kn) work_b.alloc(kn);
+    if ((which & kWorkC) && work_c.count < kn) work_c.alloc(kn);
+    if (work_ds.count < size_t(ds_stride)) work_ds.alloc(ds_stride);
 }
 
 Ctx* ctx_create(const fwi_state_desc& d) {

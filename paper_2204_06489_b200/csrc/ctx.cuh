@@ -79,7 +79,9 @@ struct Ctx {
     double2* la_of(double* base) const {
         return reinterpret_cast<double2*>(base + 2 * int64_t(K) * n + ds_stride);
     }
-    void ensure_work();
+    // K x n scratch, allocated on first use: kWorkA | kWorkB | kWorkC (+ ds scratch)
+    static constexpr unsigned kWorkA = 1, kWorkB = 2, kWorkC = 4;
+    void ensure_work(unsigned which = kWorkA | kWorkB | kWorkC);
 };
 
 struct Vec {
@@ -110,6 +112,10 @@ void dev_scal(cudaStream_t st, double a, double* x, int64_t len);
 void dev_mgs_step(cudaStream_t st, double* w, const double* vprev, const double* hprev_dev,
                   const double* vnext, double* h_out_dev, double* partials, unsigned* ticket,
                   int64_t len);
+// chunk version of dev_mgs_step: per-CTA partials (reduce_blocks() of them) to partials_out
+void dev_mgs_step_parts(cudaStream_t st, double* w, const double* vprev, const double* hprev_dev,
+                        const double* vnext, double* partials_out, int64_t len);
+void dev_sum_ordered(cudaStream_t st, const double* partials, int count, double* out_dev);
 void dev_multi_axpy(cudaStream_t st, double* out, const double* x, const double* const* v,
                     const double* y, int m, int64_t len);
 void dev_sub_norm2(cudaStream_t st, const double* b, const double* ax, double* out_dev,

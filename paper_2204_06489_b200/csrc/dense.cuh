@@ -1,0 +1,29 @@
+// dense.cuh — whole-GPU dense kernels of the long-line exact solver (dense.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace fwi_b200 {
+
+constexpr int kDenseBlk = 64;  // Gauss-Jordan block width
+
+// C = (C0 ? C0 : 0) + alpha * A B, complex double; B(k,n) = B[k*ldb+n] or, with bt, B[n*ldb+k]
+void cgemm(cudaStream_t st, bool bt, int M, int N, int K, double alpha, const double2* A, int64_t lda,
+           const double2* B, int64_t ldb, const double2* C0, int64_t ldc0, double2* C, int64_t ldc);
+
+struct DenseWork {
+    DevBuf<double2> F, Ablk, R, Dinv;
+    int nb_ = 0;
+    void ensure(int nb);
+};
+
+// A (nb x nb, row pitch lda) <- A^{-1}; block Gauss-Jordan with pivoting inside the
+// 64-wide diagonal blocks. A zero pivot sets *status = status_base + column + 1.
+void dense_invert(cudaStream_t st, int nb, double2* A, int64_t lda, DenseWork& w, int* status, int status_base);
+
+// Forward/backward line sweeps for nrhs right-hand sides in W[i][k][m] (overwritten
+// in place by y, then by the solution); T is nrhs x nb scratch.
+void dense_sweep(cudaStream_t st, int L, int nb, int nrhs, const double2* G, int64_t gp, const double2* coup,
+                 double2* W, double2* T);
+
+}  // namespace fwi_b200

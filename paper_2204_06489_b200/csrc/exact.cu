@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "ctx.cuh"
+#include "dense.cuh"
 
 namespace fwi_b200 {
 
@@ -42,6 +43,9 @@ struct ExactFactor {
     DevBuf<double2> work;   // nb x nb scratch (global-memory inversion)
     DevBuf<double2> ybuf;   // forward-sweep results of the cluster sweep
     DevBuf<int> status;
+    bool dense = false;     // long lines: whole-GPU block Gauss-Jordan + GEMM sweeps (dense.cu)
+    DenseWork dwork;
+    DevBuf<double2> tbuf;   // dense sweep operand (nrhs x nb)
 };
 
 void exact_free(ExactFactor* f) { delete f; }
@@ -66,6 +70,29 @@ __global__ void extract_lines(bool col_lines, int nx, int L, int nb, const doubl
     const int i = int(t / nb), m = int(t % nb);
     const int64_t node = line_node(col_lines, nx, i, m);
     coup[t] = col_lines ? east[node] : south[node];
+}
+
+// S_i = T_i - E_{i-1} G_{i-1} E_{i-1} into A (row pitch lda), one thread per entry
+__global__ void form_schur(bool col_lines, int nx, int nb, int line, const double2* __restrict__ diag,
+                           const double2* __restrict__ east, const double2* __restrict__ south,
+                           const double2* __restrict__ coup, const double2* __restrict__ Gprev, int gp,
+                           double2* __restrict__ A) {
+    const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (t >= int64_t(nb) * nb) return;
+    const int a = int(t / nb), b = int(t % nb);
+    double2 v = make_double2(0.0, 0.0);
+    const int64_t na = line_node(col_lines, nx, line, a);
+    if (a == b) v = diag[na];
+    else if (b == a + 1) v = col_lines ? south[na] : east[na];
+    else if (a == b + 1) v = col_lines ? south[line_node(col_lines, nx, line, b)]
+                                       : east[line_node(col_lines, nx, line, b)];
+    if (line > 0) {
+        const double2 ea = coup[int64_t(line - 1) * nb + a], eb = coup[int64_t(line - 1) * nb + b];
+        const double2 t2 = fmul(fmul(ea, Gprev[int64_t(a) * gp + b]), eb);
+        v.x -= t2.x;
+        v.y -= t2.y;
+    }
+    A[int64_t(a) * gp + b] = v;
 }
 
 // Form S_i (row-major, in A) from the line's tridiagonal block and G_{i-1},
@@ -1088,6 +1115,18 @@ void exact_factor(Ctx& c) {
     extract_lines<<<grid_blocks(int64_t(L) * nb, 256, 1 << 20), 256, 0, c.stream>>>(
         f->col_lines, c.nx, L, nb, c.east.p, c.south.p, f->coup.p);
     CK_LAUNCH();
+    f->dense = nb > 512 || std::getenv("FWI_EXACT_DENSE") != nullptr;
+    if (f->dense) {
+        const int64_t nn = int64_t(nb) * nb;
+        for (int i = 0; i < L; ++i) {
+            double2* Gi = f->G.p + i * int64_t(nb) * f->gp;
+            form_schur<<<int((nn + 255) / 256), 256, 0, c.stream>>>(
+                f->col_lines, c.nx, nb, i, c.diag.p, c.east.p, c.south.p, f->coup.p,
+                i > 0 ? Gi - int64_t(nb) * f->gp : nullptr, f->gp, Gi);
+            CK_LAUNCH();
+            dense_invert(c.stream, nb, Gi, f->gp, f->dwork, f->status.p, i * nb);
+        }
+    } else {
     const bool smem = nb <= 112;
     const size_t base = size_t(2 * nb) * sizeof(double2) + size_t((nb + 3) & ~3) * sizeof(int);
     const size_t shm = base + (smem ? size_t(nb) * nb * sizeof(double2) : 0);
@@ -1110,6 +1149,7 @@ void exact_factor(Ctx& c) {
                 f->G.p + i * int64_t(nb) * f->gp, f->gp, f->work.p, f->status.p);
         CK_LAUNCH();
     }
+    }
     int st = 0;
     CK(cudaMemcpyAsync(&st, f->status.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
@@ -1123,7 +1163,7 @@ void exact_factor(Ctx& c) {
 void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int nrhs) {
     require(c.exact != nullptr, "precond_apply: state has no exact factorization");
     const ExactFactor& f = *c.exact;
-    c.ensure_work();
+    c.ensure_work(Ctx::kWorkC);
     DevBuf<double2> tmp;  // only for batches larger than K (freed synchronously)
     double2* W = c.work_c.p;
     if (size_t(nrhs) * c.n > c.work_c.count) {
@@ -1143,9 +1183,15 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
     gather_lines<<<tg, tb, 0, c.stream>>>(f.col_lines, c.nx, c.nz, f.L, f.nb, nrhs, adjoint, b, W);
     CK_LAUNCH();
     bool done = false;
+    if (f.dense) {
+        ExactFactor& fm = const_cast<ExactFactor&>(f);
+        if (fm.tbuf.count < size_t(nrhs) * f.nb) fm.tbuf.alloc(size_t(nrhs) * f.nb);
+        dense_sweep(c.stream, f.L, f.nb, nrhs, f.G.p, f.gp, f.coup.p, W, fm.tbuf.p);
+        done = true;
+    }
     const char* sw = std::getenv("FWI_EXACT_SWEEP");  // "warp" (default) | "cta" | "legacy"
     const std::string sweep = sw ? sw : "warp";
-    if (sweep == "warp") {
+    if (!done && sweep == "warp") {
         // plans are cached per (nb, L, nrhs): the model queries cluster occupancy
         static std::vector<std::pair<std::array<int, 3>, WarpPlan>> cache;
         const std::array<int, 3> key{f.nb, f.L, nrhs};

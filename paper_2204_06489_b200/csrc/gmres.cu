@@ -10,7 +10,10 @@
 // memory until one D2H copy per iteration; x_cand = x + V y is one fused pass
 // with the reference's per-basis-vector rounding order; the true residual
 // ||b - A x_cand|| is a KKT apply plus one fused difference-norm pass.
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <functional>
 #include <optional>
@@ -68,6 +71,89 @@ double dnorm(Scratch& s, cudaStream_t st, const double* x, int64_t len) {
     return std::sqrt(h);
 }
 
+// Krylov basis storage. Normally every basis vector is a device buffer. When the
+// working set does not fit in HBM (BASELINE config 5: one KKT vector is 17.2 GB,
+// SURVEY §7 hard part 3) the basis vectors beyond the device budget live in
+// pinned host memory and are streamed through two device staging chunks; the
+// newest basis vector is always kept on the device as well (it feeds the next
+// operator apply and the last MGS step), and the best iterate is kept on the
+// host. Arithmetic is unchanged except for the reduction order of the chunked
+// dot products (per-chunk partials summed in chunk order).
+struct Basis {
+    int64_t len = 0;
+    cudaStream_t st = nullptr;
+    std::vector<DevBuf<double>> dev;  // device slots (index < ndev)
+    std::vector<double*> host;        // pinned slots (index >= ndev)
+    int ndev = 0;
+    DevBuf<double> vlast;             // device copy of the newest host-resident vector
+    int vlast_index = -1;
+    DevBuf<double> stage[2], parts;
+    int64_t chunk = 0;
+    int nchunks = 0;
+
+    ~Basis() {
+        for (double* h : host)
+            if (h) cudaFreeHost(h);
+    }
+    bool on_host(int i) const { return i >= ndev; }
+    void ensure_host(int i) {
+        if (!host[i]) CK(cudaMallocHost(&host[i], size_t(len) * sizeof(double)));
+    }
+    // device pointer of v_i if it is device-resident (or the cached newest vector), else null
+    const double* dptr(int i) const {
+        if (!on_host(i)) return dev[i].p;
+        return i == vlast_index ? vlast.p : nullptr;
+    }
+    const double* stage_chunk(int slot, int i, int64_t off, int64_t cl) {
+        if (const double* d = dptr(i)) return d + off;
+        CK(cudaMemcpyAsync(stage[slot].p, host[i] + off, size_t(cl) * sizeof(double), cudaMemcpyHostToDevice, st));
+        return stage[slot].p;
+    }
+};
+
+// w -= h_{i-1} v_{i-1}; h_i = <v_i, w>  (vi < 0: <w, w>)
+void mgs_step_any(Scratch& sc, Basis& B, double* w, int iprev, const double* hprev, int inext, double* hout) {
+    const bool dev_prev = iprev < 0 || B.dptr(iprev), dev_next = inext < 0 || B.dptr(inext);
+    if (dev_prev && dev_next) {
+        dev_mgs_step(B.st, w, iprev >= 0 ? B.dptr(iprev) : nullptr, hprev, inext >= 0 ? B.dptr(inext) : nullptr,
+                     hout, sc.partials.p, sc.ticket.p, B.len);
+        return;
+    }
+    const int rb = reduce_blocks();
+    for (int c = 0; c < B.nchunks; ++c) {
+        const int64_t off = c * B.chunk, cl = std::min(B.chunk, B.len - off);
+        const double* pv = iprev >= 0 ? B.stage_chunk(0, iprev, off, cl) : nullptr;
+        const double* nv = inext >= 0 ? B.stage_chunk(1, inext, off, cl) : nullptr;
+        dev_mgs_step_parts(B.st, w + off, pv, hprev, nv, B.parts.p + int64_t(c) * rb, cl);
+    }
+    dev_sum_ordered(B.st, B.parts.p, B.nchunks * rb, hout);
+}
+
+// out = x + sum_i y_i v_i, one basis vector at a time in index order (the fused
+// kernel's rounding order)
+void multi_axpy_any(Basis& B, double* out, const double* x, const std::vector<double>& y, const double* ydev,
+                    int m) {
+    bool all_dev = true;
+    for (int i = 0; i < m; ++i) all_dev = all_dev && B.dptr(i);
+    if (all_dev) {
+        std::vector<const double*> vp(m);
+        for (int i = 0; i < m; ++i) vp[i] = B.dptr(i);
+        dev_multi_axpy(B.st, out, x, vp.data(), ydev, m, B.len);
+        return;
+    }
+    CK(cudaMemcpyAsync(out, x, size_t(B.len) * sizeof(double), cudaMemcpyDeviceToDevice, B.st));
+    for (int i = 0; i < m; ++i) {
+        if (const double* d = B.dptr(i)) {
+            dev_axpy(B.st, y[i], d, out, B.len);
+            continue;
+        }
+        for (int c = 0; c < B.nchunks; ++c) {
+            const int64_t off = c * B.chunk, cl = std::min(B.chunk, B.len - off);
+            dev_axpy(B.st, y[i], B.stage_chunk(c & 1, i, off, cl), out + off, cl);
+        }
+    }
+}
+
 // x (device, len) receives the solution.
 Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double tol, int maxit) {
     if (restart < 1) throw FwiError(FWI_ERR_INVALID_ARGUMENT, "gmres: restart must be >= 1");
@@ -87,19 +173,79 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
         log.converged = true;
         return log;
     }
-    DevBuf<double> tmp(len), w(len), xc(len), best(len);
+    const int nbasis = std::min(restart, std::max(maxit, 1)) + 1;
+    // ---- storage plan: tmp, w, xc (+ best, + basis) on the device if they fit
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t margin = size_t(2) << 30;
+    const bool force_host = std::getenv("FWI_GMRES_HOST_BASIS") != nullptr;
+    const bool host_mode = force_host || (size_t(4 + nbasis + 1) * bytes + margin > free_b);
+    Basis B;
+    B.len = len;
+    B.st = st;
+    B.dev.resize(nbasis);
+    B.host.assign(nbasis, nullptr);
+    double* best_host = nullptr;
+    DevBuf<double> tmp(len), w(len), xc(len), best;
+    if (!host_mode) {
+        best.alloc(len);
+        B.ndev = nbasis;
+    } else {
+        B.chunk = std::min<int64_t>(len, int64_t(32) << 20);
+        B.chunk -= B.chunk % 2;
+        B.nchunks = int((len + B.chunk - 1) / B.chunk);
+        B.stage[0].alloc(B.chunk);
+        B.stage[1].alloc(B.chunk);
+        B.parts.alloc(size_t(B.nchunks) * reduce_blocks());
+        B.vlast.alloc(len);
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        const int fit = free_b > margin ? int((free_b - margin) / bytes) : 0;
+        B.ndev = force_host ? std::min(1, std::min(fit, nbasis)) : std::min(fit, nbasis);
+        CK(cudaMallocHost(&best_host, bytes));
+        std::memset(best_host, 0, bytes);
+    }
+    struct HostFree {
+        double* p;
+        ~HostFree() {
+            if (p) cudaFreeHost(p);
+        }
+    } best_guard{best_host};
+    auto save_best = [&](const double* src) {
+        if (best_host) {
+            CK(cudaMemcpyAsync(best_host, src, bytes, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        } else {
+            CK(cudaMemcpyAsync(best.p, src, bytes, cudaMemcpyDeviceToDevice, st));
+        }
+    };
+    auto load_best = [&](double* dst) {
+        CK(cudaMemcpyAsync(dst, best_host ? best_host : best.p, bytes,
+                           best_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+    };
+    // store the normalised vector in `src` (a device buffer we own) as basis vector i
+    auto put_basis = [&](int i, DevBuf<double>& src) {
+        if (!B.on_host(i)) {
+            std::swap(B.dev[i], src);
+            if (!src.p) src.alloc(len);
+        } else {
+            B.ensure_host(i);
+            CK(cudaMemcpyAsync(B.host[i], src.p, bytes, cudaMemcpyDeviceToHost, st));
+            std::swap(B.vlast, src);  // device copy of the newest vector; src reuses the old one
+            B.vlast_index = i;
+        }
+    };
+
     ops.precond(b, w.p);
     const double pbnorm = dnorm(sc, st, w.p, len);
     if (pbnorm == 0.0)
         throw FwiError(FWI_ERR_INVALID_ARGUMENT, "gmres: preconditioner annihilates the right-hand side");
     log.entries.push_back({0, 1.0, {}, 1.0, elapsed()});
 
-    CK(cudaMemsetAsync(best.p, 0, bytes, st));
+    if (best_host) std::memset(best_host, 0, bytes);
+    else CK(cudaMemsetAsync(best.p, 0, bytes, st));
     double best_res = 1.0, true_res = 1.0;
     int iter = 0;
     bool stop_requested = false;
-    const int nbasis = std::min(restart, std::max(maxit, 1)) + 1;
-    std::vector<DevBuf<double>> V(nbasis);
     DevBuf<double> hdev(size_t(restart) + 2), ydev(size_t(restart) + 1);
     std::vector<double> hh(restart + 2);
 
@@ -108,29 +254,26 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
         ops.apply(x, tmp.p);
         CK(cudaMemcpyAsync(xc.p, b, bytes, cudaMemcpyDeviceToDevice, st));
         dev_axpy(st, -1.0, tmp.p, xc.p, len);
-        if (!V[0].p) V[0].alloc(len);
-        ops.precond(xc.p, V[0].p);
-        const double beta = dnorm(sc, st, V[0].p, len);
+        ops.precond(xc.p, w.p);
+        const double beta = dnorm(sc, st, w.p, len);
         const double cycle_start_res = true_res;
         if (beta == 0.0) break;
-        dev_scal(st, 1.0 / beta, V[0].p, len);
+        dev_scal(st, 1.0 / beta, w.p, len);
+        put_basis(0, w);
 
         std::vector<std::vector<double>> hcols;
         std::vector<double> gs_c, gs_s, g(1, beta);
         CK(cudaMemcpyAsync(xc.p, x, bytes, cudaMemcpyDeviceToDevice, st));
         bool happy = false;
-        int nv = 1;
 
         for (int j = 0; j < restart && iter < maxit; ++j) {
             ++iter;
-            ops.apply(V[j].p, tmp.p);
+            ops.apply(B.dptr(j), tmp.p);
             ops.precond(tmp.p, w.p);
             // MGS: h_i = <v_i, w>; w -= h_i v_i  (fused pairwise)
             for (int i = 0; i <= j; ++i)
-                dev_mgs_step(st, w.p, i > 0 ? V[i - 1].p : nullptr, hdev.p + (i - 1), V[i].p,
-                             hdev.p + i, sc.partials.p, sc.ticket.p, len);
-            dev_mgs_step(st, w.p, V[j].p, hdev.p + j, nullptr, hdev.p + j + 1, sc.partials.p,
-                         sc.ticket.p, len);
+                mgs_step_any(sc, B, w.p, i - 1, hdev.p + (i - 1), i, hdev.p + i);
+            mgs_step_any(sc, B, w.p, j, hdev.p + j, -1, hdev.p + j + 1);
             CK(cudaMemcpyAsync(hh.data(), hdev.p, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             std::vector<double> h(hh.begin(), hh.begin() + j + 2);
@@ -176,9 +319,7 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
                 y[i] = acc / hcols[i][i];
             }
             CK(cudaMemcpyAsync(ydev.p, y.data(), (j + 1) * sizeof(double), cudaMemcpyHostToDevice, st));
-            std::vector<const double*> vp(j + 1);
-            for (int i = 0; i <= j; ++i) vp[i] = V[i].p;
-            dev_multi_axpy(st, xc.p, x, vp.data(), ydev.p, j + 1, len);
+            multi_axpy_any(B, xc.p, x, y, ydev.p, j + 1);
 
             ops.apply(xc.p, tmp.p);
             dev_sub_norm2(st, b, tmp.p, sc.out.p, sc.partials.p, sc.ticket.p, len);
@@ -189,7 +330,7 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
             log.entries.push_back({iter, true_res, {}, prec_res, elapsed()});
             if (true_res < best_res) {
                 best_res = true_res;
-                CK(cudaMemcpyAsync(best.p, xc.p, bytes, cudaMemcpyDeviceToDevice, st));
+                save_best(xc.p);
             }
             if (ops.observer) {
                 const auto to0 = std::chrono::steady_clock::now();
@@ -199,22 +340,20 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
             if (true_res <= tol) log.converged = true;
             if (wn == 0.0) happy = true;
             if (log.converged || stop_requested || happy) break;
-            // v_{j+1} = w / ||w||  (buffer rotation, no copy)
+            if (j + 1 >= restart) break;  // the next basis vector would be discarded by the restart
+            // v_{j+1} = w / ||w||
             dev_scal(st, 1.0 / wn, w.p, len);
-            std::swap(V[j + 1], w);
-            if (!w.p) w.alloc(len);
-            nv = j + 2;
+            put_basis(j + 1, w);
         }
-        (void)nv;
         CK(cudaMemcpyAsync(x, xc.p, bytes, cudaMemcpyDeviceToDevice, st));
         if (!log.converged && !stop_requested && true_res >= cycle_start_res * (1.0 - 1e-12)) {
             log.stagnated = true;
-            CK(cudaMemcpyAsync(x, best.p, bytes, cudaMemcpyDeviceToDevice, st));
+            load_best(x);
             break;
         }
         if (happy && !log.converged && !stop_requested) {
             log.stagnated = true;
-            CK(cudaMemcpyAsync(x, best.p, bytes, cudaMemcpyDeviceToDevice, st));
+            load_best(x);
             break;
         }
     }

@@ -108,7 +108,6 @@ void block_solve(Ctx& c, int mode, bool adjoint, const double2* b, double2* x, i
 void precond_apply_raw(Ctx& c, int mode, const double* v, double* out) {
     if (mode == FWI_PRECOND_ILU) require(c.ilu != nullptr, "precond_apply: state has no ILU factorization");
     if (mode == FWI_PRECOND_EXACT) require(c.exact != nullptr, "precond_apply: state has no exact factorization");
-    c.ensure_work();
     const int K = c.K;
     const int64_t n = c.n, kn = int64_t(K) * n;
     double* vv = const_cast<double*>(v);
@@ -119,10 +118,12 @@ void precond_apply_raw(Ctx& c, int mode, const double* v, double* out) {
                                                   c.ds_of(out));
     CK_LAUNCH();
     // (3)
+    // the right-hand side is built in out.du and solved in place (both block solvers
+    // read their whole input before writing)
     precond_rhs_kernel<<<ew(kn), 256, 0, c.stream>>>(kn, n, c.w2, c.u.p, c.ds_of(out), c.la_of(vv),
-                                                    c.work_a.p);
+                                                    c.du_of(out));
     CK_LAUNCH();
-    block_solve(c, mode, false, c.work_a.p, c.du_of(out), K);
+    block_solve(c, mode, false, c.du_of(out), c.du_of(out), K);
 }
 
 void precond_apply(Ctx& c, int mode, const Vec& v, Vec& out) {
@@ -134,23 +135,26 @@ void precond_apply(Ctx& c, int mode, const Vec& v, Vec& out) {
 
 // g = Re(J^H W^T W r) - eps s (gradient, src/reduced_space.cpp:141-152)
 void reduced_gradient(Ctx& c, double* g_dev) {
-    c.ensure_work();
     const int K = c.K;
     const int64_t n = c.n, kn = int64_t(K) * n;
-    CK(cudaMemsetAsync(c.work_a.p, 0, kn * sizeof(double2), c.stream));
+    // scratch of its own (freed on return): the gradient runs once per Newton step and
+    // must not keep K x n of HBM from the Krylov basis at config 5
+    DevBuf<double2> a(kn);
+    CK(cudaMemsetAsync(a.p, 0, kn * sizeof(double2), c.stream));
     if (c.ndata)
         weighted_scatter_kernel<<<(K + 127) / 128, 128, 0, c.stream>>>(
-            K, n, c.recv_offset.p, c.recv_node.p, c.w.p, nullptr, c.r.p, c.work_a.p);
+            K, n, c.recv_offset.p, c.recv_node.p, c.w.p, nullptr, c.r.p, a.p);
     CK_LAUNCH();
-    exact_solve_batch(c, true, c.work_a.p, c.work_b.p, K);
-    reduce_padj_kernel<<<ew(n), 256, 0, c.stream>>>(K, n, c.w2, c.u.p, c.work_b.p,
-                                                   c.drop ? nullptr : c.s.p, -c.eps, g_dev);
+    exact_solve_batch(c, true, a.p, a.p, K);  // in place
+    reduce_padj_kernel<<<ew(n), 256, 0, c.stream>>>(K, n, c.w2, c.u.p, a.p, c.drop ? nullptr : c.s.p, -c.eps,
+                                                   g_dev);
     CK_LAUNCH();
+    CK(cudaStreamSynchronize(c.stream));
 }
 
 // H v = Re(J^H W^T W J v) + eps v (hessian_apply, src/reduced_space.cpp:120-139)
 void reduced_hessian(Ctx& c, const double* v_dev, double* out_dev) {
-    c.ensure_work();
+    c.ensure_work(Ctx::kWorkA | Ctx::kWorkB);
     const int K = c.K;
     const int64_t n = c.n, kn = int64_t(K) * n;
     apply_p_kernel<<<ew(kn), 256, 0, c.stream>>>(kn, n, c.w2, c.u.p, v_dev, c.work_a.p);

@@ -126,6 +126,42 @@ __global__ void __launch_bounds__(kRedThreads) mgs_kernel(double2* __restrict__ 
     finish_reduction(acc, partials, ticket, out);
 }
 
+// The same fused MGS step over one chunk of the vector, leaving its per-CTA
+// partial sums in partials_out (host-resident basis: chunks are staged through
+// device buffers and the partials of all chunks are summed in order afterwards).
+__global__ void __launch_bounds__(kRedThreads) mgs_partial_kernel(double2* __restrict__ w,
+                                                                  const double2* __restrict__ vprev,
+                                                                  const double* __restrict__ hprev,
+                                                                  const double2* __restrict__ vnext, int64_t m,
+                                                                  double* partials_out) {
+    __shared__ double sh[32];
+    const double nh = vprev ? -*hprev : 0.0;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        double2 wv = w[i];
+        if (vprev) {
+            const double2 pv = vprev[i];
+            wv.x = __dadd_rn(wv.x, __dmul_rn(nh, pv.x));
+            wv.y = __dadd_rn(wv.y, __dmul_rn(nh, pv.y));
+            w[i] = wv;
+        }
+        const double2 nv = vnext ? vnext[i] : wv;
+        acc += nv.x * wv.x + nv.y * wv.y;
+    }
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) partials_out[blockIdx.x] = acc;
+}
+
+__global__ void __launch_bounds__(kRedThreads) sum_ordered_kernel(const double* __restrict__ p, int count,
+                                                                  double* out) {
+    __shared__ double sh[32];
+    double v = 0.0;
+    for (int i = threadIdx.x; i < count; i += blockDim.x) v += p[i];
+    v = block_sum(v, sh);
+    if (threadIdx.x == 0) *out = v;
+}
+
 struct MultiAxpyArgs {
     const double2* v[64];
 };
@@ -204,6 +240,19 @@ void dev_mgs_step(cudaStream_t st, double* w, const double* vprev, const double*
     mgs_kernel<<<reduce_blocks(), kRedThreads, 0, st>>>(
         reinterpret_cast<double2*>(w), reinterpret_cast<const double2*>(vprev), hprev_dev,
         reinterpret_cast<const double2*>(vnext), len / 2, partials, ticket, h_out_dev);
+    CK_LAUNCH();
+}
+
+void dev_mgs_step_parts(cudaStream_t st, double* w, const double* vprev, const double* hprev_dev,
+                        const double* vnext, double* partials_out, int64_t len) {
+    mgs_partial_kernel<<<reduce_blocks(), kRedThreads, 0, st>>>(
+        reinterpret_cast<double2*>(w), reinterpret_cast<const double2*>(vprev), hprev_dev,
+        reinterpret_cast<const double2*>(vnext), len / 2, partials_out);
+    CK_LAUNCH();
+}
+
+void dev_sum_ordered(cudaStream_t st, const double* partials, int count, double* out_dev) {
+    sum_ordered_kernel<<<1, kRedThreads, 0, st>>>(partials, count, out_dev);
     CK_LAUNCH();
 }
 

@@ -1,0 +1,101 @@
+"""The long-line exact solver (dense.cu: whole-GPU block Gauss-Jordan + GEMM sweeps, used
+for nb > 512, i.e. BASELINE config 5) forced onto small grids with FWI_EXACT_DENSE=1 and
+checked against the reference LU (oracle/_ref) on the same seeded inputs."""
+import os
+
+import numpy as np
+import pytest
+
+import pyoracle as po
+from paper_2204_06489_b200 import _abi
+from paper_2204_06489_b200 import api as fw
+from paper_2204_06489_b200.problem import c1_problem, random_kkt, small_problem, standard_instance
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def dense_state(p, **kw):
+    os.environ["FWI_EXACT_DENSE"] = "1"
+    try:
+        return fw.GnState(p, exact=True, **kw)
+    finally:
+        del os.environ["FWI_EXACT_DENSE"]
+
+
+@pytest.mark.parametrize("mk", [small_problem, standard_instance,
+                                lambda: small_problem(nx=70, nz=90, n_pml=5, K=2, R=4)])
+def test_dense_block_solve_matches_reference_lu(mk):
+    p = mk()
+    ref = po.Ref(p, full=False, exact=True)
+    dev = dense_state(p)
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal((3, p.n)) + 1j * rng.standard_normal((3, p.n))
+    for adj in (False, True):
+        for r in range(3):
+            want = ref.solve(b[r], _abi.FWI_PRECOND_EXACT, adj)
+            got = dev.solve(b[r], fw.PrecondMode.exact, adj)
+            assert rel(got, want) <= 1e-10, (adj, rel(got, want))
+
+
+def test_dense_solve_residual_c1():
+    """||A x - b|| / ||b|| of the dense solve, with A the reference's assembled CSR."""
+    import scipy.sparse as sp
+    p = c1_problem()
+    p.d_obs = po.ref_simulate(p)
+    ref = po.Ref(p, full=True, exact=False)
+    rp, ci, va = ref.csr()
+    A = sp.csr_matrix((va, ci, rp), shape=(p.n, p.n))
+    q = c1_problem()
+    q.d_obs, q.u, q.r = p.d_obs, ref.u(), ref.residual()
+    dev = dense_state(q)
+    rng = np.random.default_rng(3)
+    b = rng.standard_normal(p.n) + 1j * rng.standard_normal(p.n)
+    x = dev.solve(b, fw.PrecondMode.exact, False)
+    assert np.linalg.norm(A @ x - b) / np.linalg.norm(b) < 1e-11
+    xa = dev.solve(b, fw.PrecondMode.exact, True)
+    assert np.linalg.norm(A.conj().T @ xa - b) / np.linalg.norm(b) < 1e-11
+
+
+def test_dense_precond_and_gmres_history_c1():
+    p = c1_problem()
+    p.d_obs = po.ref_simulate(p)
+    ref = po.Ref(p, full=True, exact=True)
+    q = c1_problem()
+    q.d_obs, q.u, q.r = p.d_obs, ref.u(), ref.residual()
+    dev = dense_state(q)
+    x = random_kkt(p, 9)
+    want = ref.precond_apply(x, _abi.FWI_PRECOND_EXACT)
+    got = fw.precond_apply(dev, fw.KktVector.from_host(dev, x), fw.PrecondMode.exact).to_host()
+    assert rel(got, want) <= 1e-10
+    _, log_r = ref.fsgn(_abi.FWI_PRECOND_EXACT, 30, 0.0, 30, 0)
+    _, log_d = fw.fsgn_gmres_step(dev, fw.FsgnOptions(restart=30, tol=0.0, maxit=30, ecg_stride=0))
+    rr, rd = np.array(log_r.residuals()), np.array(log_d.residuals())
+    assert len(rr) == len(rd)
+    mask = rr >= 1e-6
+    assert (np.abs(rd - rr)[mask] / rr[mask]).max() <= 1e-8
+
+
+def test_host_basis_gmres_history_matches_reference_c1():
+    """GMRES with the Krylov basis in pinned host memory (the config-5 storage plan,
+    forced with FWI_GMRES_HOST_BASIS=1) keeps the reference's residual history."""
+    p = c1_problem()
+    p.d_obs = po.ref_simulate(p)
+    ref = po.Ref(p, full=True, exact=True)
+    q = c1_problem()
+    q.d_obs, q.u, q.r = p.d_obs, ref.u(), ref.residual()
+    dev = fw.GnState(q, exact=True)
+    _, log_r = ref.fsgn(_abi.FWI_PRECOND_EXACT, 4, 0.0, 20, 0)
+    os.environ["FWI_GMRES_HOST_BASIS"] = "1"
+    try:
+        ds_d, log_d = fw.fsgn_gmres_step(dev, fw.FsgnOptions(restart=4, tol=0.0, maxit=20, ecg_stride=0))
+    finally:
+        del os.environ["FWI_GMRES_HOST_BASIS"]
+    rr, rd = np.array(log_r.residuals()), np.array(log_d.residuals())
+    assert len(rr) == len(rd)
+    mask = rr >= 1e-6
+    assert (np.abs(rd - rr)[mask] / rr[mask]).max() <= 1e-8
+    assert log_d.stagnated == log_r.stagnated

@@ -384,3 +384,16 @@ def test_rsgn_cg_matches_reference_and_agrees_with_fsgn(c1):
     ds_cg, _ = fw.rsgn_cg_step(dv, 1e-12, 400)
     ds_gm, _ = fw.fsgn_gmres_step(dv, fw.FsgnOptions(tol=1e-12, maxit=400, ecg_stride=0))
     assert rel(ds_gm, ds_cg) < 1e-5
+
+
+def test_gradient_matches_reference(c1):
+    """gradient (src/reduced_space.cpp:141-152): K adjoint exact solves."""
+    p, ref, dev = c1
+    assert rel(fw.gradient(dev), ref.gradient()) <= 1e-10
+
+
+def test_hessian_apply_matches_reference(c1):
+    """hessian_apply (src/reduced_space.cpp:120-139): 2K exact solves."""
+    p, ref, dev = c1
+    v = np.random.default_rng(17).standard_normal(p.n)
+    assert rel(fw.hessian_apply(dev, v), ref.hessian_apply(v)) <= 1e-10
