@@ -43,7 +43,8 @@ struct ExactFactor {
     DevBuf<double2> work;   // nb x nb scratch (global-memory inversion)
     DevBuf<double2> ybuf;   // forward-sweep results of the cluster sweep
     DevBuf<int> status;
-    bool dense = false;     // long lines: whole-GPU block Gauss-Jordan + GEMM sweeps (dense.cu)
+    bool dense = false;     // long lines: GEMM line sweeps (dense.cu)
+    bool dense_factor = false;  // whole-GPU block Gauss-Jordan per line (dense.cu)
     DenseWork dwork;
     DevBuf<double2> tbuf;   // dense sweep operand (nrhs x nb)
 };
@@ -1115,8 +1116,15 @@ void exact_factor(Ctx& c) {
     extract_lines<<<grid_blocks(int64_t(L) * nb, 256, 1 << 20), 256, 0, c.stream>>>(
         f->col_lines, c.nx, L, nb, c.east.p, c.south.p, f->coup.p);
     CK_LAUNCH();
-    f->dense = nb > 512 || std::getenv("FWI_EXACT_DENSE") != nullptr;
-    if (f->dense) {
+    // Sweeps: GEMM per line beyond the cluster kernel's reach (nb > 512). Factor: the
+    // whole-GPU block Gauss-Jordan whenever a line does not fit one CTA's shared memory
+    // (nb > 112; ~8x faster than the one-CTA global-memory Gauss-Jordan at nb = 128).
+    // FWI_EXACT_DENSE=1 forces both; FWI_EXACT_FACTOR=cta keeps the one-CTA factor.
+    const bool force_dense = std::getenv("FWI_EXACT_DENSE") != nullptr;
+    const char* ef = std::getenv("FWI_EXACT_FACTOR");
+    f->dense = nb > 512 || force_dense;
+    f->dense_factor = f->dense || (nb > 112 && !(ef && std::string(ef) == "cta"));
+    if (f->dense_factor) {
         const int64_t nn = int64_t(nb) * nb;
         for (int i = 0; i < L; ++i) {
             double2* Gi = f->G.p + i * int64_t(nb) * f->gp;

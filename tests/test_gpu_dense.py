@@ -99,3 +99,16 @@ def test_host_basis_gmres_history_matches_reference_c1():
     mask = rr >= 1e-6
     assert (np.abs(rd - rr)[mask] / rr[mask]).max() <= 1e-8
     assert log_d.stagnated == log_r.stagnated
+
+
+def test_block_gauss_jordan_factor_with_cluster_sweep():
+    """nb in (112, 512]: block Gauss-Jordan factor (dense.cu) + warp-specialised sweep."""
+    p = small_problem(nx=150, nz=130, n_pml=8, K=3, R=6)
+    ref = po.Ref(p, full=False, exact=True)
+    dev = fw.GnState(p, exact=True)
+    rng = np.random.default_rng(8)
+    b = rng.standard_normal(p.n) + 1j * rng.standard_normal(p.n)
+    for adj in (False, True):
+        want = ref.solve(b, _abi.FWI_PRECOND_EXACT, adj)
+        got = dev.solve(b, fw.PrecondMode.exact, adj)
+        assert rel(got, want) <= 1e-10, (adj, rel(got, want))

@@ -13,6 +13,8 @@ from paper_2204_06489_b200 import problem as pr  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "c1"
 its = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 p = {"c1": pr.c1_problem, "c3": pr.c3_problem, "c5": pr.c5_problem}[name]()
+if len(sys.argv) > 3:
+    p.freq_hz = float(sys.argv[3])
 p.d_obs = fw.simulate(p)
 p.epsilon = 1e-300  # H v - eps v with eps ~ 0
 st = fw.GnState(p, exact=True)
