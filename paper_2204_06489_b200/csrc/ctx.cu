@@ -97,6 +97,7 @@ int sm_count() {
 }
 
 Ctx::~Ctx() {
+    if (gmres_work) gmres_work_free(gmres_work);
     if (exact) exact_free(exact);
     if (ilu) ilu_free(ilu);
     for (auto*& p : kplan)

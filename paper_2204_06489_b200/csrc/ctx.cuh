@@ -23,6 +23,7 @@ namespace fwi_b200 {
 
 struct ExactFactor;  // exact.cu
 struct IluFactor;    // ilu.cu
+struct GmresWork;    // gmres.cu
 struct KktPlan;      // kkt_tma.cu
 
 struct Ctx {
@@ -55,6 +56,7 @@ struct Ctx {
     // factorisations
     ExactFactor* exact = nullptr;  // owned (exact_free)
     IluFactor* ilu = nullptr;      // owned (ilu_free)
+    GmresWork* gmres_work = nullptr;  // owned (gmres_work_free): Krylov buffers reused across solves
     int64_t solve_count[2] = {0, 0};
     KktPlan* kplan[2] = {nullptr, nullptr};  // TMA apply plans (c128, c64), built lazily
     int kkt_variant = 0;                      // 0: TMA persistent kernel, 1: plain kernel (FWI_KKT_KERNEL=plain)
@@ -133,6 +135,7 @@ void ilu_free(IluFactor*);
 void exact_factor(Ctx& c);
 void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int nrhs);
 void exact_free(ExactFactor*);
+void gmres_work_free(GmresWork*);
 int64_t exact_bytes(const ExactFactor*);
 
 // ---- precond.cu

@@ -59,6 +59,42 @@ struct Scratch {
     }
 };
 
+}  // namespace
+
+// Krylov buffers kept by a context between solves: cudaMalloc/cudaFree serialise the
+// device, and a solve allocates ~restart+6 vectors (≈10 ms of allocation at config 1,
+// where a whole GMRES iteration takes ~0.7 ms). Host-basis solves (config 5) do not keep
+// their 17 GB vectors.
+struct GmresWork {
+    int64_t len = 0;
+    std::vector<DevBuf<double>> vecs;
+    DevBuf<double> hdev, ydev;
+    Scratch sc;
+    DevBuf<double> take(int64_t n) {
+        if (n != len) {
+            vecs.clear();
+            len = n;
+        }
+        if (!vecs.empty()) {
+            DevBuf<double> b = std::move(vecs.back());
+            vecs.pop_back();
+            return b;
+        }
+        return DevBuf<double>(size_t(n));
+    }
+    void give(DevBuf<double>&& b) {
+        if (b.p && int64_t(b.count) == len) vecs.push_back(std::move(b));
+    }
+    void small(int restart) {
+        if (hdev.count < size_t(restart) + 2) hdev.alloc(size_t(restart) + 2);
+        if (ydev.count < size_t(restart) + 1) ydev.alloc(size_t(restart) + 1);
+    }
+};
+
+void gmres_work_free(GmresWork* w) { delete w; }
+
+namespace {
+
 double seconds_since(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -155,7 +191,7 @@ void multi_axpy_any(Basis& B, double* out, const double* x, const std::vector<do
 }
 
 // x (device, len) receives the solution.
-Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double tol, int maxit) {
+Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double tol, int maxit, GmresWork& WS) {
     if (restart < 1) throw FwiError(FWI_ERR_INVALID_ARGUMENT, "gmres: restart must be >= 1");
     const auto t0 = std::chrono::steady_clock::now();
     double observer_time = 0.0;
@@ -163,7 +199,7 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
     const int64_t len = ops.len;
     const size_t bytes = size_t(len) * sizeof(double);
     cudaStream_t st = ops.st;
-    Scratch sc;
+    Scratch& sc = WS.sc;
 
     CK(cudaMemsetAsync(x, 0, bytes, st));
     Log log;
@@ -186,10 +222,32 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
     B.dev.resize(nbasis);
     B.host.assign(nbasis, nullptr);
     double* best_host = nullptr;
-    DevBuf<double> tmp(len), w(len), xc(len), best;
+    DevBuf<double> tmp, w, xc, best;
+    // buffers come from (and go back to) the context's workspace unless the basis spills to the host
+    struct Giveback {
+        GmresWork& ws;
+        bool keep;
+        std::vector<DevBuf<double>*> bufs;
+        ~Giveback() {
+            if (keep)
+                for (auto* b : bufs) ws.give(std::move(*b));
+        }
+    } gb{WS, !host_mode, {}};
+    auto grab = [&](DevBuf<double>& d) {
+        d = host_mode ? DevBuf<double>(size_t(len)) : WS.take(len);
+        // KKT vectors carry a zero pad after the ds block that the flat dot products read
+        CK(cudaMemsetAsync(d.p, 0, bytes, st));
+        gb.bufs.push_back(&d);
+    };
+    grab(tmp);
+    grab(w);
+    grab(xc);
     if (!host_mode) {
-        best.alloc(len);
+        grab(best);
         B.ndev = nbasis;
+        // all slots up front: put_basis() then only rotates buffers (no allocation inside
+        // the iteration, which would serialise the device)
+        for (int i = 0; i < nbasis; ++i) grab(B.dev[i]);
     } else {
         B.chunk = std::min<int64_t>(len, int64_t(32) << 20);
         B.chunk -= B.chunk % 2;
@@ -201,6 +259,7 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
         CK(cudaMemGetInfo(&free_b, &total_b));
         const int fit = free_b > margin ? int((free_b - margin) / bytes) : 0;
         B.ndev = force_host ? std::min(1, std::min(fit, nbasis)) : std::min(fit, nbasis);
+        for (int i = 0; i < B.ndev; ++i) B.dev[i].alloc(len);
         CK(cudaMallocHost(&best_host, bytes));
         std::memset(best_host, 0, bytes);
     }
@@ -226,7 +285,6 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
     auto put_basis = [&](int i, DevBuf<double>& src) {
         if (!B.on_host(i)) {
             std::swap(B.dev[i], src);
-            if (!src.p) src.alloc(len);
         } else {
             B.ensure_host(i);
             CK(cudaMemcpyAsync(B.host[i], src.p, bytes, cudaMemcpyDeviceToHost, st));
@@ -246,7 +304,9 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
     double best_res = 1.0, true_res = 1.0;
     int iter = 0;
     bool stop_requested = false;
-    DevBuf<double> hdev(size_t(restart) + 2), ydev(size_t(restart) + 1);
+    WS.small(restart);
+    DevBuf<double>& hdev = WS.hdev;
+    DevBuf<double>& ydev = WS.ydev;
     std::vector<double> hh(restart + 2);
 
     while (iter < maxit && !log.converged && !stop_requested) {
@@ -391,11 +451,28 @@ void fsgn_gmres_step(Ctx& c, const fwi_fsgn_options& o, double* ds_host, fwi_con
     const int64_t n = c.n;
     cudaStream_t st = c.stream;
     // b = kkt_rhs
+    if (!c.gmres_work) c.gmres_work = new GmresWork();
+    GmresWork& ws = *c.gmres_work;
+    const bool small = size_t(len) * sizeof(double) * size_t(o.restart + 8) < (size_t(8) << 30);
     Vec bv;
     bv.ctx = &c;
-    bv.d.alloc(len);
+    bv.d = small ? ws.take(len) : DevBuf<double>(size_t(len));
+    CK(cudaMemsetAsync(bv.d.p, 0, bv.d.bytes(), st));
     kkt_rhs(c, bv);
-    DevBuf<double> xv(len);
+    DevBuf<double> xv = small ? ws.take(len) : DevBuf<double>(size_t(len));
+    CK(cudaMemsetAsync(xv.p, 0, xv.bytes(), st));
+    struct Back {
+        GmresWork& ws;
+        bool on;
+        DevBuf<double>& a;
+        DevBuf<double>& b;
+        ~Back() {
+            if (on) {
+                ws.give(std::move(a));
+                ws.give(std::move(b));
+            }
+        }
+    } back{ws, small, bv.d, xv};
     // g = gradient(state): K adjoint solves (src/kkt.cpp:139-141). It only
     // normalises the E_cg metric; without the exact factorisation the metric
     // column is left unset.
@@ -403,10 +480,10 @@ void fsgn_gmres_step(Ctx& c, const fwi_fsgn_options& o, double* ds_host, fwi_con
     CK(cudaMemsetAsync(g.p, 0, g.bytes(), st));
     CK(cudaMemsetAsync(hds.p, 0, hds.bytes(), st));
     double gnorm = 0.0;
+    if (!c.gmres_work) c.gmres_work = new GmresWork();
     if (c.exact) {
         reduced_gradient(c, g.p);
-        Scratch sc;
-        gnorm = dnorm(sc, st, g.p, c.ds_stride);
+        gnorm = dnorm(c.gmres_work->sc, st, g.p, c.ds_stride);
     }
     std::vector<std::pair<int, double>> metric;
     GmresOps ops;
@@ -433,7 +510,8 @@ void fsgn_gmres_step(Ctx& c, const fwi_fsgn_options& o, double* ds_host, fwi_con
             return o.ecg_stop_tol > 0.0 && e <= o.ecg_stop_tol;
         };
     }
-    Log lg = gmres_core(ops, bv.d.p, xv.p, o.restart, o.tol, o.maxit);
+    if (!c.gmres_work) c.gmres_work = new GmresWork();
+    Log lg = gmres_core(ops, bv.d.p, xv.p, o.restart, o.tol, o.maxit, *c.gmres_work);
     if (!lg.entries.empty() && c.exact) lg.entries.front().normal_residual = gnorm > 0.0 ? 1.0 : 0.0;
     for (const auto& [it, e] : metric)
         for (auto& en : lg.entries)
@@ -523,7 +601,8 @@ void gmres_generic(int64_t n, fwi_op_cb apply, fwi_op_cb precond, fwi_observer_c
             CK(cudaStreamSynchronize(nullptr));
             return observer(user, it, xc) != 0;
         };
-    Log lg = gmres_core(ops, b, x, restart, tol, maxit);
+    GmresWork ws;
+    Log lg = gmres_core(ops, b, x, restart, tol, maxit, ws);
     fill_log(lg, log);
 }
 
