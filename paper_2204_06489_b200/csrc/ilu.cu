@@ -241,15 +241,22 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int KIND>
+// XS = false: the vector stays in global memory (L2-resident; loaded with
+// ld.global.cg so a CTA always sees its own earlier levels' stores) and only the
+// level metadata is staged — for vectors beyond shared memory (config 3/4:
+// n = 49,152 -> 786 KB per right-hand side).
+__device__ __forceinline__ double2 xload(const double2* p, bool glob) { return glob ? __ldcg(p) : *p; }
+
+template <int KIND, bool XS>
 __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int* __restrict__ lvl_ptr,
                                                      const int* __restrict__ lvl_rows,
                                                      const int* __restrict__ rstart,
                                                      const int* __restrict__ idx,
                                                      const double2* __restrict__ val, double2* x, int ecap,
                                                      int rcap) {
-    extern __shared__ __align__(16) double2 xs[];
-    double2* vb = xs + n;                                     // [kLvlBuf][ecap]
+    extern __shared__ __align__(16) double2 dyn[];
+    double2* xs = XS ? dyn : x + int64_t(blockIdx.x) * n;
+    double2* vb = dyn + (XS ? n : 0);                         // [kLvlBuf][ecap]
     int* ib = reinterpret_cast<int*>(vb + size_t(kLvlBuf) * ecap);  // [kLvlBuf][ecap]
     int* rib = ib + kLvlBuf * ecap;                           // [kLvlBuf][rcap] row ids
     int* rpb = rib + kLvlBuf * rcap;                          // [kLvlBuf][rcap + 1] entry starts
@@ -269,7 +276,8 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
         }
         cp_commit();  // (possibly empty) group per level keeps the counting uniform
     };
-    for (int i = tid; i < n; i += nt) xs[i] = xk[i];
+    if (XS)
+        for (int i = tid; i < n; i += nt) xs[i] = xk[i];
 #pragma unroll
     for (int l = 0; l < kLvlBuf - 1; ++l) prefetch(l);
     for (int l = 0; l < nlev; ++l) {
@@ -284,15 +292,15 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
         for (int t = tid; t < nrow; t += nt) {
             const int i = rib[b * rcap + t];
             const int p0 = rp[t] - e0, p1 = rp[t + 1] - e0;
-            double2 s = xs[i];
+            double2 s = xload(xs + i, !XS);
             if (KIND == kLfwd || KIND == kLtbwd) {
                 for (int p = p0; p < p1; ++p) {
-                    const double2 xv = xs[il[p]];
+                    const double2 xv = xload(xs + il[p], !XS);
                     s = csub(s, KIND == kLfwd ? cmul(vl[p], xv) : cmulc(vl[p], xv));
                 }
                 xs[i] = s;
             } else if (KIND == kUbwd) {
-                for (int p = p0 + 1; p < p1; ++p) s = csub(s, cmul(vl[p], xs[il[p]]));
+                for (int p = p0 + 1; p < p1; ++p) s = csub(s, cmul(vl[p], xload(xs + il[p], !XS)));
                 xs[i] = cdiv(s, vl[p0]);
             } else {
                 double2 dg = make_double2(0.0, 0.0);
@@ -301,7 +309,7 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
                     if (k == i)
                         dg = vl[p];
                     else
-                        s = csub(s, cmulc(vl[p], xs[k]));
+                        s = csub(s, cmulc(vl[p], xload(xs + k, !XS)));
                 }
                 xs[i] = cdiv(s, make_double2(dg.x, -dg.y));
             }
@@ -310,21 +318,36 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
         prefetch(l + kLvlBuf - 1);
     }
     cp_wait<0>();
-    for (int t = tid; t < n; t += nt) xk[t] = xs[t];
+    if (XS)
+        for (int t = tid; t < n; t += nt) xk[t] = xs[t];
 }
 
 template <int KIND>
 void run_sweep(const Sweep& s, int64_t n, int nrhs, double2* x, cudaStream_t st) {
-    const size_t smem = size_t(n) * sizeof(double2) + size_t(kLvlBuf) * s.ecap * (sizeof(double2) + 4) +
-                        size_t(kLvlBuf) * (2 * s.rcap + 1) * 4 + 64;
-    if (smem <= 220 * 1024 && !std::getenv("FWI_ILU_GLOBAL")) {
+    const size_t meta = size_t(kLvlBuf) * s.ecap * (sizeof(double2) + 4) + size_t(kLvlBuf) * (2 * s.rcap + 1) * 4 + 64;
+    const size_t smem = size_t(n) * sizeof(double2) + meta;
+    const char* mode = std::getenv("FWI_ILU_GLOBAL");  // diagnostics: "1" = unstaged global kernel
+    if (smem <= 220 * 1024 && !mode) {
         static size_t set = 0;
         if (smem > set) {
-            CK(cudaFuncSetAttribute(ilu_sweep_smem<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            CK(cudaFuncSetAttribute(ilu_sweep_smem<KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(smem)));
             set = smem;
         }
-        ilu_sweep_smem<KIND><<<nrhs, 256, smem, st>>>(int(n), s.nlev, s.lvl_ptr.p, s.lvl_rows.p, s.rstart.p,
-                                                     s.lidx.p, s.lval.p, x, s.ecap, s.rcap);
+        ilu_sweep_smem<KIND, true><<<nrhs, 256, smem, st>>>(int(n), s.nlev, s.lvl_ptr.p, s.lvl_rows.p, s.rstart.p,
+                                                           s.lidx.p, s.lval.p, x, s.ecap, s.rcap);
+        CK_LAUNCH();
+        return;
+    }
+    if (meta <= 220 * 1024 && !mode) {  // vector in L2, level metadata staged in shared memory
+        static size_t set = 0;
+        if (meta > set) {
+            CK(cudaFuncSetAttribute(ilu_sweep_smem<KIND, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(meta)));
+            set = meta;
+        }
+        ilu_sweep_smem<KIND, false><<<nrhs, 256, meta, st>>>(int(n), s.nlev, s.lvl_ptr.p, s.lvl_rows.p,
+                                                            s.rstart.p, s.lidx.p, s.lval.p, x, s.ecap, s.rcap);
         CK_LAUNCH();
         return;
     }

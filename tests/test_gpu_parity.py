@@ -397,3 +397,19 @@ def test_hessian_apply_matches_reference(c1):
     p, ref, dev = c1
     v = np.random.default_rng(17).standard_normal(p.n)
     assert rel(fw.hessian_apply(dev, v), ref.hessian_apply(v)) <= 1e-10
+
+
+@pytest.mark.parametrize("level", [0, 4])
+def test_ilu_solves_bit_exact_beyond_shared_memory(level):
+    """n * 16 B above shared memory (the config-4 regime): the sweep keeps the vector in L2 and
+    stages only the level metadata; still bit-identical to the reference IluFactors::solve."""
+    p = small_problem(nx=170, nz=120, n_pml=8, K=3, R=6)
+    assert p.n * 16 > 220 * 1024
+    ref, dev = pair_direct(p, ilu_level=level)
+    rng = np.random.default_rng(level + 11)
+    b = rng.standard_normal((3, p.n)) + 1j * rng.standard_normal((3, p.n))
+    for adj in (False, True):
+        for r in range(3):
+            want = ref.solve(b[r], _abi.FWI_PRECOND_ILU, adj)
+            got = dev.solve(b[r], fw.PrecondMode.ilu, adj)
+            assert np.array_equal(got, want), (adj, rel(got, want))
