@@ -31,6 +31,7 @@ struct Sweep {          // one triangular sweep in CSR form + its level schedule
     // entries [rstart[r], rstart[r+1]) of (lidx, lval), in the row's own order
     DevBuf<int> rstart, lidx;
     DevBuf<double2> lval;
+    DevBuf<int4> lmeta;  // per level: first row, end row, first entry, end entry
     int nlev = 0;
     int ecap = 0, rcap = 0;  // max entries / rows of one level
 };
@@ -139,6 +140,9 @@ void upload_sweep(Sweep& s, int n, const std::vector<int>& ptr, const std::vecto
             s.ecap = std::max(s.ecap, rst[lp[l + 1]] - rst[lp[l]]);
         }
         s.ecap = (s.ecap + 1) / 2 * 2;
+        std::vector<int4> meta(s.nlev);
+        for (int l = 0; l < s.nlev; ++l) meta[l] = make_int4(lp[l], lp[l + 1], rst[lp[l]], rst[lp[l + 1]]);
+        up(s.lmeta, meta);
         up(s.lidx, li);
         s.lval.alloc(std::max<size_t>(lv.size(), 1));
         if (!lv.empty())
@@ -248,8 +252,8 @@ __device__ __forceinline__ void cp_wait() {
 __device__ __forceinline__ double2 xload(const double2* p, bool glob) { return glob ? __ldcg(p) : *p; }
 
 template <int KIND, bool XS>
-__global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int* __restrict__ lvl_ptr,
-                                                     const int* __restrict__ lvl_rows,
+__global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int4* __restrict__ lmeta,
+                                                     int meta_smem, const int* __restrict__ lvl_rows,
                                                      const int* __restrict__ rstart,
                                                      const int* __restrict__ idx,
                                                      const double2* __restrict__ val, double2* x, int ecap,
@@ -260,13 +264,21 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
     int* ib = reinterpret_cast<int*>(vb + size_t(kLvlBuf) * ecap);  // [kLvlBuf][ecap]
     int* rib = ib + kLvlBuf * ecap;                           // [kLvlBuf][rcap] row ids
     int* rpb = rib + kLvlBuf * rcap;                          // [kLvlBuf][rcap + 1] entry starts
+    int4* ms = reinterpret_cast<int4*>(rpb + kLvlBuf * (rcap + 1) + 3 - ((kLvlBuf * (rcap + 1) + 3) & 3));
     double2* xk = x + int64_t(blockIdx.x) * n;
     const int tid = threadIdx.x, nt = blockDim.x;
+    // level bounds in shared memory: the prefetch of level l+3 then issues its copies
+    // without a dependent chain of global loads on every level's critical path
+    if (meta_smem)
+        for (int l = tid; l < nlev; l += nt) ms[l] = lmeta[l];
+    const int4* mt = meta_smem ? ms : lmeta;
+    __syncthreads();
     auto prefetch = [&](int l) {
         if (l < nlev) {
             const int b = l % kLvlBuf;
-            const int r0 = lvl_ptr[l], r1 = lvl_ptr[l + 1];
-            const int e0 = rstart[r0], e1 = rstart[r1];
+            const int4 m = mt[l];
+            const int r0 = m.x, r1 = m.y;
+            const int e0 = m.z, e1 = m.w;
             for (int t = tid; t < e1 - e0; t += nt) {
                 cp_async16(vb + b * ecap + t, val + e0 + t);
                 cp_async4(ib + b * ecap + t, idx + e0 + t);
@@ -284,7 +296,7 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
         cp_wait<kLvlBuf - 2>();
         __syncthreads();
         const int b = l % kLvlBuf;
-        const int nrow = lvl_ptr[l + 1] - lvl_ptr[l];
+        const int nrow = mt[l].y - mt[l].x;
         const int* rp = rpb + b * (rcap + 1);
         const int e0 = rp[0];
         const double2* vl = vb + b * ecap;
@@ -293,26 +305,42 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
             const int i = rib[b * rcap + t];
             const int p0 = rp[t] - e0, p1 = rp[t + 1] - e0;
             double2 s = xload(xs + i, !XS);
-            if (KIND == kLfwd || KIND == kLtbwd) {
-                for (int p = p0; p < p1; ++p) {
-                    const double2 xv = xload(xs + il[p], !XS);
-                    s = csub(s, KIND == kLfwd ? cmul(vl[p], xv) : cmulc(vl[p], xv));
+            // entries in the reference's order; the x operands of a batch of 8 are loaded
+            // before the dependent subtraction chain (one L2 round trip per batch, not per entry)
+            constexpr int BT = 8;
+            const int q0 = (KIND == kUbwd) ? p0 + 1 : p0;
+            double2 dg = make_double2(0.0, 0.0);
+            for (int pb = q0; pb < p1; pb += BT) {
+                double2 xv[BT];
+#pragma unroll
+                for (int u = 0; u < BT; ++u) {
+                    const int p = pb + u;
+                    if (p < p1) {
+                        const int k = il[p];
+                        xv[u] = (KIND == kUtfwd && k == i) ? make_double2(0.0, 0.0) : xload(xs + k, !XS);
+                    }
                 }
-                xs[i] = s;
-            } else if (KIND == kUbwd) {
-                for (int p = p0 + 1; p < p1; ++p) s = csub(s, cmul(vl[p], xload(xs + il[p], !XS)));
-                xs[i] = cdiv(s, vl[p0]);
-            } else {
-                double2 dg = make_double2(0.0, 0.0);
-                for (int p = p0; p < p1; ++p) {
-                    const int k = il[p];
-                    if (k == i)
-                        dg = vl[p];
-                    else
-                        s = csub(s, cmulc(vl[p], xload(xs + k, !XS)));
+#pragma unroll
+                for (int u = 0; u < BT; ++u) {
+                    const int p = pb + u;
+                    if (p < p1) {
+                        if (KIND == kUtfwd) {
+                            if (il[p] == i)
+                                dg = vl[p];
+                            else
+                                s = csub(s, cmulc(vl[p], xv[u]));
+                        } else {
+                            s = csub(s, (KIND == kLfwd || KIND == kUbwd) ? cmul(vl[p], xv[u]) : cmulc(vl[p], xv[u]));
+                        }
+                    }
                 }
-                xs[i] = cdiv(s, make_double2(dg.x, -dg.y));
             }
+            if (KIND == kLfwd || KIND == kLtbwd)
+                xs[i] = s;
+            else if (KIND == kUbwd)
+                xs[i] = cdiv(s, vl[p0]);
+            else
+                xs[i] = cdiv(s, make_double2(dg.x, -dg.y));
         }
         __syncthreads();
         prefetch(l + kLvlBuf - 1);
@@ -324,7 +352,10 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
 
 template <int KIND>
 void run_sweep(const Sweep& s, int64_t n, int nrhs, double2* x, cudaStream_t st) {
-    const size_t meta = size_t(kLvlBuf) * s.ecap * (sizeof(double2) + 4) + size_t(kLvlBuf) * (2 * s.rcap + 1) * 4 + 64;
+    size_t meta = size_t(kLvlBuf) * s.ecap * (sizeof(double2) + 4) + size_t(kLvlBuf) * (2 * s.rcap + 1) * 4 + 64;
+    const size_t lm = size_t(s.nlev) * sizeof(int4);
+    const int meta_smem = (lm <= 48 * 1024) ? 1 : 0;
+    if (meta_smem) meta += lm + 16;
     const size_t smem = size_t(n) * sizeof(double2) + meta;
     const char* mode = std::getenv("FWI_ILU_GLOBAL");  // diagnostics: "1" = unstaged global kernel
     if (smem <= 220 * 1024 && !mode) {
@@ -334,8 +365,8 @@ void run_sweep(const Sweep& s, int64_t n, int nrhs, double2* x, cudaStream_t st)
                                     int(smem)));
             set = smem;
         }
-        ilu_sweep_smem<KIND, true><<<nrhs, 256, smem, st>>>(int(n), s.nlev, s.lvl_ptr.p, s.lvl_rows.p, s.rstart.p,
-                                                           s.lidx.p, s.lval.p, x, s.ecap, s.rcap);
+        ilu_sweep_smem<KIND, true><<<nrhs, 256, smem, st>>>(int(n), s.nlev, s.lmeta.p, meta_smem, s.lvl_rows.p,
+                                                           s.rstart.p, s.lidx.p, s.lval.p, x, s.ecap, s.rcap);
         CK_LAUNCH();
         return;
     }
@@ -346,8 +377,9 @@ void run_sweep(const Sweep& s, int64_t n, int nrhs, double2* x, cudaStream_t st)
                                     int(meta)));
             set = meta;
         }
-        ilu_sweep_smem<KIND, false><<<nrhs, 256, meta, st>>>(int(n), s.nlev, s.lvl_ptr.p, s.lvl_rows.p,
-                                                            s.rstart.p, s.lidx.p, s.lval.p, x, s.ecap, s.rcap);
+        ilu_sweep_smem<KIND, false><<<nrhs, 256, meta, st>>>(int(n), s.nlev, s.lmeta.p, meta_smem,
+                                                            s.lvl_rows.p, s.rstart.p, s.lidx.p, s.lval.p, x,
+                                                            s.ecap, s.rcap);
         CK_LAUNCH();
         return;
     }
