@@ -282,7 +282,7 @@ def run_ours(args):
                          "frac": achieved / peak, "peak_source": peak_src,
                          "traffic": tr.get("dram_bytes_per_launch") if tr else None,
                          "algorithmic_bytes_per_launch": alg_bytes,
-                         "kernel": "kkt_apply_kernel<F64>"},
+                         "kernel": "kkt_tma_kernel<F64, 8, 2> (persistent TMA K1, csrc/kkt_tma.cu)"},
             "c64": {"applies_per_s": ws / per32, "ms_per_apply": per32 * 1e3,
                     "achieved_gbs": alg_bytes32 / per32 / 1e9,
                     "frac": alg_bytes32 / per32 / 1e9 / peak},
