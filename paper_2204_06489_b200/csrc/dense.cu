@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "dense.cuh"
@@ -140,18 +141,23 @@ __global__ void __launch_bounds__(kGemmThreads) cgemm_kernel(int M, int N, int K
 }
 
 // Inverse of one b x b diagonal block (b <= 64) by Gauss-Jordan with partial
-// pivoting inside the block, in shared memory; one CTA.
+// pivoting inside the block, in shared memory; one CTA of 256 threads. Per pivot
+// step: warp 0 finds the pivot and its reciprocal; 64 threads form the
+// multiplier column and 64 the scaled pivot row (reading the pre-swap rows, so
+// the swap needs no extra pass); then every thread updates 16 entries of one
+// column. Three barriers per step; the column permutation is applied on output.
 __global__ void __launch_bounds__(256) block_inverse_kernel(int b, const double2* __restrict__ D, int64_t ldd,
                                                             double2* __restrict__ out, int64_t ldo, int* status,
                                                             int status_base) {
     extern __shared__ double2 bsm[];
     double2(*A)[65] = reinterpret_cast<double2(*)[65]>(bsm);  // [64][65]
     __shared__ double2 prow[64], pcol[64];
-    __shared__ int piv[64];
+    __shared__ int piv[64], perm[64];
     __shared__ int s_p;
     __shared__ double2 s_inv;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    for (int e = tid; e < b * b; e += blockDim.x) A[e / b][e % b] = D[int64_t(e / b) * ldd + e % b];
+    const int cj = tid & 63, rg = tid >> 6;  // column, row group (rows rg, rg+4, ...)
+    for (int r = rg; r < 64; r += 4) A[r][cj] = (r < b && cj < b) ? D[int64_t(r) * ldd + cj] : make_double2(0.0, 0.0);
     __syncthreads();
     for (int k = 0; k < b; ++k) {
         if (wid == 0) {  // pivot: max |A[r][k]|, r >= k (ties: lowest row)
@@ -171,58 +177,56 @@ __global__ void __launch_bounds__(256) block_inverse_kernel(int b, const double2
                     if (*status == 0) *status = status_base + k + 1;
                     bi = k;
                 }
+                const double2 d = A[bi][k];
+                const double m2 = d.x * d.x + d.y * d.y;
+                const double r = m2 > 0.0 ? 1.0 / m2 : 0.0;
+                s_inv = make_double2(d.x * r, -d.y * r);
                 s_p = bi;
                 piv[k] = bi;
             }
         }
         __syncthreads();
         const int p = s_p;
-        if (p != k)
-            for (int j = tid; j < b; j += blockDim.x) {
-                const double2 t = A[k][j];
-                A[k][j] = A[p][j];
-                A[p][j] = t;
-            }
-        __syncthreads();
-        if (tid == 0) {
-            const double2 d = A[k][k];
-            s_inv = (d.x == 0.0 && d.y == 0.0) ? make_double2(0.0, 0.0) : cdiv(make_double2(1.0, 0.0), d);
-        }
-        __syncthreads();
         const double2 pinv = s_inv;
-        for (int j = tid; j < b; j += blockDim.x) {
-            const double2 a = (j == k) ? make_double2(1.0, 0.0) : A[k][j];
-            const double2 v = make_double2(a.x * pinv.x - a.y * pinv.y, a.x * pinv.y + a.y * pinv.x);
-            prow[j] = v;
-            pcol[j] = (j == k) ? make_double2(0.0, 0.0) : A[j][k];
+        if (tid < 64) {  // multiplier column of the swapped matrix (rows p and k exchanged)
+            const int r = tid;
+            pcol[r] = (r == k || r >= b) ? make_double2(0.0, 0.0) : (r == p ? A[k][k] : A[r][k]);
+        } else if (tid < 128) {  // scaled pivot row (old row p) and the swap of old row k into row p
+            const int j = tid - 64;
+            if (j < b) {
+                const double2 a = (j == k) ? make_double2(1.0, 0.0) : A[p][j];
+                prow[j] = make_double2(a.x * pinv.x - a.y * pinv.y, a.x * pinv.y + a.y * pinv.x);
+                if (p != k) A[p][j] = A[k][j];
+            }
         }
         __syncthreads();
-        for (int e = tid; e < b * b; e += blockDim.x) {
-            const int r = e / b, j = e % b;
-            if (r == k) {
-                A[r][j] = prow[j];
-            } else {
-                const double2 f = pcol[r];
-                double2 v = (j == k) ? make_double2(0.0, 0.0) : A[r][j];
-                const double2 pr = prow[j];
-                v.x -= f.x * pr.x - f.y * pr.y;
-                v.y -= f.x * pr.y + f.y * pr.x;
-                A[r][j] = v;
+        if (cj < b) {
+            const double2 pr = prow[cj];
+            for (int r = rg; r < b; r += 4) {
+                if (r == k) {
+                    A[r][cj] = pr;
+                } else {
+                    const double2 f = pcol[r];
+                    double2 v = (cj == k) ? make_double2(0.0, 0.0) : A[r][cj];
+                    v.x -= f.x * pr.x - f.y * pr.y;
+                    v.y -= f.x * pr.y + f.y * pr.x;
+                    A[r][cj] = v;
+                }
             }
         }
         __syncthreads();
     }
-    for (int k = b - 1; k >= 0; --k) {  // undo the column permutation
-        const int p = piv[k];
-        if (p != k)
-            for (int r = tid; r < b; r += blockDim.x) {
-                const double2 t = A[r][k];
-                A[r][k] = A[r][p];
-                A[r][p] = t;
-            }
-        __syncthreads();
+    if (tid == 0) {  // undoing the column swaps in reverse order = one permutation
+        for (int j = 0; j < b; ++j) perm[j] = j;
+        for (int k = b - 1; k >= 0; --k) {
+            const int t = perm[k];
+            perm[k] = perm[piv[k]];
+            perm[piv[k]] = t;
+        }
     }
-    for (int e = tid; e < b * b; e += blockDim.x) out[int64_t(e / b) * ldo + e % b] = A[e / b][e % b];
+    __syncthreads();
+    if (cj < b)
+        for (int r = rg; r < b; r += 4) out[int64_t(r) * ldo + cj] = A[r][perm[cj]];
 }
 
 // F = A[:, K] with rows K zeroed (nb x bs, ld kBlk), then A[:, K] = 0
@@ -265,9 +269,127 @@ __global__ void sweep_prologue(int nb, int nrhs, const double2* __restrict__ b, 
     T[t] = r;
 }
 
+// ---------------------------------------------------------------------------
+// FP64 tensor-core variant: mma.sync m8n8k4 (DMMA). Complex products as four real
+// MMAs into three accumulators: P = Ar Br, Q = Ai Bi, I = Ar Bi + Ai Br (C = P - Q + iI).
+// 32x64 output tile per CTA, 8 warps in a 2x4 grid of 16x16 warp tiles (2x2 MMA tiles),
+// 16-deep complex K slabs staged in shared memory as separate re/im planes (k-major)
+// with a register prefetch of the next slab.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+constexpr int kTBM = 32, kTBN = 64, kTBK = 16, kTPadM = kTBM + 4, kTPadN = kTBN + 4;
+
+template <bool BT>
+__global__ void __launch_bounds__(256) zgemm_dmma_kernel(int M, int N, int K, double alpha,
+                                                         const double2* __restrict__ A, int64_t lda,
+                                                         const double2* __restrict__ B, int64_t ldb,
+                                                         const double2* C0, int64_t ldc0, double2* C, int64_t ldc) {
+    __shared__ double Ar[kTBK][kTPadM], Ai[kTBK][kTPadM], Br[kTBK][kTPadN], Bi[kTBK][kTPadN];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 1, wn = warp >> 1;  // 2 x 4 warp grid of 16 x 16 tiles
+    const int m0 = blockIdx.y * kTBM, n0 = blockIdx.x * kTBN;
+    constexpr int A_PER = kTBM * kTBK / 256, B_PER = kTBN * kTBK / 256;  // 2, 4
+    double2 ra[A_PER], rb[B_PER];
+    auto load = [&](int k0) {
+#pragma unroll
+        for (int q = 0; q < A_PER; ++q) {
+            const int e = tid + q * 256, kk = e % kTBK, mm = e / kTBK;
+            const int m = m0 + mm, k = k0 + kk;
+            ra[q] = (m < M && k < K) ? A[int64_t(m) * lda + k] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int q = 0; q < B_PER; ++q) {
+            const int e = tid + q * 256;
+            int kk, nn;
+            if (BT) { kk = e % kTBK; nn = e / kTBK; }
+            else { nn = e % kTBN; kk = e / kTBN; }
+            const int n = n0 + nn, k = k0 + kk;
+            rb[q] = (n < N && k < K) ? (BT ? B[int64_t(n) * ldb + k] : B[int64_t(k) * ldb + n])
+                                     : make_double2(0.0, 0.0);
+        }
+    };
+    auto store = [&]() {
+#pragma unroll
+        for (int q = 0; q < A_PER; ++q) {
+            const int e = tid + q * 256, kk = e % kTBK, mm = e / kTBK;
+            Ar[kk][mm] = ra[q].x;
+            Ai[kk][mm] = ra[q].y;
+        }
+#pragma unroll
+        for (int q = 0; q < B_PER; ++q) {
+            const int e = tid + q * 256;
+            int kk, nn;
+            if (BT) { kk = e % kTBK; nn = e / kTBK; }
+            else { nn = e % kTBN; kk = e / kTBN; }
+            Br[kk][nn] = rb[q].x;
+            Bi[kk][nn] = rb[q].y;
+        }
+    };
+    double P[2][2][2] = {}, Q[2][2][2] = {}, I[2][2][2] = {};
+    const int g = lane >> 2, t4 = lane & 3;
+    load(0);
+    for (int k0 = 0; k0 < K; k0 += kTBK) {
+        __syncthreads();
+        store();
+        __syncthreads();
+        if (k0 + kTBK < K) load(k0 + kTBK);
+#pragma unroll
+        for (int ks = 0; ks < kTBK; ks += 4) {
+            double ar[2], ai[2], br[2], bi[2];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                ar[t] = Ar[ks + t4][wm * 16 + t * 8 + g];
+                ai[t] = Ai[ks + t4][wm * 16 + t * 8 + g];
+                br[t] = Br[ks + t4][wn * 16 + t * 8 + g];
+                bi[t] = Bi[ks + t4][wn * 16 + t * 8 + g];
+            }
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    dmma(P[t][u], ar[t], br[u]);
+                    dmma(Q[t][u], ai[t], bi[u]);
+                    dmma(I[t][u], ar[t], bi[u]);
+                    dmma(I[t][u], ai[t], br[u]);
+                }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int m = m0 + wm * 16 + t * 8 + g, n = n0 + wn * 16 + u * 8 + 2 * t4 + e;
+                if (m >= M || n >= N) continue;
+                double2 v = make_double2(alpha * (P[t][u][e] - Q[t][u][e]), alpha * I[t][u][e]);
+                if (C0) {
+                    const double2 c = C0[int64_t(m) * ldc0 + n];
+                    v.x += c.x;
+                    v.y += c.y;
+                }
+                C[int64_t(m) * ldc + n] = v;
+            }
+}
+
 template <bool BT>
 void cgemm_launch(cudaStream_t st, int M, int N, int K, double alpha, const double2* A, int64_t lda,
                   const double2* B, int64_t ldb, const double2* C0, int64_t ldc0, double2* C, int64_t ldc) {
+    static const bool simt = [] {
+        const char* e = std::getenv("FWI_CGEMM");
+        return e && std::string(e) == "simt";
+    }();
+    if (!simt) {
+        zgemm_dmma_kernel<BT><<<dim3((N + kTBN - 1) / kTBN, (M + kTBM - 1) / kTBM), 256, 0, st>>>(
+            M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
+        CK_LAUNCH();
+        return;
+    }
     const int gx = (N + kBN - 1) / kBN;
     const int big = gx * ((M + 63) / 64);
     if (big >= sm_count()) {
