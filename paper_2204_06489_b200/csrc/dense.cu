@@ -202,16 +202,24 @@ __global__ void __launch_bounds__(256) block_inverse_kernel(int b, const double2
         __syncthreads();
         if (cj < b) {
             const double2 pr = prow[cj];
-            for (int r = rg; r < b; r += 4) {
+            double2 v[16], f[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {  // all loads first, then the updates
+                const int r = rg + 4 * i;
+                v[i] = (cj == k) ? make_double2(0.0, 0.0) : A[r][cj];
+                f[i] = pcol[r];
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int r = rg + 4 * i;
+                if (r >= b) continue;
                 if (r == k) {
-                    A[r][cj] = pr;
+                    v[i] = pr;
                 } else {
-                    const double2 f = pcol[r];
-                    double2 v = (cj == k) ? make_double2(0.0, 0.0) : A[r][cj];
-                    v.x -= f.x * pr.x - f.y * pr.y;
-                    v.y -= f.x * pr.y + f.y * pr.x;
-                    A[r][cj] = v;
+                    v[i].x -= f[i].x * pr.x - f[i].y * pr.y;
+                    v[i].y -= f[i].x * pr.y + f[i].y * pr.x;
                 }
+                A[r][cj] = v[i];
             }
         }
         __syncthreads();

@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <string>
 #include <array>
+#include <mutex>
 #include <type_traits>
 #include <cstdio>
 #include <vector>
@@ -1200,19 +1201,28 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
     const char* sw = std::getenv("FWI_EXACT_SWEEP");  // "warp" (default) | "cta" | "legacy"
     const std::string sweep = sw ? sw : "warp";
     if (!done && sweep == "warp") {
-        // plans are cached per (nb, L, nrhs): the model queries cluster occupancy
+        // plans are cached per (nb, L, nrhs) (the model queries cluster occupancy);
+        // process-wide, so guarded for contexts driven from several host threads
+        static std::mutex mu;
         static std::vector<std::pair<std::array<int, 3>, WarpPlan>> cache;
+        const bool forced = std::getenv("FWI_EXACT_CS") || std::getenv("FWI_EXACT_KG");
         const std::array<int, 3> key{f.nb, f.L, nrhs};
-        WarpPlan* wp = nullptr;
-        for (auto& e : cache)
-            if (e.first == key && !std::getenv("FWI_EXACT_CS") && !std::getenv("FWI_EXACT_KG")) wp = &e.second;
-        WarpPlan fresh;
-        if (!wp && warp_plan(f.nb, f.L, f.gp, nrhs, fresh)) {
-            cache.emplace_back(key, fresh);
-            wp = &cache.back().second;
+        bool have = false;
+        WarpPlan plan;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            for (auto& e : cache)
+                if (e.first == key && !forced) {
+                    plan = e.second;
+                    have = true;
+                }
+            if (!have && warp_plan(f.nb, f.L, f.gp, nrhs, plan)) {
+                if (!forced) cache.emplace_back(key, plan);
+                have = true;
+            }
         }
-        if (wp) {
-            WarpPlan p = *wp;
+        if (have) {
+            WarpPlan p = plan;
             p.a.G = f.G.p;
             p.a.coup = f.coup.p;
             p.a.W = W;
