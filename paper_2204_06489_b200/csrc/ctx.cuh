@@ -118,6 +118,10 @@ void dev_mgs_step(cudaStream_t st, double* w, const double* vprev, const double*
 void dev_mgs_step_parts(cudaStream_t st, double* w, const double* vprev, const double* hprev_dev,
                         const double* vnext, double* partials_out, int64_t len);
 void dev_sum_ordered(cudaStream_t st, const double* partials, int count, double* out_dev);
+// all m+1 fused MGS steps of one GMRES iteration in one launch (v: m device vectors,
+// h_dev: m+1 outputs); false if it cannot run (caller falls back to dev_mgs_step)
+bool dev_mgs_all(cudaStream_t st, double* w, const double* const* v, int m, double* h_dev, double* partials,
+                 unsigned* ticket, unsigned* flag, unsigned& epoch, int64_t len);
 void dev_multi_axpy(cudaStream_t st, double* out, const double* x, const double* const* v,
                     const double* y, int m, int64_t len);
 void dev_sub_norm2(cudaStream_t st, const double* b, const double* ax, double* out_dev,

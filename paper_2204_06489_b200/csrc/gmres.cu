@@ -50,12 +50,15 @@ struct GmresOps {
 
 struct Scratch {
     DevBuf<double> partials, out;
-    DevBuf<unsigned> ticket;
+    DevBuf<unsigned> ticket, flag;
+    unsigned epoch = 0;  // grid-barrier generation of the fused MGS kernel
     Scratch() {
         partials.alloc(4096);
         out.alloc(256);
         ticket.alloc(64);
+        flag.alloc(1);
         CK(cudaMemset(ticket.p, 0, 64 * sizeof(unsigned)));
+        CK(cudaMemset(flag.p, 0, sizeof(unsigned)));
     }
 };
 
@@ -331,9 +334,18 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
             ops.apply(B.dptr(j), tmp.p);
             ops.precond(tmp.p, w.p);
             // MGS: h_i = <v_i, w>; w -= h_i v_i  (fused pairwise)
-            for (int i = 0; i <= j; ++i)
-                mgs_step_any(sc, B, w.p, i - 1, hdev.p + (i - 1), i, hdev.p + i);
-            mgs_step_any(sc, B, w.p, j, hdev.p + j, -1, hdev.p + j + 1);
+            bool fused = false;
+            if (!host_mode && !std::getenv("FWI_GMRES_MGS_STEPS")) {
+                std::vector<const double*> vp(j + 1);
+                for (int i = 0; i <= j; ++i) vp[i] = B.dptr(i);
+                fused = dev_mgs_all(st, w.p, vp.data(), j + 1, hdev.p, sc.partials.p, sc.ticket.p, sc.flag.p,
+                                    sc.epoch, len);
+            }
+            if (!fused) {
+                for (int i = 0; i <= j; ++i)
+                    mgs_step_any(sc, B, w.p, i - 1, hdev.p + (i - 1), i, hdev.p + i);
+                mgs_step_any(sc, B, w.p, j, hdev.p + j, -1, hdev.p + j + 1);
+            }
             CK(cudaMemcpyAsync(hh.data(), hdev.p, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             std::vector<double> h(hh.begin(), hh.begin() + j + 2);

@@ -162,6 +162,64 @@ __global__ void __launch_bounds__(kRedThreads) sum_ordered_kernel(const double* 
     if (threadIdx.x == 0) *out = v;
 }
 
+// The whole MGS sweep of one GMRES iteration in one launch (device-resident
+// basis): for i = 0..m, w -= h_{i-1} v_{i-1}; h_i = <v_i, w> (v_m := w, the norm).
+// Every step is the same grid-stride pass and the same ordered partial sum as
+// mgs_kernel, so the h values are bit-identical to m+1 separate launches; the
+// steps are separated by a software grid barrier (the grid is sized to be
+// co-resident): the last CTA of a step sums the partials and publishes h_i.
+struct MgsAllArgs {
+    const double2* v[64];
+};
+
+__global__ void __launch_bounds__(kRedThreads) mgs_all_kernel(double2* __restrict__ w, MgsAllArgs a, int m,
+                                                              int64_t len2, double* partials, unsigned* ticket,
+                                                              volatile unsigned* flag, unsigned epoch, double* h) {
+    __shared__ double sh[32];
+    __shared__ bool last;
+    for (int i = 0; i <= m; ++i) {
+        const double2* vprev = i > 0 ? a.v[i - 1] : nullptr;
+        const double2* vnext = i < m ? a.v[i] : nullptr;
+        const double nh = vprev ? -__ldcg(h + i - 1) : 0.0;  // published by another CTA: bypass L1
+        double acc = 0.0;
+        for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < len2;
+             t += int64_t(gridDim.x) * blockDim.x) {
+            double2 wv = w[t];
+            if (vprev) {
+                const double2 pv = vprev[t];
+                wv.x = __dadd_rn(wv.x, __dmul_rn(nh, pv.x));
+                wv.y = __dadd_rn(wv.y, __dmul_rn(nh, pv.y));
+                w[t] = wv;
+            }
+            const double2 nv = vnext ? vnext[t] : wv;
+            acc += nv.x * wv.x + nv.y * wv.y;
+        }
+        acc = block_sum(acc, sh);
+        if (threadIdx.x == 0) {
+            partials[blockIdx.x] = acc;
+            __threadfence();
+            last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+        }
+        __syncthreads();
+        if (last) {  // same ordered combine as finish_reduction
+            __threadfence();
+            double v = 0.0;
+            for (int q = threadIdx.x; q < gridDim.x; q += blockDim.x) v += __ldcg(partials + q);
+            v = block_sum(v, sh);
+            if (threadIdx.x == 0) {
+                h[i] = v;
+                *ticket = 0u;
+                __threadfence();
+                flag[0] = epoch + unsigned(i) + 1u;
+            }
+        }
+        if (threadIdx.x == 0)
+            while (flag[0] < epoch + unsigned(i) + 1u) __nanosleep(32);
+        __syncthreads();
+        __threadfence();
+    }
+}
+
 struct MultiAxpyArgs {
     const double2* v[64];
 };
@@ -249,6 +307,26 @@ void dev_mgs_step_parts(cudaStream_t st, double* w, const double* vprev, const d
         reinterpret_cast<double2*>(w), reinterpret_cast<const double2*>(vprev), hprev_dev,
         reinterpret_cast<const double2*>(vnext), len / 2, partials_out);
     CK_LAUNCH();
+}
+
+bool dev_mgs_all(cudaStream_t st, double* w, const double* const* v, int m, double* h_dev, double* partials,
+                 unsigned* ticket, unsigned* flag, unsigned& epoch, int64_t len) {
+    if (m + 1 > 64) return false;
+    // co-residency of the software grid barrier: reduce_blocks() CTAs of 256 threads
+    static int ok = -1;
+    if (ok < 0) {
+        int per_sm = 0;
+        ok = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgs_all_kernel, kRedThreads, 0) == cudaSuccess &&
+             per_sm * sm_count() >= reduce_blocks();
+    }
+    if (!ok) return false;
+    MgsAllArgs a{};
+    for (int i = 0; i < m; ++i) a.v[i] = reinterpret_cast<const double2*>(v[i]);
+    mgs_all_kernel<<<reduce_blocks(), kRedThreads, 0, st>>>(reinterpret_cast<double2*>(w), a, m, len / 2, partials,
+                                                            ticket, flag, epoch, h_dev);
+    CK_LAUNCH();
+    epoch += unsigned(m) + 1u;
+    return true;
 }
 
 void dev_sum_ordered(cudaStream_t st, const double* partials, int count, double* out_dev) {

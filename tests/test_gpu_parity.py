@@ -413,3 +413,19 @@ def test_ilu_solves_bit_exact_beyond_shared_memory(level):
             want = ref.solve(b[r], _abi.FWI_PRECOND_ILU, adj)
             got = dev.solve(b[r], fw.PrecondMode.ilu, adj)
             assert np.array_equal(got, want), (adj, rel(got, want))
+
+
+def test_fused_mgs_bitwise_equals_stepwise(c1):
+    """The one-launch MGS sweep (grid barrier between steps) reproduces the per-step
+    launches bit for bit: same grid-stride passes, same ordered partial sums."""
+    import os
+    p, ref, dev = c1
+    opts = fw.FsgnOptions(restart=30, tol=0.0, maxit=20, ecg_stride=0)
+    ds_f, log_f = fw.fsgn_gmres_step(dev, opts)
+    os.environ["FWI_GMRES_MGS_STEPS"] = "1"
+    try:
+        ds_s, log_s = fw.fsgn_gmres_step(dev, opts)
+    finally:
+        del os.environ["FWI_GMRES_MGS_STEPS"]
+    assert log_f.residuals() == log_s.residuals()
+    assert np.array_equal(ds_f, ds_s)
