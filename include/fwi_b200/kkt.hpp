@@ -236,4 +236,18 @@ inline StepResult fsgn_gmres_step(GnState& s, const FsgnOptions& o = {}) {
     return r;
 }
 
+// fwi::gradient / fwi::hessian_apply (include/fwi/reduced_space.hpp; src/reduced_space.cpp:
+// 120-152): the reduced-space building blocks of the E_cg metric and the RSGN path.
+inline std::vector<double> gradient(GnState& s) {
+    std::vector<double> g(size_t(s.model_size()));
+    check(fwi_dev_gradient(s.handle(), g.data()));
+    return g;
+}
+inline std::vector<double> hessian_apply(GnState& s, const std::vector<double>& v) {
+    if (v.size() != size_t(s.model_size())) throw std::invalid_argument("hessian_apply: size mismatch");
+    std::vector<double> out(v.size());
+    check(fwi_dev_hessian_apply(s.handle(), v.data(), out.data()));
+    return out;
+}
+
 }  // namespace fwi::gpu

@@ -188,6 +188,27 @@ int main() {
         }
         CHECK(std::sqrt(num / den) < 1e-6);
     }
+    // reduced-space gradient and Hessian action (src/reduced_space.cpp:120-152)
+    {
+        const std::vector<double> g = gpu::gradient(dev);
+        const RealVector gr = gradient(ref);
+        double num = 0, den = 0;
+        for (size_t i = 0; i < g.size(); ++i) {
+            num += (g[i] - gr[i]) * (g[i] - gr[i]);
+            den += gr[i] * gr[i];
+        }
+        CHECK(std::sqrt(num / den) < 1e-10);
+        RealVector v(gr.size());
+        for (size_t i = 0; i < v.size(); ++i) v[i] = std::sin(0.37 * double(i));
+        const std::vector<double> hv = gpu::hessian_apply(dev, std::vector<double>(v.begin(), v.end()));
+        const RealVector hr = hessian_apply(ref, v);
+        num = den = 0;
+        for (size_t i = 0; i < hv.size(); ++i) {
+            num += (hv[i] - hr[i]) * (hv[i] - hr[i]);
+            den += hr[i] * hr[i];
+        }
+        CHECK(std::sqrt(num / den) < 1e-10);
+    }
     // error conventions: ZeroPivotError carries the index
     {
         bool threw = false;
