@@ -872,7 +872,7 @@ struct WarpPlan {
     double est = 0;
 };
 
-bool warp_layout(int nb, int L, int gp, int nrhs, int CS, int KG, WarpPlan& p) {
+bool warp_layout(int nb, int L, int gp, int nrhs, int CS, int KG, int KR, WarpPlan& p) {
     const int R = (nb + CS - 1) / CS;
     if (R > 32) return false;
     int Rp = 1;
@@ -901,7 +901,7 @@ bool warp_layout(int nb, int L, int gp, int nrhs, int CS, int KG, WarpPlan& p) {
     p.smem = a.off_bar + 512;
     p.CS = CS;
     p.KG = KG;
-    p.KR = KG >= 4 ? 2 : 1;
+    p.KR = KR;
     p.even = (R == Rp) && (nb % CS == 0) && (nb % (4 * (32 / Rp)) == 0);
     return p.smem <= 220 * 1024;
 }
@@ -959,11 +959,13 @@ bool warp_launch(const WarpPlan& p, int nrhs, cudaStream_t st) {
     return true;
 }
 
-#define FWI_WARP_VARIANTS(X) X(8, 8, 2) X(8, 4, 2) X(8, 2, 1) X(8, 1, 1) X(16, 8, 2) X(16, 4, 2) X(16, 2, 1) X(16, 1, 1)
+#define FWI_WARP_VARIANTS(X)                                                                      \
+    X(16, 8, 2) X(16, 8, 1) X(16, 6, 1) X(16, 4, 2) X(16, 4, 1) X(16, 2, 1) X(16, 1, 1) X(8, 8, 2) X(8, 8, 1) \
+    X(8, 4, 2) X(8, 2, 1) X(8, 1, 1)
 
 bool warp_dispatch_prepare(const WarpPlan& p, int* maxc) {
 #define X(cs, kg, kr) \
-    if (p.CS == cs && p.KG == kg)                                                        \
+    if (p.CS == cs && p.KG == kg && p.KR == kr)                                          \
         return p.even ? warp_prepare<cs, kg, kr, false, true>(p, maxc) : warp_prepare<cs, kg, kr, false, false>(p, maxc);
     FWI_WARP_VARIANTS(X)
 #undef X
@@ -972,7 +974,7 @@ bool warp_dispatch_prepare(const WarpPlan& p, int* maxc) {
 
 bool warp_dispatch_launch(const WarpPlan& p, int nrhs, cudaStream_t st) {
 #define X(cs, kg, kr) \
-    if (p.CS == cs && p.KG == kg)                                   \
+    if (p.CS == cs && p.KG == kg && p.KR == kr)                     \
         return !p.even ? warp_launch<cs, kg, kr, false, false>(p, nrhs, st)                         \
                        : (p.a.trace ? warp_launch<cs, kg, kr, true, true>(p, nrhs, st)                   \
                                     : warp_launch<cs, kg, kr, false, true>(p, nrhs, st));
@@ -989,13 +991,23 @@ bool warp_dispatch_launch(const WarpPlan& p, int nrhs, cudaStream_t st) {
 bool warp_plan(int nb, int L, int gp, int nrhs, WarpPlan& best) {
     const char* ecs = std::getenv("FWI_EXACT_CS");
     const char* ekg = std::getenv("FWI_EXACT_KG");
-    const int want_cs = ecs ? std::atoi(ecs) : 0, want_kg = ekg ? std::atoi(ekg) : 0;
+    const char* ekr = std::getenv("FWI_EXACT_KR");
+    const int want_cs = ecs ? std::atoi(ecs) : 0, want_kg = ekg ? std::atoi(ekg) : 0, want_kr = ekr ? std::atoi(ekr) : 0;
     bool found = false;
-    for (int cs : {16, 8})
-        for (int kg : {8, 4, 2, 1}) {
-            if ((want_cs && cs != want_cs) || (want_kg && kg != want_kg)) continue;
+    struct V {
+        int cs, kg, kr;
+    };
+    static const V variants[] = {
+#define X(cs, kg, kr) {cs, kg, kr},
+        FWI_WARP_VARIANTS(X)
+#undef X
+    };
+    for (const V& v : variants) {
+        const int cs = v.cs, kg = v.kg, kr = v.kr;
+        if (true) {
+            if ((want_cs && cs != want_cs) || (want_kg && kg != want_kg) || (want_kr && kr != want_kr)) continue;
             WarpPlan p;
-            if (!warp_layout(nb, L, gp, nrhs, cs, kg, p)) continue;
+            if (!warp_layout(nb, L, gp, nrhs, cs, kg, kr, p)) continue;
             int maxc = 0;
             if (!warp_dispatch_prepare(p, &maxc)) continue;
             const int groups = (nrhs + kg - 1) / kg;
@@ -1009,6 +1021,7 @@ bool warp_plan(int nb, int L, int gp, int nrhs, WarpPlan& best) {
                 found = true;
             }
         }
+    }
     return found;
 }
 
@@ -1205,7 +1218,7 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
         // process-wide, so guarded for contexts driven from several host threads
         static std::mutex mu;
         static std::vector<std::pair<std::array<int, 3>, WarpPlan>> cache;
-        const bool forced = std::getenv("FWI_EXACT_CS") || std::getenv("FWI_EXACT_KG");
+        const bool forced = std::getenv("FWI_EXACT_CS") || std::getenv("FWI_EXACT_KG") || std::getenv("FWI_EXACT_KR");
         const std::array<int, 3> key{f.nb, f.L, nrhs};
         bool have = false;
         WarpPlan plan;
