@@ -983,11 +983,12 @@ bool warp_dispatch_launch(const WarpPlan& p, int nrhs, cudaStream_t st) {
     return false;
 }
 
-// Pick (CS, KG) by a model of one line step, fitted to clock64 traces of the
-// kernel on B200 (tools/sweep_trace.py): a consumer warp's step is bound by its
-// dependent instruction stream, ~1400 cycles of fixed work (barrier wake-ups,
-// butterfly, pushes, DSMEM flight) plus ~35 cycles per column element per RHS it
-// owns; clusters beyond the resident limit run in further waves.
+// Pick (CS, KG, KR) by a model of one line step, fitted to clock64 traces of the
+// kernel on B200 (tools/sweep_trace.py, tools/sweep_grid.sh): a consumer warp's step
+// is bound by its dependent instruction stream, ~1400 cycles of fixed work (barrier
+// wake-ups, butterfly, pushes, DSMEM flight) plus ~35 cycles per column element per
+// RHS it owns, plus ~4.5 cycles per element for every consumer warp beyond two that
+// shares the SM; clusters beyond the resident limit run in further waves.
 bool warp_plan(int nb, int L, int gp, int nrhs, WarpPlan& best) {
     const char* ecs = std::getenv("FWI_EXACT_CS");
     const char* ekg = std::getenv("FWI_EXACT_KG");
@@ -1014,9 +1015,10 @@ bool warp_plan(int nb, int L, int gp, int nrhs, WarpPlan& best) {
             const int waves = (groups + maxc - 1) / maxc;
             const int ncls = 32 / p.a.Rp;
             const double per_lane = double((nb + ncls - 1) / ncls);
-            p.est = double(waves) * (2.0 * L - 1) * (1400.0 + 35.0 * per_lane * p.KR);
-            // ties go to fewer clusters (less G traffic through L2)
-            if (!found || p.est < best.est - 1e-9 || (p.est <= best.est + 1e-9 && kg > best.KG)) {
+            const int nw = kg / kr;
+            p.est = double(waves) * (2.0 * L - 1) *
+                    (1400.0 + 35.0 * per_lane * kr + 4.5 * per_lane * kr * std::max(0, nw - 2));
+            if (!found || p.est < best.est - 1e-9) {
                 best = p;
                 found = true;
             }
@@ -1117,7 +1119,22 @@ size_t sweep_smem(int nb) {
 
 void exact_factor(Ctx& c) {
     auto f = std::make_unique<ExactFactor>();
-    f->col_lines = c.nz <= c.nx;
+    f->col_lines = c.nz <= c.nx;  // short lines by default (least factor work and storage)
+    // A line step is latency-bound (fixed dependent chain + work per column), so
+    // fewer, longer lines can sweep faster: take the long-line orientation when the
+    // sweep model says so (config 1: 64 lines of 128 instead of 128 lines of 64).
+    {
+        const int nbs = std::min(c.nx, c.nz), nbl = std::max(c.nx, c.nz);
+        const char* eo = std::getenv("FWI_EXACT_LINES");  // "short" | "long" (diagnostics)
+        const std::string o = eo ? eo : "";
+        WarpPlan ps, pl;
+        if (o == "long" && nbl <= 512) {
+            f->col_lines = !f->col_lines;
+        } else if (o.empty() && nbl <= 512 && nbs != nbl && warp_plan(nbs, nbl, nbs + 1, c.K, ps) &&
+                   warp_plan(nbl, nbs, nbl + 1, c.K, pl) && pl.est < 0.9 * ps.est) {
+            f->col_lines = !f->col_lines;
+        }
+    }
     f->nb = f->col_lines ? c.nz : c.nx;
     f->L = f->col_lines ? c.nx : c.nz;
     const int nb = f->nb, L = f->L;
