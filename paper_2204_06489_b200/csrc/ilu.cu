@@ -358,6 +358,7 @@ void run_sweep(const Sweep& s, int64_t n, int nrhs, double2* x, cudaStream_t st)
     if (meta_smem) meta += lm + 16;
     const size_t smem = size_t(n) * sizeof(double2) + meta;
     const char* mode = std::getenv("FWI_ILU_GLOBAL");  // diagnostics: "1" = unstaged global kernel
+    static const int nthr = std::getenv("FWI_ILU_THREADS") ? std::atoi(std::getenv("FWI_ILU_THREADS")) : 256;
     if (smem <= 220 * 1024 && !mode) {
         static size_t set = 0;
         if (smem > set) {
@@ -365,7 +366,7 @@ void run_sweep(const Sweep& s, int64_t n, int nrhs, double2* x, cudaStream_t st)
                                     int(smem)));
             set = smem;
         }
-        ilu_sweep_smem<KIND, true><<<nrhs, 256, smem, st>>>(int(n), s.nlev, s.lmeta.p, meta_smem, s.lvl_rows.p,
+        ilu_sweep_smem<KIND, true><<<nrhs, nthr, smem, st>>>(int(n), s.nlev, s.lmeta.p, meta_smem, s.lvl_rows.p,
                                                            s.rstart.p, s.lidx.p, s.lval.p, x, s.ecap, s.rcap);
         CK_LAUNCH();
         return;
@@ -377,7 +378,7 @@ void run_sweep(const Sweep& s, int64_t n, int nrhs, double2* x, cudaStream_t st)
                                     int(meta)));
             set = meta;
         }
-        ilu_sweep_smem<KIND, false><<<nrhs, 256, meta, st>>>(int(n), s.nlev, s.lmeta.p, meta_smem,
+        ilu_sweep_smem<KIND, false><<<nrhs, nthr, meta, st>>>(int(n), s.nlev, s.lmeta.p, meta_smem,
                                                             s.lvl_rows.p, s.rstart.p, s.lidx.p, s.lval.p, x,
                                                             s.ecap, s.rcap);
         CK_LAUNCH();
