@@ -112,3 +112,45 @@ def test_block_gauss_jordan_factor_with_cluster_sweep():
         want = ref.solve(b, _abi.FWI_PRECOND_EXACT, adj)
         got = dev.solve(b, fw.PrecondMode.exact, adj)
         assert rel(got, want) <= 1e-10, (adj, rel(got, want))
+
+
+@pytest.mark.parametrize("lines", ["short", "long"])
+@pytest.mark.parametrize("mk", [lambda: small_problem(nx=40, nz=26, n_pml=4, K=3, R=5),
+                                lambda: small_problem(nx=22, nz=37, n_pml=3, K=2, R=4, seed=5)])
+def test_exact_solve_both_line_orientations(mk, lines):
+    """The exact solver may cut the grid into short or long lines (chosen by its step
+    model); both orientations match the reference LU."""
+    p = mk()
+    ref = po.Ref(p, full=False, exact=True)
+    os.environ["FWI_EXACT_LINES"] = lines
+    try:
+        dev = fw.GnState(p, exact=True)
+    finally:
+        del os.environ["FWI_EXACT_LINES"]
+    rng = np.random.default_rng(21)
+    b = rng.standard_normal(p.n) + 1j * rng.standard_normal(p.n)
+    for adj in (False, True):
+        want = ref.solve(b, _abi.FWI_PRECOND_EXACT, adj)
+        got = dev.solve(b, fw.PrecondMode.exact, adj)
+        assert rel(got, want) <= 1e-10, (lines, adj, rel(got, want))
+
+
+@pytest.mark.parametrize("restart", [1, 2])
+def test_host_basis_small_restart_matches_reference(restart):
+    """Host-resident basis at the restart lengths config 5 uses (1-4), incl. stagnation."""
+    p = c1_problem()
+    p.d_obs = po.ref_simulate(p)
+    ref = po.Ref(p, full=True, exact=True)
+    q = c1_problem()
+    q.d_obs, q.u, q.r = p.d_obs, ref.u(), ref.residual()
+    dev = fw.GnState(q, exact=True)
+    _, log_r = ref.fsgn(_abi.FWI_PRECOND_EXACT, restart, 0.0, 12, 0)
+    os.environ["FWI_GMRES_HOST_BASIS"] = "1"
+    try:
+        _, log_d = fw.fsgn_gmres_step(dev, fw.FsgnOptions(restart=restart, tol=0.0, maxit=12, ecg_stride=0))
+    finally:
+        del os.environ["FWI_GMRES_HOST_BASIS"]
+    rr, rd = np.array(log_r.residuals()), np.array(log_d.residuals())
+    assert len(rr) == len(rd) and log_d.stagnated == log_r.stagnated
+    mask = rr >= 1e-6
+    assert (np.abs(rd - rr)[mask] / rr[mask]).max() <= 1e-8
