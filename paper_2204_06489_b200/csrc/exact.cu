@@ -46,6 +46,8 @@ struct ExactFactor {
     DevBuf<int> status;
     bool dense = false;     // long lines: GEMM line sweeps (dense.cu)
     bool dense_factor = false;  // whole-GPU block Gauss-Jordan per line (dense.cu)
+    bool twisted = false;       // factored from both ends towards line `mid` (two sweep chains)
+    int mid = 0;
     DenseWork dwork;
     DevBuf<double2> tbuf;   // dense sweep operand (nrhs x nb)
 };
@@ -74,10 +76,13 @@ __global__ void extract_lines(bool col_lines, int nx, int L, int nb, const doubl
     coup[t] = col_lines ? east[node] : south[node];
 }
 
-// S_i = T_i - E_{i-1} G_{i-1} E_{i-1} into A (row pitch lda), one thread per entry
+// S_i = T_i - E_a G_a E_a - E_b G_b E_b into A (row pitch gp), one thread per entry;
+// (cA, GA) is the neighbour already eliminated on one side (the previous line of a
+// sweep), (cB, GB) the other side (the twisted factorisation's middle line), either null.
 __global__ void form_schur(bool col_lines, int nx, int nb, int line, const double2* __restrict__ diag,
                            const double2* __restrict__ east, const double2* __restrict__ south,
-                           const double2* __restrict__ coup, const double2* __restrict__ Gprev, int gp,
+                           const double2* __restrict__ cA, const double2* __restrict__ GA,
+                           const double2* __restrict__ cB, const double2* __restrict__ GB, int gp,
                            double2* __restrict__ A) {
     const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (t >= int64_t(nb) * nb) return;
@@ -88,9 +93,13 @@ __global__ void form_schur(bool col_lines, int nx, int nb, int line, const doubl
     else if (b == a + 1) v = col_lines ? south[na] : east[na];
     else if (a == b + 1) v = col_lines ? south[line_node(col_lines, nx, line, b)]
                                        : east[line_node(col_lines, nx, line, b)];
-    if (line > 0) {
-        const double2 ea = coup[int64_t(line - 1) * nb + a], eb = coup[int64_t(line - 1) * nb + b];
-        const double2 t2 = fmul(fmul(ea, Gprev[int64_t(a) * gp + b]), eb);
+    if (GA) {
+        const double2 t2 = fmul(fmul(cA[a], GA[int64_t(a) * gp + b]), cA[b]);
+        v.x -= t2.x;
+        v.y -= t2.y;
+    }
+    if (GB) {
+        const double2 t2 = fmul(fmul(cB[a], GB[int64_t(a) * gp + b]), cB[b]);
         v.x -= t2.x;
         v.y -= t2.y;
     }
@@ -627,6 +636,17 @@ uint32_t al128(size_t b) { return uint32_t((b + 127) / 128 * 128); }
 // ---------------------------------------------------------------------------
 constexpr int kWMaxStages = 8;
 
+// A chain of line steps over lines first, first+dir, ... (count lines):
+//   mode 0: forward over the chain, then backward over it (the classical sweep);
+//   mode 1: forward only (y_i into Y);
+//   mode 2: backward only, starting from the boundary solution xin of the line
+//           before `first` (x_i into W).
+// The twisted solve runs two chains per launch (top and bottom half of the lines).
+struct SweepChain {
+    int first = 0, count = 0, dir = 1, mode = 0;
+    const double2* xin = nullptr;  // mode 2: boundary line's solution, [k][m]
+};
+
 struct WSweepArgs {
     int L, nb, nrhs, gp, R, Rp, nst;
     const double2* G;
@@ -635,7 +655,19 @@ struct WSweepArgs {
     double2* Y;
     uint32_t off_e, off_b, stage_bytes, off_y, off_w, off_bar;
     unsigned long long* trace;  // diagnostics: per-step clock64 stamps of CTA 0 / warp 0, or null
+    SweepChain chain[2];        // clusters [0, groups0) run chain[0], the rest chain[1]
+    int groups0;
 };
+
+__host__ __device__ __forceinline__ int chain_steps(const SweepChain& c) {
+    return c.mode == 0 ? 2 * c.count - 1 : c.count;
+}
+__host__ __device__ __forceinline__ int chain_line(const SweepChain& c, int st) {
+    return c.first + c.dir * ((c.mode == 0 && st >= c.count) ? 2 * c.count - 2 - st : st);
+}
+__host__ __device__ __forceinline__ bool chain_fwd(const SweepChain& c, int st) {
+    return c.mode == 1 || (c.mode == 0 && st < c.count);
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -677,8 +709,11 @@ __global__ void __launch_bounds__((KG / KR + 1) * 32) sweep_warp_kernel(const WS
     extern __shared__ __align__(128) unsigned char wsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
-    const int grp = blockIdx.x / CS;
-    const int nb = a.nb, L = a.L, gp = a.gp, nrhs = a.nrhs, R = a.R, Rp = a.Rp;
+    const int cid = blockIdx.x / CS;
+    const int chn = cid < a.groups0 ? 0 : 1;
+    const SweepChain C = a.chain[chn];
+    const int grp = chn == 0 ? cid : cid - a.groups0;
+    const int nb = a.nb, gp = a.gp, nrhs = a.nrhs, R = a.R, Rp = a.Rp;
     const int S = a.nst, smask = a.nst - 1;  // power of two
     const int nbp = nb + 1;
     const int k0 = grp * KG;
@@ -689,7 +724,8 @@ __global__ void __launch_bounds__((KG / KR + 1) * 32) sweep_warp_kernel(const WS
     uint64_t* full = reinterpret_cast<uint64_t*>(wsm + a.off_bar);
     uint64_t* empty = full + kWMaxStages;
     uint64_t* rbar = empty + kWMaxStages;  // [2][NW]
-    const int nsteps = 2 * L - 1;
+    const int nsteps = chain_steps(C);
+    const int last_fwd_line = C.first + C.dir * (C.count - 1);
 
     if (threadIdx.x == 0) {
         for (int q = 0; q < S; ++q) {
@@ -711,11 +747,11 @@ __global__ void __launch_bounds__((KG / KR + 1) * 32) sweep_warp_kernel(const WS
                 const int sb = st & smask;
                 if (st >= S) bar_wait_lazy(&empty[sb], ((st - S) / S) & 1);
                 unsigned char* buf = wsm + sb * a.stage_bytes;
-                const bool fwd = st < L;
-                const int i = fwd ? st : 2 * L - 2 - st;
-                // coupling that scales this step's result before it is pushed: the next
-                // step uses E_i (forward, line i+1) or E_{i-1} (backward, line i-1)
-                const int cidx = st + 1 < L ? st : 2 * L - 3 - st;
+                const bool fwd = chain_fwd(C, st);
+                const int i = chain_line(C, st);
+                // coupling that scales this step's result before it is pushed: the one
+                // between this line and the chain's next line
+                const int cidx = st + 1 < nsteps ? min(i, chain_line(C, st + 1)) : 0;
                 const uint32_t eb = (st + 1 < nsteps) ? ebytes : 0u;
                 const uint32_t bb = fwd ? bbytes : 0u;
                 bar_expect(&full[sb], gbytes + eb + bb);
@@ -747,6 +783,20 @@ __global__ void __launch_bounds__((KG / KR + 1) * 32) sweep_warp_kernel(const WS
         //   forward   y_i = G_i (b_i - z_{i-1}),   backward  x_i = y_i - G_i z'_{i+1},
         // and the CTA scales its own rows of the result before pushing them.
         // EVEN: every lane owns a row and nj is a multiple of 4 (no element guards).
+        if (C.mode == 2 && kr > 0) {
+            // the chain's first step receives E (x of the boundary line) from global memory
+            const int bl = C.first - C.dir;
+            const double2* e = a.coup + int64_t(min(C.first, bl)) * nb;
+            for (int q = 0; q < kr; ++q) {
+                double2* dst = yfull + (KG + kw + q) * nbp;  // the buffer step 0 reads
+                const double2* src = C.xin + int64_t(k0 + kw + q) * nb;
+                for (int m = lane; m < nb; m += 32) {
+                    const double2 ev = e[m], xv = src[m];
+                    dst[m] = make_double2(ev.x * xv.x - ev.y * xv.y, ev.x * xv.y + ev.y * xv.x);
+                }
+            }
+            __syncwarp();
+        }
         int sb = 0;
         uint32_t fph = 0;
         auto step = [&](auto fwd_tag, auto first_tag, const int st, const int i) {
@@ -776,7 +826,7 @@ __global__ void __launch_bounds__((KG / KR + 1) * 32) sweep_warp_kernel(const WS
                 const double2* z = yfull + (((st + 1) & 1) * KG + kw) * nbp + cls;
                 const double2* bq = bs + kw * nb + cls;
                 const double2 esc = has_row && st + 1 < nsteps ? es[row] : make_double2(0.0, 0.0);
-                if (!first) bar_wait(&rbar[((st - 1) & 1) * NW + w], ((st - 1) >> 1) & 1);
+                if (!first && st > 0) bar_wait(&rbar[((st - 1) & 1) * NW + w], ((st - 1) >> 1) & 1);
                 if (tr) a.trace[8 * st + 2] = gtimer();
                 if (tr) a.trace[8 * st + 3] = gtimer();
                 // w_j = b_j - z_j (forward) | b_j (first line) | z_j (backward)
@@ -839,7 +889,7 @@ __global__ void __launch_bounds__((KG / KR + 1) * 32) sweep_warp_kernel(const WS
                                 const int64_t off = i * line_stride + q * nb;
                                 if (fwd) {
                                     Yrow[off] = v[q];
-                                    if (i == L - 1) Wrow[off] = v[q];
+                                    if (C.mode == 0 && i == last_fwd_line) Wrow[off] = v[q];
                                 } else {
                                     Wrow[off] = v[q];
                                 }
@@ -856,12 +906,29 @@ __global__ void __launch_bounds__((KG / KR + 1) * 32) sweep_warp_kernel(const WS
                 fph ^= 1u;
             }
         };
-        step(std::true_type{}, std::true_type{}, 0, 0);
-        for (int st = 1; st < L; ++st) step(std::true_type{}, std::false_type{}, st, st);
-        for (int st = L; st < nsteps; ++st) step(std::false_type{}, std::false_type{}, st, 2 * L - 2 - st);
+        if (C.mode != 2) {
+            step(std::true_type{}, std::true_type{}, 0, chain_line(C, 0));
+            for (int st = 1; st < C.count; ++st) step(std::true_type{}, std::false_type{}, st, chain_line(C, st));
+        }
+        for (int st = (C.mode == 2 ? 0 : C.count); C.mode != 1 && st < nsteps; ++st)
+            step(std::false_type{}, std::false_type{}, st, chain_line(C, st));
     }
     __syncthreads();
     cluster_sync_all();
+}
+
+// twisted solve, middle line: T[k][m] = b[k][m] - eA[m] yA[k][m] - eB[m] yB[k][m]
+__global__ void middle_rhs(int nb, int64_t blk, const double2* __restrict__ b, const double2* __restrict__ eA,
+                           const double2* __restrict__ yA, const double2* __restrict__ eB,
+                           const double2* __restrict__ yB, double2* __restrict__ T) {
+    const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (t >= blk) return;
+    const int m = int(t % nb);
+    const double2 a = eA[m], ya = yA[t], e = eB[m], yb = yB[t];
+    double2 v = b[t];
+    v.x -= (a.x * ya.x - a.y * ya.y) + (e.x * yb.x - e.y * yb.y);
+    v.y -= (a.x * ya.y + a.y * ya.x) + (e.x * yb.y + e.y * yb.x);
+    T[t] = v;
 }
 
 struct WarpPlan {
@@ -880,6 +947,11 @@ bool warp_layout(int nb, int L, int gp, int nrhs, int CS, int KG, int KR, WarpPl
     WSweepArgs& a = p.a;
     a = WSweepArgs{};
     a.L = L;
+    a.chain[0].first = 0;
+    a.chain[0].count = L;
+    a.chain[0].dir = 1;
+    a.chain[0].mode = 0;
+    a.chain[1].count = 0;
     a.nb = nb;
     a.nrhs = nrhs;
     a.gp = gp;
@@ -943,8 +1015,11 @@ template <int CS, int KG, int KR, bool TRACE, bool EVEN>
 bool warp_launch(const WarpPlan& p, int nrhs, cudaStream_t st) {
     if (!warp_prepare<CS, KG, KR, TRACE, EVEN>(p, nullptr)) return false;
     const int groups = (nrhs + KG - 1) / KG;
+    const int chains = p.a.chain[1].count > 0 ? 2 : 1;
+    WSweepArgs args = p.a;
+    args.groups0 = groups;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(groups * CS);
+    cfg.gridDim = dim3(chains * groups * CS);
     cfg.blockDim = dim3((KG / KR + 1) * 32);
     cfg.dynamicSmemBytes = p.smem;
     cfg.stream = st;
@@ -955,7 +1030,7 @@ bool warp_launch(const WarpPlan& p, int nrhs, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, sweep_warp_kernel<CS, KG, KR, TRACE, EVEN>, p.a));
+    CK(cudaLaunchKernelEx(&cfg, sweep_warp_kernel<CS, KG, KR, TRACE, EVEN>, args));
     return true;
 }
 
@@ -989,7 +1064,8 @@ bool warp_dispatch_launch(const WarpPlan& p, int nrhs, cudaStream_t st) {
 // wake-ups, butterfly, pushes, DSMEM flight) plus ~35 cycles per column element per
 // RHS it owns, plus ~4.5 cycles per element for every consumer warp beyond two that
 // shares the SM; clusters beyond the resident limit run in further waves.
-bool warp_plan(int nb, int L, int gp, int nrhs, WarpPlan& best) {
+bool warp_plan(int nb, int L, int gp, int nrhs, WarpPlan& best, int chains = 1, int steps = -1) {
+    if (steps < 0) steps = 2 * L - 1;
     const char* ecs = std::getenv("FWI_EXACT_CS");
     const char* ekg = std::getenv("FWI_EXACT_KG");
     const char* ekr = std::getenv("FWI_EXACT_KR");
@@ -1011,12 +1087,12 @@ bool warp_plan(int nb, int L, int gp, int nrhs, WarpPlan& best) {
             if (!warp_layout(nb, L, gp, nrhs, cs, kg, kr, p)) continue;
             int maxc = 0;
             if (!warp_dispatch_prepare(p, &maxc)) continue;
-            const int groups = (nrhs + kg - 1) / kg;
+            const int groups = chains * ((nrhs + kg - 1) / kg);
             const int waves = (groups + maxc - 1) / maxc;
             const int ncls = 32 / p.a.Rp;
             const double per_lane = double((nb + ncls - 1) / ncls);
             const int nw = kg / kr;
-            p.est = double(waves) * (2.0 * L - 1) *
+            p.est = double(waves) * double(steps) *
                     (1400.0 + 35.0 * per_lane * kr + 4.5 * per_lane * kr * std::max(0, nw - 2));
             if (!found || p.est < best.est - 1e-9) {
                 best = p;
@@ -1155,15 +1231,43 @@ void exact_factor(Ctx& c) {
     const char* ef = std::getenv("FWI_EXACT_FACTOR");
     f->dense = nb > 512 || force_dense;
     f->dense_factor = f->dense || (nb > 112 && !(ef && std::string(ef) == "cta"));
+    if (!f->dense && std::getenv("FWI_EXACT_TWISTED") && std::string(std::getenv("FWI_EXACT_TWISTED")) == "1")
+        f->dense_factor = true;  // the twisted factorisation is built with the block Gauss-Jordan
+    // Twisted factorisation: Schur recursions from both ends meet at the middle line,
+    // so a solve is two concurrent sweep chains of ~L/2 lines each (then a dense
+    // solve of the middle line) instead of one chain of L: a line step is latency-
+    // bound, so this halves the sweep. Used when the step model says it pays.
+    if (f->dense_factor && !f->dense && L >= 8) {
+        const char* et = std::getenv("FWI_EXACT_TWISTED");
+        if (et) {
+            f->twisted = std::string(et) == "1";
+        } else {
+            WarpPlan p1, p2;
+            const int m = L / 2;
+            const int steps2 = 2 * std::max(m, L - 1 - m);
+            f->twisted = warp_plan(nb, L, nb + 1, c.K, p1) && warp_plan(nb, L, nb + 1, c.K, p2, 2, steps2) &&
+                         p2.est + 40000.0 < 0.9 * p1.est;
+        }
+    }
     if (f->dense_factor) {
         const int64_t nn = int64_t(nb) * nb;
-        for (int i = 0; i < L; ++i) {
-            double2* Gi = f->G.p + i * int64_t(nb) * f->gp;
-            form_schur<<<int((nn + 255) / 256), 256, 0, c.stream>>>(
-                f->col_lines, c.nx, nb, i, c.diag.p, c.east.p, c.south.p, f->coup.p,
-                i > 0 ? Gi - int64_t(nb) * f->gp : nullptr, f->gp, Gi);
+        auto Gl = [&](int i) { return f->G.p + i * int64_t(nb) * f->gp; };
+        auto cl = [&](int i) { return f->coup.p + int64_t(i) * nb; };  // coupling of lines i, i+1
+        auto line = [&](int i, const double2* cA, const double2* GA, const double2* cB, const double2* GB) {
+            form_schur<<<int((nn + 255) / 256), 256, 0, c.stream>>>(f->col_lines, c.nx, nb, i, c.diag.p, c.east.p,
+                                                                    c.south.p, cA, GA, cB, GB, f->gp, Gl(i));
             CK_LAUNCH();
-            dense_invert(c.stream, nb, Gi, f->gp, f->dwork, f->status.p, i * nb);
+            dense_invert(c.stream, nb, Gl(i), f->gp, f->dwork, f->status.p, i * nb);
+        };
+        if (!f->twisted) {
+            for (int i = 0; i < L; ++i) line(i, i > 0 ? cl(i - 1) : nullptr, i > 0 ? Gl(i - 1) : nullptr, nullptr, nullptr);
+        } else {
+            const int m = L / 2;
+            f->mid = m;
+            for (int i = 0; i < m; ++i) line(i, i > 0 ? cl(i - 1) : nullptr, i > 0 ? Gl(i - 1) : nullptr, nullptr, nullptr);
+            for (int i = L - 1; i > m; --i)
+                line(i, i < L - 1 ? cl(i) : nullptr, i < L - 1 ? Gl(i + 1) : nullptr, nullptr, nullptr);
+            line(m, cl(m - 1), Gl(m - 1), cl(m), Gl(m + 1));
         }
     } else {
     const bool smem = nb <= 112;
@@ -1234,9 +1338,12 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
         // plans are cached per (nb, L, nrhs) (the model queries cluster occupancy);
         // process-wide, so guarded for contexts driven from several host threads
         static std::mutex mu;
-        static std::vector<std::pair<std::array<int, 3>, WarpPlan>> cache;
+        static std::vector<std::pair<std::array<int, 4>, WarpPlan>> cache;
         const bool forced = std::getenv("FWI_EXACT_CS") || std::getenv("FWI_EXACT_KG") || std::getenv("FWI_EXACT_KR");
-        const std::array<int, 3> key{f.nb, f.L, nrhs};
+        const std::array<int, 4> key{f.nb, f.L, nrhs, f.twisted ? 1 : 0};
+        const int m = f.mid;
+        const int chains = f.twisted ? 2 : 1;
+        const int steps = f.twisted ? 2 * std::max(m, f.L - 1 - m) : 2 * f.L - 1;
         bool have = false;
         WarpPlan plan;
         {
@@ -1246,7 +1353,7 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
                     plan = e.second;
                     have = true;
                 }
-            if (!have && warp_plan(f.nb, f.L, f.gp, nrhs, plan)) {
+            if (!have && warp_plan(f.nb, f.L, f.gp, nrhs, plan, chains, steps)) {
                 if (!forced) cache.emplace_back(key, plan);
                 have = true;
             }
@@ -1265,8 +1372,33 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
                 CK(cudaMemsetAsync(tbuf.p, 0, tbuf.count * 8, c.stream));
                 p.a.trace = tbuf.p;
             }
-            done = warp_dispatch_launch(p, nrhs, c.stream);
-            if (tpath && done) {
+            if (!f.twisted) {
+                done = warp_dispatch_launch(p, nrhs, c.stream);
+            } else {
+                // (1) both halves forward, concurrently: y_i for lines 0..m-1 and L-1..m+1
+                p.a.trace = nullptr;
+                p.a.chain[0] = SweepChain{0, m, 1, 1, nullptr};
+                p.a.chain[1] = SweepChain{f.L - 1, f.L - 1 - m, -1, 1, nullptr};
+                done = warp_dispatch_launch(p, nrhs, c.stream);
+                if (done) {
+                    // (2) middle line: x_m = G_m (b_m - E_{m-1} y_{m-1} - E_m y_{m+1})
+                    ExactFactor& fm = const_cast<ExactFactor&>(f);
+                    if (fm.tbuf.count < size_t(nrhs) * f.nb) fm.tbuf.alloc(size_t(nrhs) * f.nb);
+                    const int64_t blk = int64_t(nrhs) * f.nb;
+                    middle_rhs<<<int((blk + 255) / 256), 256, 0, c.stream>>>(
+                        f.nb, blk, W + m * blk, f.coup.p + int64_t(m - 1) * f.nb, f.ybuf.p + (m - 1) * blk,
+                        f.coup.p + int64_t(m) * f.nb, f.ybuf.p + (m + 1) * blk, fm.tbuf.p);
+                    CK_LAUNCH();
+                    cgemm(c.stream, true, nrhs, f.nb, f.nb, 1.0, fm.tbuf.p, f.nb, f.G.p + int64_t(m) * f.nb * f.gp,
+                          f.gp, nullptr, 0, W + m * blk, f.nb);
+                    // (3) both halves backward from the middle line outwards
+                    p.a.chain[0] = SweepChain{m - 1, m, -1, 2, W + m * blk};
+                    p.a.chain[1] = SweepChain{m + 1, f.L - 1 - m, 1, 2, W + m * blk};
+                    done = warp_dispatch_launch(p, nrhs, c.stream);
+                    if (!done) throw FwiError(FWI_ERR_CUDA, "exact solve: twisted backward sweep could not launch");
+                }
+            }
+            if (tpath && done && !f.twisted) {
                 std::vector<unsigned long long> h(tbuf.count);
                 CK(cudaMemcpyAsync(h.data(), tbuf.p, tbuf.count * 8, cudaMemcpyDeviceToHost, c.stream));
                 CK(cudaStreamSynchronize(c.stream));

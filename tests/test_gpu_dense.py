@@ -154,3 +154,29 @@ def test_host_basis_small_restart_matches_reference(restart):
     assert len(rr) == len(rd) and log_d.stagnated == log_r.stagnated
     mask = rr >= 1e-6
     assert (np.abs(rd - rr)[mask] / rr[mask]).max() <= 1e-8
+
+
+@pytest.mark.parametrize("mk", [lambda: small_problem(nx=40, nz=26, n_pml=4, K=3, R=5),
+                                lambda: small_problem(nx=22, nz=37, n_pml=3, K=2, R=4, seed=5),
+                                lambda: small_problem(nx=31, nz=23, n_pml=4, K=9, R=7, seed=3)])
+def test_twisted_factorisation_matches_reference(mk):
+    """Factorisation from both ends meeting at the middle line; the solve runs the two
+    half-sweeps concurrently. Forced with FWI_EXACT_TWISTED=1."""
+    p = mk()
+    ref = po.Ref(p, full=False, exact=True)
+    os.environ["FWI_EXACT_TWISTED"] = "1"
+    try:
+        dev = fw.GnState(p, exact=True)
+    finally:
+        del os.environ["FWI_EXACT_TWISTED"]
+    rng = np.random.default_rng(31)
+    b = rng.standard_normal((2, p.n)) + 1j * rng.standard_normal((2, p.n))
+    for adj in (False, True):
+        for r in range(2):
+            want = ref.solve(b[r], _abi.FWI_PRECOND_EXACT, adj)
+            got = dev.solve(b[r], fw.PrecondMode.exact, adj)
+            assert rel(got, want) <= 1e-10, (adj, rel(got, want))
+    x = random_kkt(p, 4)
+    want = ref.precond_apply(x, _abi.FWI_PRECOND_EXACT)
+    got = fw.precond_apply(dev, fw.KktVector.from_host(dev, x), fw.PrecondMode.exact).to_host()
+    assert rel(got, want) <= 1e-10
