@@ -172,27 +172,64 @@ struct MgsAllArgs {
     const double2* v[64];
 };
 
+template <int QMAX>
 __global__ void __launch_bounds__(kRedThreads) mgs_all_kernel(double2* __restrict__ w, MgsAllArgs a, int m,
                                                               int64_t len2, double* partials, unsigned* ticket,
                                                               volatile unsigned* flag, unsigned epoch, double* h) {
     __shared__ double sh[32];
     __shared__ bool last;
+    // QMAX > 0: this thread's grid-stride elements of w (at most QMAX) stay in registers
+    // for the whole sweep and the next basis vector's elements are loaded before the
+    // grid barrier; same elements, same order of accumulation as the streaming form.
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x, t0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    double2 wq[QMAX > 0 ? QMAX : 1], nq[QMAX > 0 ? QMAX : 1], pq[QMAX > 0 ? QMAX : 1];
+    if constexpr (QMAX > 0) {
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q) {
+            const int64_t t = t0 + q * stride;
+            wq[q] = t < len2 ? w[t] : make_double2(0.0, 0.0);
+            nq[q] = (t < len2 && m > 0) ? a.v[0][t] : make_double2(0.0, 0.0);
+        }
+    }
     for (int i = 0; i <= m; ++i) {
         const double2* vprev = i > 0 ? a.v[i - 1] : nullptr;
         const double2* vnext = i < m ? a.v[i] : nullptr;
         const double nh = vprev ? -__ldcg(h + i - 1) : 0.0;  // published by another CTA: bypass L1
         double acc = 0.0;
-        for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < len2;
-             t += int64_t(gridDim.x) * blockDim.x) {
-            double2 wv = w[t];
-            if (vprev) {
-                const double2 pv = vprev[t];
-                wv.x = __dadd_rn(wv.x, __dmul_rn(nh, pv.x));
-                wv.y = __dadd_rn(wv.y, __dmul_rn(nh, pv.y));
-                w[t] = wv;
+        if constexpr (QMAX > 0) {
+#pragma unroll
+            for (int q = 0; q < QMAX; ++q) {
+                const int64_t t = t0 + q * stride;
+                if (t < len2) {
+                    double2 wv = wq[q];
+                    if (vprev) {
+                        const double2 pv = pq[q];  // v_{i-1}: the previous step's vnext
+                        wv.x = __dadd_rn(wv.x, __dmul_rn(nh, pv.x));
+                        wv.y = __dadd_rn(wv.y, __dmul_rn(nh, pv.y));
+                        wq[q] = wv;
+                    }
+                    const double2 nv = vnext ? nq[q] : wv;
+                    acc += nv.x * wv.x + nv.y * wv.y;
+                }
             }
-            const double2 nv = vnext ? vnext[t] : wv;
-            acc += nv.x * wv.x + nv.y * wv.y;
+#pragma unroll
+            for (int q = 0; q < QMAX; ++q) {  // v_i becomes the next step's vprev; prefetch v_{i+1}
+                const int64_t t = t0 + q * stride;
+                pq[q] = nq[q];
+                if (i + 1 < m && t < len2) nq[q] = a.v[i + 1][t];
+            }
+        } else {
+            for (int64_t t = t0; t < len2; t += stride) {
+                double2 wv = w[t];
+                if (vprev) {
+                    const double2 pv = vprev[t];
+                    wv.x = __dadd_rn(wv.x, __dmul_rn(nh, pv.x));
+                    wv.y = __dadd_rn(wv.y, __dmul_rn(nh, pv.y));
+                    w[t] = wv;
+                }
+                const double2 nv = vnext ? vnext[t] : wv;
+                acc += nv.x * wv.x + nv.y * wv.y;
+            }
         }
         acc = block_sum(acc, sh);
         if (threadIdx.x == 0) {
@@ -217,6 +254,13 @@ __global__ void __launch_bounds__(kRedThreads) mgs_all_kernel(double2* __restric
             while (flag[0] < epoch + unsigned(i) + 1u) __nanosleep(32);
         __syncthreads();
         __threadfence();
+    }
+    if constexpr (QMAX > 0) {
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q) {
+            const int64_t t = t0 + q * stride;
+            if (t < len2) w[t] = wq[q];
+        }
     }
 }
 
@@ -316,14 +360,20 @@ bool dev_mgs_all(cudaStream_t st, double* w, const double* const* v, int m, doub
     static int ok = -1;
     if (ok < 0) {
         int per_sm = 0;
-        ok = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgs_all_kernel, kRedThreads, 0) == cudaSuccess &&
+        ok = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgs_all_kernel<4>, kRedThreads, 0) == cudaSuccess &&
              per_sm * sm_count() >= reduce_blocks();
     }
     if (!ok) return false;
     MgsAllArgs a{};
     for (int i = 0; i < m; ++i) a.v[i] = reinterpret_cast<const double2*>(v[i]);
-    mgs_all_kernel<<<reduce_blocks(), kRedThreads, 0, st>>>(reinterpret_cast<double2*>(w), a, m, len / 2, partials,
-                                                            ticket, flag, epoch, h_dev);
+    const int64_t len2 = len / 2, per = int64_t(reduce_blocks()) * kRedThreads;
+    auto go = [&](auto kern) {
+        kern<<<reduce_blocks(), kRedThreads, 0, st>>>(reinterpret_cast<double2*>(w), a, m, len2, partials, ticket, flag,
+                                                      epoch, h_dev);
+    };
+    if (len2 <= 2 * per) go(mgs_all_kernel<2>);
+    else if (len2 <= 4 * per) go(mgs_all_kernel<4>);
+    else go(mgs_all_kernel<0>);
     CK_LAUNCH();
     epoch += unsigned(m) + 1u;
     return true;
