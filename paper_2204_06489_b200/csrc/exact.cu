@@ -931,6 +931,39 @@ __global__ void middle_rhs(int nb, int64_t blk, const double2* __restrict__ b, c
     T[t] = v;
 }
 
+// twisted solve, middle line for few right-hand sides: X[k][r] = sum_j G[r][j] T[k][j],
+// one warp per row r (lanes split j, fixed-order butterfly), all k in registers
+template <int KMAX>
+__global__ void __launch_bounds__(256) middle_gemv(int nb, int nrhs, const double2* __restrict__ G, int gp,
+                                                   const double2* __restrict__ T, double2* __restrict__ X) {
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r >= nb) return;
+    double2 acc[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) acc[k] = make_double2(0.0, 0.0);
+    for (int j = lane; j < nb; j += 32) {
+        const double2 g = G[int64_t(r) * gp + j];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+            if (k < nrhs) {
+                const double2 t = T[int64_t(k) * nb + j];
+                acc[k].x = fma(g.x, t.x, acc[k].x);
+                acc[k].y = fma(g.x, t.y, acc[k].y);
+                acc[k].x = fma(-g.y, t.y, acc[k].x);
+                acc[k].y = fma(g.y, t.x, acc[k].y);
+            }
+    }
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+        for (int o = 16; o > 0; o >>= 1) {
+            acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, o);
+            acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, o);
+        }
+        if (lane == 0 && k < nrhs) X[int64_t(k) * nb + r] = acc[k];
+    }
+}
+
 struct WarpPlan {
     WSweepArgs a;
     int CS = 0, KG = 0, KR = 0;
@@ -1389,8 +1422,15 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
                         f.nb, blk, W + m * blk, f.coup.p + int64_t(m - 1) * f.nb, f.ybuf.p + (m - 1) * blk,
                         f.coup.p + int64_t(m) * f.nb, f.ybuf.p + (m + 1) * blk, fm.tbuf.p);
                     CK_LAUNCH();
-                    cgemm(c.stream, true, nrhs, f.nb, f.nb, 1.0, fm.tbuf.p, f.nb, f.G.p + int64_t(m) * f.nb * f.gp,
-                          f.gp, nullptr, 0, W + m * blk, f.nb);
+                    const double2* Gm = f.G.p + int64_t(m) * f.nb * f.gp;
+                    if (nrhs <= 8) {
+                        middle_gemv<8><<<(f.nb + 7) / 8, 256, 0, c.stream>>>(f.nb, nrhs, Gm, f.gp, fm.tbuf.p,
+                                                                             W + m * blk);
+                        CK_LAUNCH();
+                    } else {
+                        cgemm(c.stream, true, nrhs, f.nb, f.nb, 1.0, fm.tbuf.p, f.nb, Gm, f.gp, nullptr, 0, W + m * blk,
+                              f.nb);
+                    }
                     // (3) both halves backward from the middle line outwards
                     p.a.chain[0] = SweepChain{m - 1, m, -1, 2, W + m * blk};
                     p.a.chain[1] = SweepChain{m + 1, f.L - 1 - m, 1, 2, W + m * blk};
