@@ -1389,6 +1389,9 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
             if (!have && warp_plan(f.nb, f.L, f.gp, nrhs, plan, chains, steps)) {
                 if (!forced) cache.emplace_back(key, plan);
                 have = true;
+                if (std::getenv("FWI_EXACT_PLAN_LOG"))
+                    std::fprintf(stderr, "[fwi] exact plan nb=%d L=%d nrhs=%d twisted=%d: CS=%d KG=%d KR=%d est=%.0f\n",
+                                 f.nb, f.L, nrhs, int(f.twisted), plan.CS, plan.KG, plan.KR, plan.est);
             }
         }
         if (have) {
