@@ -129,8 +129,30 @@ struct Basis {
     DevBuf<double> stage[2], parts;
     int64_t chunk = 0;
     int nchunks = 0;
+    // device-to-host copies (new basis vectors, the best iterate) run on their own
+    // stream, overlapping the next iteration; events order every later use
+    cudaStream_t cs = nullptr;
+    std::vector<cudaEvent_t> ev_slot;  // copy into host[i] done
+    cudaEvent_t ev_ready = nullptr, ev_vlast = nullptr, ev_best = nullptr;
 
+    void init_copies() {
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        ev_slot.assign(host.size(), nullptr);
+        for (auto& e : ev_slot) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_vlast, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_best, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev_vlast, cs));
+        CK(cudaEventRecord(ev_best, cs));
+        for (auto& e : ev_slot) CK(cudaEventRecord(e, cs));
+    }
     ~Basis() {
+        if (cs) cudaStreamSynchronize(cs);
+        for (auto& e : ev_slot)
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : {ev_ready, ev_vlast, ev_best})
+            if (e) cudaEventDestroy(e);
+        if (cs) cudaStreamDestroy(cs);
         for (double* h : host)
             if (h) cudaFreeHost(h);
     }
@@ -145,6 +167,7 @@ struct Basis {
     }
     const double* stage_chunk(int slot, int i, int64_t off, int64_t cl) {
         if (const double* d = dptr(i)) return d + off;
+        if (cs && off == 0) CK(cudaStreamWaitEvent(st, ev_slot[i], 0));  // host[i] fully written
         CK(cudaMemcpyAsync(stage[slot].p, host[i] + off, size_t(cl) * sizeof(double), cudaMemcpyHostToDevice, st));
         return stage[slot].p;
     }
@@ -265,6 +288,7 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
         for (int i = 0; i < B.ndev; ++i) B.dev[i].alloc(len);
         CK(cudaMallocHost(&best_host, bytes));
         std::memset(best_host, 0, bytes);
+        B.init_copies();
     }
     struct HostFree {
         double* p;
@@ -272,15 +296,23 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
             if (p) cudaFreeHost(p);
         }
     } best_guard{best_host};
+    // the host copy of the best iterate reads x_cand on the copy stream; x_cand is not
+    // written again before that copy has finished (xc_guard)
+    auto xc_guard = [&] {
+        if (best_host) CK(cudaStreamWaitEvent(st, B.ev_best, 0));
+    };
     auto save_best = [&](const double* src) {
         if (best_host) {
-            CK(cudaMemcpyAsync(best_host, src, bytes, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
+            CK(cudaEventRecord(B.ev_ready, st));
+            CK(cudaStreamWaitEvent(B.cs, B.ev_ready, 0));
+            CK(cudaMemcpyAsync(best_host, src, bytes, cudaMemcpyDeviceToHost, B.cs));
+            CK(cudaEventRecord(B.ev_best, B.cs));
         } else {
             CK(cudaMemcpyAsync(best.p, src, bytes, cudaMemcpyDeviceToDevice, st));
         }
     };
     auto load_best = [&](double* dst) {
+        xc_guard();
         CK(cudaMemcpyAsync(dst, best_host ? best_host : best.p, bytes,
                            best_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
     };
@@ -290,7 +322,14 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
             std::swap(B.dev[i], src);
         } else {
             B.ensure_host(i);
-            CK(cudaMemcpyAsync(B.host[i], src.p, bytes, cudaMemcpyDeviceToHost, st));
+            CK(cudaEventRecord(B.ev_ready, st));
+            CK(cudaStreamWaitEvent(B.cs, B.ev_ready, 0));
+            CK(cudaMemcpyAsync(B.host[i], src.p, bytes, cudaMemcpyDeviceToHost, B.cs));
+            CK(cudaEventRecord(B.ev_slot[i], B.cs));
+            // src takes the previous newest vector's buffer, whose own host copy must be
+            // finished before it is overwritten
+            CK(cudaStreamWaitEvent(st, B.ev_vlast, 0));
+            CK(cudaEventRecord(B.ev_vlast, B.cs));
             std::swap(B.vlast, src);  // device copy of the newest vector; src reuses the old one
             B.vlast_index = i;
         }
@@ -315,6 +354,7 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
     while (iter < maxit && !log.converged && !stop_requested) {
         // r0 = M^{-1}(b - A x)
         ops.apply(x, tmp.p);
+        xc_guard();
         CK(cudaMemcpyAsync(xc.p, b, bytes, cudaMemcpyDeviceToDevice, st));
         dev_axpy(st, -1.0, tmp.p, xc.p, len);
         ops.precond(xc.p, w.p);
@@ -391,6 +431,7 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
                 y[i] = acc / hcols[i][i];
             }
             CK(cudaMemcpyAsync(ydev.p, y.data(), (j + 1) * sizeof(double), cudaMemcpyHostToDevice, st));
+            xc_guard();
             multi_axpy_any(B, xc.p, x, y, ydev.p, j + 1);
 
             ops.apply(xc.p, tmp.p);
@@ -430,6 +471,7 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
         }
     }
     CK(cudaStreamSynchronize(st));
+    if (B.cs) CK(cudaStreamSynchronize(B.cs));
     return log;
 }
 
