@@ -273,18 +273,25 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
         for (int l = tid; l < nlev; l += nt) ms[l] = lmeta[l];
     const int4* mt = meta_smem ? ms : lmeta;
     __syncthreads();
+    // The last warp stages level metadata (cp.async, kLvlBuf-1 levels ahead) while the
+    // other warps evaluate the current level: one barrier per level, and the staging
+    // of level l+3 overlaps the rows of level l.
+    const int pw0 = nt - 32;  // first thread of the staging warp
+    const bool stager = tid >= pw0;
+    const int ct = stager ? 0 : tid, cn = pw0;  // compute threads 0..pw0-1
     auto prefetch = [&](int l) {
+        if (!stager) return;
         if (l < nlev) {
             const int b = l % kLvlBuf;
             const int4 m = mt[l];
             const int r0 = m.x, r1 = m.y;
             const int e0 = m.z, e1 = m.w;
-            for (int t = tid; t < e1 - e0; t += nt) {
+            for (int t = tid - pw0; t < e1 - e0; t += 32) {
                 cp_async16(vb + b * ecap + t, val + e0 + t);
                 cp_async4(ib + b * ecap + t, idx + e0 + t);
             }
-            for (int t = tid; t < r1 - r0; t += nt) cp_async4(rib + b * rcap + t, lvl_rows + r0 + t);
-            for (int t = tid; t <= r1 - r0; t += nt) cp_async4(rpb + b * (rcap + 1) + t, rstart + r0 + t);
+            for (int t = tid - pw0; t < r1 - r0; t += 32) cp_async4(rib + b * rcap + t, lvl_rows + r0 + t);
+            for (int t = tid - pw0; t <= r1 - r0; t += 32) cp_async4(rpb + b * (rcap + 1) + t, rstart + r0 + t);
         }
         cp_commit();  // (possibly empty) group per level keeps the counting uniform
     };
@@ -293,15 +300,17 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
 #pragma unroll
     for (int l = 0; l < kLvlBuf - 1; ++l) prefetch(l);
     for (int l = 0; l < nlev; ++l) {
-        cp_wait<kLvlBuf - 2>();
-        __syncthreads();
+        if (stager) cp_wait<kLvlBuf - 2>();
+        __syncthreads();  // level l staged; level l-1's rows written
+        prefetch(l + kLvlBuf - 1);  // into level l-1's buffer, free now
+        if (stager) continue;
         const int b = l % kLvlBuf;
         const int nrow = mt[l].y - mt[l].x;
         const int* rp = rpb + b * (rcap + 1);
         const int e0 = rp[0];
         const double2* vl = vb + b * ecap;
         const int* il = ib + b * ecap;
-        for (int t = tid; t < nrow; t += nt) {
+        for (int t = ct; t < nrow; t += cn) {
             const int i = rib[b * rcap + t];
             const int p0 = rp[t] - e0, p1 = rp[t + 1] - e0;
             double2 s = xload(xs + i, !XS);
@@ -342,10 +351,9 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
             else
                 xs[i] = cdiv(s, make_double2(dg.x, -dg.y));
         }
-        __syncthreads();
-        prefetch(l + kLvlBuf - 1);
     }
     cp_wait<0>();
+    __syncthreads();
     if (XS)
         for (int t = tid; t < n; t += nt) xk[t] = xs[t];
 }
