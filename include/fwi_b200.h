@@ -274,6 +274,10 @@ int fwi_dev_memcpy_d2h(void* dst_host, const void* src_dev, int64_t bytes);
 /* Page-lock an existing host buffer (so uploads/downloads run at DMA speed). */
 int fwi_host_register(void* host, int64_t bytes);
 int fwi_host_unregister(void* host);
+/* Allocate / free page-locked host memory (cudaHostAlloc): the fastest source and
+ * destination for fwi_dev_kkt_apply_host and the vector uploads/downloads. */
+int fwi_host_alloc(void** out, int64_t bytes);
+int fwi_host_free(void* host);
 
 #ifdef __cplusplus
 }

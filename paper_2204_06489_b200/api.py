@@ -148,6 +148,8 @@ def lib() -> C.CDLL:
                 "fwi_dev_ctx_stream": [_vp, C.POINTER(_vp)],
                 "fwi_host_register": [_vp, C.c_int64],
                 "fwi_host_unregister": [_vp],
+                "fwi_host_alloc": [C.POINTER(_vp), C.c_int64],
+                "fwi_host_free": [_vp],
             }
             for name, args in sig.items():
                 f = getattr(L, name)
@@ -443,6 +445,30 @@ def host_register(a: np.ndarray) -> None:
 
 def host_unregister(a: np.ndarray) -> None:
     _check(lib().fwi_host_unregister(a.ctypes.data))
+
+
+class _PinnedOwner:
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        try:
+            lib().fwi_host_free(self.ptr)
+        except Exception:
+            pass
+
+
+def host_empty(n: int, dtype=np.float64) -> np.ndarray:
+    """A numpy array backed by page-locked memory from cudaHostAlloc (freed with the array)."""
+    dt = np.dtype(dtype)
+    p = _vp()
+    _check(lib().fwi_host_alloc(C.byref(p), max(int(n) * dt.itemsize, 1)))
+    buf = (C.c_char * (int(n) * dt.itemsize)).from_address(p.value)
+    a = np.frombuffer(buf, dtype=dt, count=int(n))
+    a.setflags(write=True)
+    owner = _PinnedOwner(p.value)
+    buf._owner = owner  # keep the allocation alive as long as the array
+    return a
 
 
 def simulate(problem: Problem, s: np.ndarray | None = None) -> np.ndarray:

@@ -489,4 +489,15 @@ int fwi_host_unregister(void* host) {
     return guard([&] { CK(cudaHostUnregister(host)); });
 }
 
+int fwi_host_alloc(void** out, int64_t bytes) {
+    return guard([&] {
+        need(out, "out");
+        CK(cudaHostAlloc(out, size_t(bytes), cudaHostAllocDefault));
+    });
+}
+
+int fwi_host_free(void* host) {
+    return guard([&] { CK(cudaFreeHost(host)); });
+}
+
 }  // extern "C"

@@ -70,7 +70,7 @@ struct Ctx {
     DevBuf<double2> work_a, work_b, work_c;  // K*n complex scratch (precond)
     DevBuf<double> work_ds;
     // pipelined host-buffer apply (kkt_apply_host)
-    static constexpr int kMaxChunks = 16;
+    static constexpr int kMaxChunks = 64;
     DevBuf<double> hx, hy, hpl;
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_in[kMaxChunks] = {}, ev_out[kMaxChunks] = {};

@@ -19,6 +19,8 @@
 // order — the same summation order as the reference's column scatter, so the
 // complex128 result is bit-identical to the reference.
 #include "arith.cuh"
+#include <cstdlib>
+
 #include "ctx.cuh"
 
 #include <algorithm>
@@ -163,7 +165,8 @@ void kkt_apply_host(Ctx& c, const double* in, double* out) {
             CK(cudaEventCreateWithFlags(&c.ev_out[i], cudaEventDisableTiming));
         }
     }
-    const int nch = std::min(K, Ctx::kMaxChunks);
+    static const int want = std::getenv("FWI_HOST_CHUNKS") ? std::atoi(std::getenv("FWI_HOST_CHUNKS")) : 16;
+    const int nch = std::max(1, std::min(K, std::min(want, Ctx::kMaxChunks)));
     double* x = c.hx.p;
     double* y = c.hy.p;
     const size_t cb = sizeof(double2);

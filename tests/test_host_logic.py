@@ -92,3 +92,11 @@ def test_replica_timing_is_max_over_ranks_gloo():
     ts = {r: t for r, t, _ in res}
     for _, _, tmax in res:
         assert tmax == pytest.approx(max(ts.values()))
+
+
+def test_host_alloc_symbols_declared():
+    """fwi_host_alloc/free are part of the C ABI (page-locked buffers for the host apply)."""
+    import re
+    hdr = open(os.path.join(ROOT, "include", "fwi_b200.h")).read()
+    assert re.search(r"int fwi_host_alloc\(void\*\* out, int64_t bytes\);", hdr)
+    assert re.search(r"int fwi_host_free\(void\* host\);", hdr)
