@@ -141,90 +141,115 @@ __global__ void __launch_bounds__(kGemmThreads) cgemm_kernel(int M, int N, int K
 }
 
 // Inverse of one b x b diagonal block (b <= 64) by Gauss-Jordan with partial
-// pivoting inside the block, in shared memory; one CTA of 256 threads. Per pivot
-// step: warp 0 finds the pivot and its reciprocal; 64 threads form the
-// multiplier column and 64 the scaled pivot row (reading the pre-swap rows, so
-// the swap needs no extra pass); then every thread updates 16 entries of one
-// column. Three barriers per step; the column permutation is applied on output.
+// pivoting inside the block; one CTA of 256 threads. Thread (cj, rg) keeps entries
+// (rg + 4i, cj), i < 16, of the working matrix in registers, so a pivot step moves
+// only O(b) values through shared memory (the pivot column, the candidates, the
+// pivot row and the row it swaps with; double-buffered, two barriers per step)
+// instead of the whole 64 KB block. The column permutation is applied on output.
 __global__ void __launch_bounds__(256) block_inverse_kernel(int b, const double2* __restrict__ D, int64_t ldd,
                                                             double2* __restrict__ out, int64_t ldo, int* status,
                                                             int status_base) {
     extern __shared__ double2 bsm[];
-    double2(*A)[65] = reinterpret_cast<double2(*)[65]>(bsm);  // [64][65]
-    __shared__ double2 prow[64], pcol[64];
+    double2(*A)[65] = reinterpret_cast<double2(*)[65]>(bsm);  // [64][65], only for the final permutation
+    __shared__ double2 colk[2][64], rowp[2][64], rowk[2][64];
+    __shared__ double cbest[2][4];
+    __shared__ int crow[2][4];
     __shared__ int piv[64], perm[64];
-    __shared__ int s_p;
-    __shared__ double2 s_inv;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int cj = tid & 63, rg = tid >> 6;  // column, row group (rows rg, rg+4, ...)
-    for (int r = rg; r < 64; r += 4) A[r][cj] = (r < b && cj < b) ? D[int64_t(r) * ldd + cj] : make_double2(0.0, 0.0);
-    __syncthreads();
+    const int tid = threadIdx.x;
+    const int cj = tid & 63, rg = tid >> 6;  // column; rows rg, rg+4, ...
+    double2 a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int r = rg + 4 * i;
+        a[i] = (r < b && cj < b) ? D[int64_t(r) * ldd + cj] : make_double2(0.0, 0.0);
+    }
     for (int k = 0; k < b; ++k) {
-        if (wid == 0) {  // pivot: max |A[r][k]|, r >= k (ties: lowest row)
+        const int buf = k & 1;
+        // (1) the four owners of column k publish it and their best candidate (rows >= k)
+        if (cj == k) {
             double best = -1.0;
             int bi = b;
-            for (int r = k + lane; r < b; r += 32) {
-                const double m2 = A[r][k].x * A[r][k].x + A[r][k].y * A[r][k].y;
-                if (m2 > best) { best = m2; bi = r; }
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_down_sync(0xffffffffu, best, o);
-                const int oi = __shfl_down_sync(0xffffffffu, bi, o);
-                if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-            }
-            if (lane == 0) {
-                if (!(best > 0.0)) {
-                    if (*status == 0) *status = status_base + k + 1;
-                    bi = k;
-                }
-                const double2 d = A[bi][k];
-                const double m2 = d.x * d.x + d.y * d.y;
-                const double r = m2 > 0.0 ? 1.0 / m2 : 0.0;
-                s_inv = make_double2(d.x * r, -d.y * r);
-                s_p = bi;
-                piv[k] = bi;
-            }
-        }
-        __syncthreads();
-        const int p = s_p;
-        const double2 pinv = s_inv;
-        if (tid < 64) {  // multiplier column of the swapped matrix (rows p and k exchanged)
-            const int r = tid;
-            pcol[r] = (r == k || r >= b) ? make_double2(0.0, 0.0) : (r == p ? A[k][k] : A[r][k]);
-        } else if (tid < 128) {  // scaled pivot row (old row p) and the swap of old row k into row p
-            const int j = tid - 64;
-            if (j < b) {
-                const double2 a = (j == k) ? make_double2(1.0, 0.0) : A[p][j];
-                prow[j] = make_double2(a.x * pinv.x - a.y * pinv.y, a.x * pinv.y + a.y * pinv.x);
-                if (p != k) A[p][j] = A[k][j];
-            }
-        }
-        __syncthreads();
-        if (cj < b) {
-            const double2 pr = prow[cj];
-            double2 v[16], f[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {  // all loads first, then the updates
-                const int r = rg + 4 * i;
-                v[i] = (cj == k) ? make_double2(0.0, 0.0) : A[r][cj];
-                f[i] = pcol[r];
-            }
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
                 const int r = rg + 4 * i;
-                if (r >= b) continue;
-                if (r == k) {
-                    v[i] = pr;
-                } else {
-                    v[i].x -= f[i].x * pr.x - f[i].y * pr.y;
-                    v[i].y -= f[i].x * pr.y + f[i].y * pr.x;
+                colk[buf][r] = a[i];
+                const double m2 = a[i].x * a[i].x + a[i].y * a[i].y;
+                if (r >= k && r < b && m2 > best) {  // rows ascend: ties keep the lowest
+                    best = m2;
+                    bi = r;
                 }
-                A[r][cj] = v[i];
             }
+            cbest[buf][rg] = best;
+            crow[buf][rg] = bi;
         }
         __syncthreads();
+        // (2) every thread picks the same pivot (max |.|^2, ties: lowest row)
+        double best = cbest[buf][0];
+        int p = crow[buf][0];
+#pragma unroll
+        for (int q = 1; q < 4; ++q) {
+            const double v = cbest[buf][q];
+            const int r = crow[buf][q];
+            if (v > best || (v == best && r < p)) {
+                best = v;
+                p = r;
+            }
+        }
+        if (!(best > 0.0)) p = k;
+        if (tid == 0) {
+            piv[k] = p;
+            if (!(best > 0.0) && *status == 0) *status = status_base + k + 1;
+        }
+        // owners of rows p and k publish them (pre-swap); register index by unrolled select
+        const int ip = p >> 2, ik = k >> 2;
+        if ((p & 3) == rg) {
+            double2 v = a[0];
+#pragma unroll
+            for (int i = 1; i < 16; ++i)
+                if (i == ip) v = a[i];
+            rowp[buf][cj] = v;
+        }
+        if ((k & 3) == rg) {
+            double2 v = a[0];
+#pragma unroll
+            for (int i = 1; i < 16; ++i)
+                if (i == ik) v = a[i];
+            rowk[buf][cj] = v;
+        }
+        __syncthreads();
+        // (3) swap rows k <-> p, scale the pivot row, eliminate column k everywhere
+        const double2 d = colk[buf][p];
+        const double m2 = d.x * d.x + d.y * d.y;
+        const double rr = m2 > 0.0 ? 1.0 / m2 : 0.0;
+        const double2 pinv = make_double2(d.x * rr, -d.y * rr);
+        const double2 ap = (cj == k) ? make_double2(1.0, 0.0) : rowp[buf][cj];
+        const double2 pr = make_double2(ap.x * pinv.x - ap.y * pinv.y, ap.x * pinv.y + ap.y * pinv.x);
+        const bool colk_thread = (cj == k);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {  // common path: a -= f * pr (column k starts from 0)
+            const double2 f = colk[buf][rg + 4 * i];
+            double2 v = colk_thread ? make_double2(0.0, 0.0) : a[i];
+            v.x -= f.x * pr.x - f.y * pr.y;
+            v.y -= f.x * pr.y + f.y * pr.x;
+            a[i] = v;
+        }
+        if ((p & 3) == rg && p != k) {  // row p now holds the old row k
+            const double2 f = colk[buf][k];
+            double2 v = colk_thread ? make_double2(0.0, 0.0) : rowk[buf][cj];
+            v.x -= f.x * pr.x - f.y * pr.y;
+            v.y -= f.x * pr.y + f.y * pr.x;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (i == ip) a[i] = v;
+        }
+        if ((k & 3) == rg) {  // the pivot row
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (i == ik) a[i] = pr;
+        }
     }
-    if (tid == 0) {  // undoing the column swaps in reverse order = one permutation
+    // undoing the column swaps in reverse order = one permutation, applied through shared memory
+    if (tid == 0) {
         for (int j = 0; j < b; ++j) perm[j] = j;
         for (int k = b - 1; k >= 0; --k) {
             const int t = perm[k];
@@ -232,6 +257,8 @@ __global__ void __launch_bounds__(256) block_inverse_kernel(int b, const double2
             perm[piv[k]] = t;
         }
     }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) A[rg + 4 * i][cj] = a[i];
     __syncthreads();
     if (cj < b)
         for (int r = rg; r < b; r += 4) out[int64_t(r) * ldo + cj] = A[r][perm[cj]];
