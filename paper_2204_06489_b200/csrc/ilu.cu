@@ -314,11 +314,46 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
             const int i = rib[b * rcap + t];
             const int p0 = rp[t] - e0, p1 = rp[t + 1] - e0;
             double2 s = xload(xs + i, !XS);
+            double2 dg = make_double2(0.0, 0.0);
+            if constexpr (XS) {
+            // Entries in the reference's order. A batch of 8 loads its indices, values and x
+            // operands first, forms the 8 products independently, then runs the dependent
+            // subtraction chain with selects (no per-entry branches, so the loads overlap).
+            constexpr int BT = 8;
+            const int q0 = (KIND == kUbwd) ? p0 + 1 : p0;
+            for (int pb = q0; pb < p1; pb += BT) {
+                double2 xv[BT], av[BT];
+                int kv[BT];
+#pragma unroll
+                for (int u = 0; u < BT; ++u) {
+                    const int pp = min(pb + u, p1 - 1);  // clamped: in range, result discarded
+                    kv[u] = il[pp];
+                    av[u] = vl[pp];
+                }
+#pragma unroll
+                for (int u = 0; u < BT; ++u) xv[u] = xload(xs + kv[u], !XS);
+                double2 tv[BT];
+#pragma unroll
+                for (int u = 0; u < BT; ++u)
+                    tv[u] = (KIND == kLfwd || KIND == kUbwd) ? cmul(av[u], xv[u]) : cmulc(av[u], xv[u]);
+#pragma unroll
+                for (int u = 0; u < BT; ++u) {
+                    const bool valid = pb + u < p1;
+                    bool use = valid;
+                    if (KIND == kUtfwd) {
+                        const bool diag = valid && kv[u] == i;
+                        dg = diag ? av[u] : dg;
+                        use = valid && !diag;
+                    }
+                    const double2 sn = csub(s, tv[u]);
+                    s = use ? sn : s;
+                }
+            }
+            } else {
             // entries in the reference's order; the x operands of a batch of 8 are loaded
             // before the dependent subtraction chain (one L2 round trip per batch, not per entry)
             constexpr int BT = 8;
             const int q0 = (KIND == kUbwd) ? p0 + 1 : p0;
-            double2 dg = make_double2(0.0, 0.0);
             for (int pb = q0; pb < p1; pb += BT) {
                 double2 xv[BT];
 #pragma unroll
@@ -343,6 +378,7 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
                         }
                     }
                 }
+            }
             }
             if (KIND == kLfwd || KIND == kLtbwd)
                 xs[i] = s;
