@@ -39,17 +39,21 @@ def record(label, tag, ds, log, setup=0.0):
     runs.append((label, log, setup))
 
 
-ds, log = fw.rsgn_cg_step(st, ecg_stop_tol if ecg_stop_tol > 0 else inner_tol, max_inner)
+# each solver runs twice; the second (warm: workspaces, plans, clocks) is recorded
+for _ in range(2):
+    ds, log = fw.rsgn_cg_step(st, ecg_stop_tol if ecg_stop_tol > 0 else inner_tol, max_inner)
 record("CG", "cg", ds, log)
-ds, log = fw.fsgn_gmres_step(st, fw.FsgnOptions(mode=fw.PrecondMode.exact, restart=restart, tol=inner_tol,
-                                                maxit=max_inner, ecg_stride=1, ecg_stop_tol=ecg_stop_tol))
+for _ in range(2):
+    ds, log = fw.fsgn_gmres_step(st, fw.FsgnOptions(mode=fw.PrecondMode.exact, restart=restart, tol=inner_tol,
+                                                    maxit=max_inner, ecg_stride=1, ecg_stop_tol=ecg_stop_tol))
 record("GMRes-full", "gmres_full", ds, log)
 for lev in levels:
     t0 = time.perf_counter()
     st.factor_ilu(lev)
     setup = time.perf_counter() - t0
-    ds, log = fw.fsgn_gmres_step(st, fw.FsgnOptions(mode=fw.PrecondMode.ilu, restart=restart, tol=inner_tol,
-                                                    maxit=max_inner, ecg_stride=1, ecg_stop_tol=ecg_stop_tol))
+    for _ in range(2):
+        ds, log = fw.fsgn_gmres_step(st, fw.FsgnOptions(mode=fw.PrecondMode.ilu, restart=restart, tol=inner_tol,
+                                                        maxit=max_inner, ecg_stride=1, ecg_stop_tol=ecg_stop_tol))
     record(f"GMRes-approx(p={lev})", f"gmres_ilu_p{lev}", ds, log, setup)
 
 lines = [f"{'solver':28s} {'iterations':>10s} {'time/iteration [s]':>19s} {'ILU initialization [s]':>23s} "
