@@ -56,6 +56,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -130,6 +133,15 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 
 constexpr int kRing = 8;
 
+// barrier over the consumer threads only (the producer warp never joins)
+template <int WS>
+__device__ __forceinline__ void consumer_sync() {
+    if (WS == 1)
+        asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+    else
+        __syncthreads();
+}
+
 // Units = (tile, chunk of KC sources), claimed dynamically in chunk-major
 // order by persistent CTAs. A unit's ds contribution is folded into the
 // tile's running partial sum (kept in out.ds) strictly in source order: the
@@ -173,8 +185,17 @@ __device__ __forceinline__ void node_step(const typename A::T* dr, const typenam
 // unit waits for the tile's previous chunk, so the complex128 result stays
 // bit-identical to the reference's sequential sum. S (stages) divides KC, so
 // stage indices and mbarrier parities are compile-time within a unit.
-template <class A, int KC, int S>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+//
+// WS = 1 (warp-specialised): a 17th warp is the producer. It waits on
+// per-stage "empty" mbarriers (one arrive per consumer warp) instead of the
+// block-wide barrier after every step, and hands the claimed unit id over
+// through the stage's "full" mbarrier (release/acquire). The 17th warp caps
+// the register budget at 96 per thread (5 warps on one SM sub-partition), so
+// it suits the complex64 kernel. WS = 2: same empty barriers, no extra warp —
+// thread 0 waits for the stage to drain and refills it, the other warps run
+// ahead within the ring. WS = 0: a block barrier after every step.
+template <class A, int KC, int S, int WS>
+__global__ void __launch_bounds__(WS == 1 ? kThreads + 32 : kThreads, kCtasPerSm)
     kkt_tma_kernel(const __grid_constant__ CUtensorMap tdu, const __grid_constant__ CUtensorMap tla,
                    const __grid_constant__ CUtensorMap tu, const TmaArgs<A> P) {
     static_assert(KC % S == 0, "stages must divide the chunk");
@@ -182,7 +203,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     using R = typename A::R;
     extern __shared__ __align__(1024) unsigned char sm[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + size_t(S) * P.stage_bytes);
-    int* ring = reinterpret_cast<int*>(bar + kMaxStages);
+    uint64_t* empty = bar + kMaxStages;
+    int* ring = reinterpret_cast<int*>(bar + 2 * kMaxStages);
     // this chunk's Re(w^2 conj(u_k) lambda_k) terms, [KC][2][kThreads]
     R* terms = reinterpret_cast<R*>(sm + size_t(S) * P.stage_bytes + 128);
     const int nx = P.nx, nz = P.nz, Tn = P.T_;
@@ -193,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
     // producer (thread 0): claims units lazily, issues one step = 3 TMA boxes
     int nclaimed = 0;
-    auto issue = [&](int j) {
+    auto issue = [&](int j) -> bool {
         const int qq = j / KC;
         while (nclaimed <= qq) {
             const unsigned u = atomicAdd(P.sched, 1u);
@@ -201,7 +223,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             ++nclaimed;
         }
         const int u = ring[qq % kRing];
-        if (u < 0) return;
+        if (u < 0) {
+            if (WS == 1) mbar_arrive(&bar[j % S]);  // wakes the consumers, who read the end marker
+            return false;
+        }
         const int t = u % Tn, c = u / Tn;
         const int k = c * KC + j % KC;
         const int4 tl = P.tiles[t];
@@ -213,16 +238,30 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         tma_load_4d(st, &tdu, 0, tl.x / P.gr - 1, tl.z - 1, k, &bar[s]);
         tma_load_4d(st + P.dub, &tla, 0, tl.x / P.gr - 1, tl.z - 1, k, &bar[s]);
         if (!P.nou) tma_load_4d(st + 2 * P.dub, &tu, 0, tl.x / P.gr, tl.z, k, &bar[s]);
+        return true;
     };
 
     if (tid == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&bar[s], 1);
+            if (WS) mbar_init(&empty[s], kThreads / 32);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int j = 0; j < S; ++j) issue(j);
+        if (WS != 1)
+            for (int j = 0; j < S; ++j) issue(j);
     }
     __syncthreads();
+    if (WS == 1 && tid >= kThreads) {
+        if (tid == kThreads)
+            for (int j = 0;; ++j) {
+                if (j >= S) mbar_wait(&empty[j % S], ((j / S) - 1) & 1);
+                if (!issue(j)) break;
+            }
+        return;
+    }
 
     for (int q = 0;; ++q) {
+        if (WS == 1) mbar_wait(&bar[0], (q * (KC / S)) & 1);  // the unit's first stage carries its id
         const int u = ring[q % kRing];
         if (u < 0) break;
         const int t = u % Tn, c = u / Tn;
@@ -311,13 +350,22 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 }
                 st_stream(P.odu + o, tv);
             }
-            __syncthreads();  // every thread is done with stage s
-            if (tid == 0) issue(q * KC + kk + S);
+            if (WS) {
+                __syncwarp();
+                if ((tid & 31) == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
+                if (WS == 2 && tid == 0) {
+                    mbar_wait(&empty[s], (par0 + kk / S) & 1);
+                    issue(q * KC + kk + S);
+                }
+            } else {
+                __syncthreads();  // every thread is done with stage s
+                if (tid == 0) issue(q * KC + kk + S);
+            }
         }
         // fold this chunk into the tile's running ds sum, in source order
         if (tid == 0 && c > 0 && !P.nofold)
             while (ld_acquire(P.flags + t) != P.base + unsigned(c)) __nanosleep(64);
-        __syncthreads();
+        consumer_sync<WS>();
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             if (!act[r]) continue;
@@ -326,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             for (int kk = 0; kk < KC; ++kk) pl = A::radd(pl, terms[(kk * 2 + r) * kThreads + tid]);
             P.ods[cnode[r]] = (c == P.C - 1) ? A::rsub(A::rmulr(P.eps, dsv[r]), pl) : pl;
         }
-        __syncthreads();
+        consumer_sync<WS>();
         if (tid == 0) {
             __threadfence();
             st_release(P.flags + t, P.base + unsigned(c) + 1u);
@@ -363,6 +411,7 @@ uint32_t align128(size_t b) { return uint32_t((b + 127) / 128 * 128); }
 struct KktPlan {
     bool ok = false;
     int G = 0, T = 0, C = 0, KC = 0, RP = 0, UP = 0, stages = 0, gr = 2;
+    int ws = 0;  // stage hand-off (kernel WS parameter; FWI_KKT_WS)
     uint32_t dub = 0, ub = 0, stage_bytes = 0, tx_bytes = 0;
     unsigned epoch = 0;
     size_t smem = 0;
@@ -403,11 +452,11 @@ bool encode(CUtensorMap* tm, bool f32, const void* base, int nx, int nz, int K, 
     return r == CUDA_SUCCESS;
 }
 
-template <class A, int KC, int S>
+template <class A, int KC, int S, int WS>
 void set_smem(size_t smem) {
     static size_t smem_set = 0;  // per-kernel, process-wide attribute: only ever raise it
     if (smem > smem_set) {
-        CK(cudaFuncSetAttribute(kkt_tma_kernel<A, KC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(kkt_tma_kernel<A, KC, S, WS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(smem)));
         smem_set = smem;
     }
@@ -480,9 +529,12 @@ KktPlan* build_plan(Ctx& c, bool f32) {
     while (st > 1 && (size_t(st) * p->stage_bytes > budget || kc % st != 0)) st /= 2;
     if (kc == 1) st = 1;
     p->stages = st;
+    p->ws = f32 ? 1 : 0;
+    if (const char* e = std::getenv("FWI_KKT_WS")) p->ws = std::atoi(e);
     if (size_t(st) * p->stage_bytes > budget) return p.release();
     p->smem = size_t(p->stages) * p->stage_bytes + tail;
-#define FWI_SET(KCc, Sc) set_smem<A, KCc, Sc>(p->smem)
+#define FWI_SET(KCc, Sc) \
+    set_smem<A, KCc, Sc, 0>(p->smem), set_smem<A, KCc, Sc, 1>(p->smem), set_smem<A, KCc, Sc, 2>(p->smem)
     FWI_KKT_DISPATCH(kc, st, FWI_SET)
 #undef FWI_SET
     const void* ubase = f32 ? static_cast<const void*>(c.u32.p) : static_cast<const void*>(c.u.p);
@@ -540,8 +592,10 @@ bool launch(Ctx& c, KktPlan* p, const typename A::T* du, const typename A::R* ds
     a.ub = p->ub;
     a.stage_bytes = p->stage_bytes;
     a.tx_bytes = p->tx_bytes;
-#define FWI_LAUNCH(KCc, Sc) \
-    kkt_tma_kernel<A, KCc, Sc><<<p->G, kThreads, p->smem, c.stream>>>(tdu, tla, p->tm_u, a)
+#define FWI_LAUNCH(KCc, Sc)                                                                            \
+    (p->ws == 1   ? kkt_tma_kernel<A, KCc, Sc, 1><<<p->G, kThreads + 32, p->smem, c.stream>>>(tdu, tla, p->tm_u, a) \
+     : p->ws == 2 ? kkt_tma_kernel<A, KCc, Sc, 2><<<p->G, kThreads, p->smem, c.stream>>>(tdu, tla, p->tm_u, a)      \
+                  : kkt_tma_kernel<A, KCc, Sc, 0><<<p->G, kThreads, p->smem, c.stream>>>(tdu, tla, p->tm_u, a))
     FWI_KKT_DISPATCH(p->KC, p->stages, FWI_LAUNCH)
 #undef FWI_LAUNCH
     CK_LAUNCH();
