@@ -283,6 +283,7 @@ def run_ours(args):
                        "parallelism": f"replicas x{ws}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,
+                         "frac_of_datasheet_8000gbs": achieved / 8000.0,
                          "traffic": tr.get("dram_bytes_per_launch") if tr else None,
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "kernel": "kkt_tma_kernel<F64, 8, 2> (persistent TMA K1, csrc/kkt_tma.cu)"},

@@ -492,12 +492,15 @@ int fwi_host_unregister(void* host) {
 int fwi_host_alloc(void** out, int64_t bytes) {
     return guard([&] {
         need(out, "out");
-        CK(cudaHostAlloc(out, size_t(bytes), cudaHostAllocDefault));
+        require(bytes >= 0, "fwi_host_alloc: negative size");
+        *out = pinned_alloc(size_t(bytes));
     });
 }
 
 int fwi_host_free(void* host) {
-    return guard([&] { CK(cudaFreeHost(host)); });
+    return guard([&] {
+        if (!pinned_free(host)) CK(cudaFreeHost(host));
+    });
 }
 
 }  // extern "C"

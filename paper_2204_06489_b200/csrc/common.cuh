@@ -156,5 +156,9 @@ inline int grid_blocks(int64_t work, int threads, int max_blocks) {
 }
 
 int sm_count();
+// page-locked host memory (host_mem.cu): huge-page mapping, parallel first touch,
+// cudaHostRegister; zero-filled. pinned_free returns false for foreign pointers.
+void* pinned_alloc(size_t bytes);
+bool pinned_free(void* p);
 
 }  // namespace fwi_b200

@@ -13,9 +13,11 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <cmath>
 #include <functional>
+#include <future>
 #include <optional>
 
 #include "ctx.cuh"
@@ -126,6 +128,11 @@ struct Basis {
     int ndev = 0;
     DevBuf<double> vlast;             // device copy of the newest host-resident vector
     int vlast_index = -1;
+    // a free full-length device buffer during MGS + x_cand (host mode: the x_cand buffer):
+    // holds the last host vector the MGS sweep streamed in, so the next step and x_cand
+    // do not stream it again
+    double* cache = nullptr;
+    int cache_index = -1;
     DevBuf<double> stage[2], parts;
     int64_t chunk = 0;
     int nchunks = 0;
@@ -133,7 +140,7 @@ struct Basis {
     // stream, overlapping the next iteration; events order every later use
     cudaStream_t cs = nullptr;
     std::vector<cudaEvent_t> ev_slot;  // copy into host[i] done
-    cudaEvent_t ev_ready = nullptr, ev_vlast = nullptr, ev_best = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_vlast = nullptr;
 
     void init_copies() {
         CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -141,29 +148,31 @@ struct Basis {
         for (auto& e : ev_slot) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_vlast, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ev_best, cudaEventDisableTiming));
         CK(cudaEventRecord(ev_vlast, cs));
-        CK(cudaEventRecord(ev_best, cs));
         for (auto& e : ev_slot) CK(cudaEventRecord(e, cs));
     }
+    std::future<void> prealloc;  // host slots mapped in the background (host mode)
     ~Basis() {
+        if (prealloc.valid()) prealloc.wait();
         if (cs) cudaStreamSynchronize(cs);
         for (auto& e : ev_slot)
             if (e) cudaEventDestroy(e);
-        for (cudaEvent_t e : {ev_ready, ev_vlast, ev_best})
+        for (cudaEvent_t e : {ev_ready, ev_vlast})
             if (e) cudaEventDestroy(e);
         if (cs) cudaStreamDestroy(cs);
         for (double* h : host)
-            if (h) cudaFreeHost(h);
+            if (h) pinned_free(h);
     }
     bool on_host(int i) const { return i >= ndev; }
     void ensure_host(int i) {
-        if (!host[i]) CK(cudaMallocHost(&host[i], size_t(len) * sizeof(double)));
+        if (prealloc.valid()) prealloc.get();  // rethrows an allocation failure
+        if (!host[i]) host[i] = static_cast<double*>(pinned_alloc(size_t(len) * sizeof(double)));
     }
     // device pointer of v_i if it is device-resident (or the cached newest vector), else null
     const double* dptr(int i) const {
         if (!on_host(i)) return dev[i].p;
-        return i == vlast_index ? vlast.p : nullptr;
+        if (i == vlast_index) return vlast.p;
+        return cache && i == cache_index ? cache : nullptr;
     }
     const double* stage_chunk(int slot, int i, int64_t off, int64_t cl) {
         if (const double* d = dptr(i)) return d + off;
@@ -176,18 +185,25 @@ struct Basis {
 // w -= h_{i-1} v_{i-1}; h_i = <v_i, w>  (vi < 0: <w, w>)
 void mgs_step_any(Scratch& sc, Basis& B, double* w, int iprev, const double* hprev, int inext, double* hout) {
     const bool dev_prev = iprev < 0 || B.dptr(iprev), dev_next = inext < 0 || B.dptr(inext);
-    if (dev_prev && dev_next) {
+    // host mode (nchunks > 1) always reduces chunk by chunk, so h does not depend on which
+    // basis vectors happen to be device-resident
+    if (dev_prev && dev_next && B.nchunks <= 1) {
         dev_mgs_step(B.st, w, iprev >= 0 ? B.dptr(iprev) : nullptr, hprev, inext >= 0 ? B.dptr(inext) : nullptr,
                      hout, sc.partials.p, sc.ticket.p, B.len);
         return;
     }
     const int rb = reduce_blocks();
+    const bool keep = B.cache && !dev_next;  // v_inext streams in: keep it for the next step
     for (int c = 0; c < B.nchunks; ++c) {
         const int64_t off = c * B.chunk, cl = std::min(B.chunk, B.len - off);
         const double* pv = iprev >= 0 ? B.stage_chunk(0, iprev, off, cl) : nullptr;
         const double* nv = inext >= 0 ? B.stage_chunk(1, inext, off, cl) : nullptr;
         dev_mgs_step_parts(B.st, w + off, pv, hprev, nv, B.parts.p + int64_t(c) * rb, cl);
+        // chunk c of the cached v_iprev has been consumed: replace it by v_inext's
+        if (keep)
+            CK(cudaMemcpyAsync(B.cache + off, nv, size_t(cl) * sizeof(double), cudaMemcpyDeviceToDevice, B.st));
     }
+    if (keep) B.cache_index = inext;
     dev_sum_ordered(B.st, B.parts.p, B.nchunks * rb, hout);
 }
 
@@ -196,13 +212,33 @@ void mgs_step_any(Scratch& sc, Basis& B, double* w, int iprev, const double* hpr
 void multi_axpy_any(Basis& B, double* out, const double* x, const std::vector<double>& y, const double* ydev,
                     int m) {
     bool all_dev = true;
-    for (int i = 0; i < m; ++i) all_dev = all_dev && B.dptr(i);
-    if (all_dev) {
+    int staged = 0;
+    for (int i = 0; i < m; ++i) {
+        all_dev = all_dev && B.dptr(i);
+        staged += B.dptr(i) ? 0 : 1;
+    }
+    if (all_dev && !(B.cache && out == B.cache)) {
         std::vector<const double*> vp(m);
         for (int i = 0; i < m; ++i) vp[i] = B.dptr(i);
         dev_multi_axpy(B.st, out, x, vp.data(), ydev, m, B.len);
+        B.cache_index = -1;
         return;
     }
+    if (staged <= 2) {
+        // chunk-major: every element still sums x + y_0 v_0 + y_1 v_1 + ... in index order;
+        // chunk c of a cached vector is read before out's chunk c (possibly the cache
+        // buffer itself) is written
+        std::vector<const double*> vp(m);
+        for (int c = 0; c < B.nchunks; ++c) {
+            const int64_t off = c * B.chunk, cl = std::min(B.chunk, B.len - off);
+            int s = 0;
+            for (int i = 0; i < m; ++i) vp[i] = B.dptr(i) ? B.dptr(i) + off : B.stage_chunk(s++, i, off, cl);
+            dev_multi_axpy(B.st, out + off, x + off, vp.data(), ydev, m, cl);
+        }
+        B.cache_index = -1;
+        return;
+    }
+    B.cache_index = -1;  // out may be the cache buffer: stream every host vector
     CK(cudaMemcpyAsync(out, x, size_t(B.len) * sizeof(double), cudaMemcpyDeviceToDevice, B.st));
     for (int i = 0; i < m; ++i) {
         if (const double* d = B.dptr(i)) {
@@ -265,7 +301,9 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
         CK(cudaMemsetAsync(d.p, 0, bytes, st));
         gb.bufs.push_back(&d);
     };
-    grab(tmp);
+    // host mode keeps three vector buffers (w, xc and the newest basis vector's device
+    // copy) and rotates their roles; the device mode also has tmp
+    if (!host_mode) grab(tmp);
     grab(w);
     grab(xc);
     if (!host_mode) {
@@ -286,35 +324,73 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
         const int fit = free_b > margin ? int((free_b - margin) / bytes) : 0;
         B.ndev = force_host ? std::min(1, std::min(fit, nbasis)) : std::min(fit, nbasis);
         for (int i = 0; i < B.ndev; ++i) B.dev[i].alloc(len);
-        CK(cudaMallocHost(&best_host, bytes));
-        std::memset(best_host, 0, bytes);
         B.init_copies();
+        // mapping 17 GB of page-locked memory takes ~0.65 s: do it while the device works
+        B.prealloc = std::async(std::launch::async, [&B, nbasis, bytes] {
+            for (int i = B.ndev; i < nbasis; ++i) B.host[i] = static_cast<double*>(pinned_alloc(bytes));
+        });
     }
+    // FWI_GMRES_TRACE: per-iteration phase times (events on the solver stream) to stderr
+    struct Trace {
+        bool on = std::getenv("FWI_GMRES_TRACE") != nullptr;
+        cudaEvent_t ev[8] = {};
+        int n = 0;
+        Trace() {
+            if (on)
+                for (auto& e : ev) CK(cudaEventCreate(&e));
+        }
+        ~Trace() {
+            for (auto& e : ev)
+                if (e) cudaEventDestroy(e);
+        }
+        void mark(cudaStream_t s) {
+            if (on && n < 8) CK(cudaEventRecord(ev[n++], s));
+        }
+        void report(int iter, int j) {
+            if (!on) return;
+            CK(cudaEventSynchronize(ev[n - 1]));
+            std::fprintf(stderr, "gmres-trace it %d j %d ms:", iter, j);
+            for (int i = 1; i < n; ++i) {
+                float ms = 0;
+                CK(cudaEventElapsedTime(&ms, ev[i - 1], ev[i]));
+                std::fprintf(stderr, " %.1f", ms);
+            }
+            std::fprintf(stderr, "\n");
+            n = 0;
+        }
+    } trace;
+    if (trace.on)
+        std::fprintf(stderr, "gmres-trace host_mode %d ndev %d nbasis %d free %.1f GB vec %.1f GB\n", int(host_mode),
+                     B.ndev, nbasis, double(free_b) / 1e9, double(bytes) / 1e9);
+    // The best iterate (returned on stagnation). Device mode: a device copy. Host mode:
+    // kept recoverable without a 17 GB copy per improvement. best_kind 1: the cycle-start
+    // x (the x buffer itself); 2: iterate best_j of the current cycle, x + V y_best,
+    // recomputed from the basis when needed (same arithmetic, so bit-identical); 3: a
+    // page-locked host copy, made only when x moves on while the best lies elsewhere.
+    int best_kind = 1, best_j = -1, last_j = -1;
+    std::vector<double> best_y;
     struct HostFree {
-        double* p;
+        double*& p;
         ~HostFree() {
-            if (p) cudaFreeHost(p);
+            if (p) pinned_free(p);
         }
     } best_guard{best_host};
-    // the host copy of the best iterate reads x_cand on the copy stream; x_cand is not
-    // written again before that copy has finished (xc_guard)
-    auto xc_guard = [&] {
-        if (best_host) CK(cudaStreamWaitEvent(st, B.ev_best, 0));
-    };
     auto save_best = [&](const double* src) {
-        if (best_host) {
-            CK(cudaEventRecord(B.ev_ready, st));
-            CK(cudaStreamWaitEvent(B.cs, B.ev_ready, 0));
-            CK(cudaMemcpyAsync(best_host, src, bytes, cudaMemcpyDeviceToHost, B.cs));
-            CK(cudaEventRecord(B.ev_best, B.cs));
-        } else {
-            CK(cudaMemcpyAsync(best.p, src, bytes, cudaMemcpyDeviceToDevice, st));
-        }
+        CK(cudaMemcpyAsync(best.p, src, bytes, cudaMemcpyDeviceToDevice, st));
     };
     auto load_best = [&](double* dst) {
-        xc_guard();
-        CK(cudaMemcpyAsync(dst, best_host ? best_host : best.p, bytes,
-                           best_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(dst, best.p, bytes, cudaMemcpyDeviceToDevice, st));
+    };
+    auto recompute_best = [&](double* dst) {
+        B.cache_index = -1;
+        CK(cudaMemcpyAsync(WS.ydev.p, best_y.data(), best_y.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+        multi_axpy_any(B, dst, x, best_y, WS.ydev.p, best_j + 1);
+    };
+    auto materialise = [&](const double* src) {
+        if (!best_host) best_host = static_cast<double*>(pinned_alloc(bytes));
+        CK(cudaMemcpyAsync(best_host, src, bytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        best_kind = 3;
     };
     // store the normalised vector in `src` (a device buffer we own) as basis vector i
     auto put_basis = [&](int i, DevBuf<double>& src) {
@@ -341,8 +417,7 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
         throw FwiError(FWI_ERR_INVALID_ARGUMENT, "gmres: preconditioner annihilates the right-hand side");
     log.entries.push_back({0, 1.0, {}, 1.0, elapsed()});
 
-    if (best_host) std::memset(best_host, 0, bytes);
-    else CK(cudaMemsetAsync(best.p, 0, bytes, st));
+    if (!host_mode) CK(cudaMemsetAsync(best.p, 0, bytes, st));
     double best_res = 1.0, true_res = 1.0;
     int iter = 0;
     bool stop_requested = false;
@@ -353,10 +428,9 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
 
     while (iter < maxit && !log.converged && !stop_requested) {
         // r0 = M^{-1}(b - A x)
-        ops.apply(x, tmp.p);
-        xc_guard();
+        ops.apply(x, w.p);
         CK(cudaMemcpyAsync(xc.p, b, bytes, cudaMemcpyDeviceToDevice, st));
-        dev_axpy(st, -1.0, tmp.p, xc.p, len);
+        dev_axpy(st, -1.0, w.p, xc.p, len);
         ops.precond(xc.p, w.p);
         const double beta = dnorm(sc, st, w.p, len);
         const double cycle_start_res = true_res;
@@ -371,8 +445,21 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
 
         for (int j = 0; j < restart && iter < maxit; ++j) {
             ++iter;
-            ops.apply(B.dptr(j), tmp.p);
-            ops.precond(tmp.p, w.p);
+            trace.mark(st);
+            ops.apply(B.dptr(j), w.p);
+            trace.mark(st);
+            // host mode: x_cand of the previous iteration is dead (the best iterate is
+            // recoverable from the basis)
+            DevBuf<double>& spare = host_mode ? xc : tmp;
+            ops.precond(w.p, spare.p);
+            std::swap(w, spare);
+            if (host_mode) {  // xc is free until x_cand: it caches streamed basis vectors
+                B.cache = xc.p;
+                B.cache_index = -1;
+            }
+            // the host slot of the next basis vector is mapped while the device works
+            if (j + 1 < nbasis && B.on_host(j + 1)) B.ensure_host(j + 1);
+            trace.mark(st);
             // MGS: h_i = <v_i, w>; w -= h_i v_i  (fused pairwise)
             bool fused = false;
             if (!host_mode && !std::getenv("FWI_GMRES_MGS_STEPS")) {
@@ -386,6 +473,7 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
                     mgs_step_any(sc, B, w.p, i - 1, hdev.p + (i - 1), i, hdev.p + i);
                 mgs_step_any(sc, B, w.p, j, hdev.p + j, -1, hdev.p + j + 1);
             }
+            trace.mark(st);
             CK(cudaMemcpyAsync(hh.data(), hdev.p, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             std::vector<double> h(hh.begin(), hh.begin() + j + 2);
@@ -431,19 +519,36 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
                 y[i] = acc / hcols[i][i];
             }
             CK(cudaMemcpyAsync(ydev.p, y.data(), (j + 1) * sizeof(double), cudaMemcpyHostToDevice, st));
-            xc_guard();
+            trace.mark(st);
+            trace.mark(st);
             multi_axpy_any(B, xc.p, x, y, ydev.p, j + 1);
+            last_j = j;
+            trace.mark(st);
 
-            ops.apply(xc.p, tmp.p);
-            dev_sub_norm2(st, b, tmp.p, sc.out.p, sc.partials.p, sc.ticket.p, len);
+            // host mode: v_j's device copy is dead (its host copy is complete) and takes A x_cand
+            DevBuf<double>& ax = host_mode ? B.vlast : tmp;
+            if (host_mode) {
+                CK(cudaStreamWaitEvent(st, B.ev_vlast, 0));
+                B.vlast_index = -1;
+            }
+            ops.apply(xc.p, ax.p);
+            dev_sub_norm2(st, b, ax.p, sc.out.p, sc.partials.p, sc.ticket.p, len);
+            trace.mark(st);
             double r2 = 0;
             CK(cudaMemcpyAsync(&r2, sc.out.p, sizeof(double), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
+            trace.report(iter, j);
             true_res = std::sqrt(r2) / bnorm;
             log.entries.push_back({iter, true_res, {}, prec_res, elapsed()});
             if (true_res < best_res) {
                 best_res = true_res;
-                save_best(xc.p);
+                if (host_mode) {
+                    best_kind = 2;
+                    best_j = j;
+                    best_y = y;
+                } else {
+                    save_best(xc.p);
+                }
             }
             if (ops.observer) {
                 const auto to0 = std::chrono::steady_clock::now();
@@ -458,17 +563,40 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
             dev_scal(st, 1.0 / wn, w.p, len);
             put_basis(j + 1, w);
         }
+        // a full cycle without reducing the true residual (or a happy breakdown short of the
+        // tolerance) returns the best iterate
+        const bool fin = log.converged || stop_requested;
+        const bool stag = !fin && (true_res >= cycle_start_res * (1.0 - 1e-12) || happy);
+        if (!host_mode) {
+            CK(cudaMemcpyAsync(x, xc.p, bytes, cudaMemcpyDeviceToDevice, st));
+            if (stag) {
+                log.stagnated = true;
+                load_best(x);
+                break;
+            }
+            continue;
+        }
+        if (stag) {
+            if (best_kind == 2) {
+                recompute_best(xc.p);
+                CK(cudaMemcpyAsync(x, xc.p, bytes, cudaMemcpyDeviceToDevice, st));
+            } else if (best_kind == 3) {
+                CK(cudaMemcpyAsync(x, best_host, bytes, cudaMemcpyHostToDevice, st));
+            }  // best_kind 1: x holds it
+            log.stagnated = true;
+            break;
+        }
+        if (!fin) {  // x moves on to x_cand: keep the best iterate recoverable
+            if (best_kind == 2 && best_j != last_j) {
+                recompute_best(w.p);
+                materialise(w.p);
+            } else if (best_kind == 2) {
+                best_kind = 1;
+            } else if (best_kind == 1) {
+                materialise(x);
+            }
+        }
         CK(cudaMemcpyAsync(x, xc.p, bytes, cudaMemcpyDeviceToDevice, st));
-        if (!log.converged && !stop_requested && true_res >= cycle_start_res * (1.0 - 1e-12)) {
-            log.stagnated = true;
-            load_best(x);
-            break;
-        }
-        if (happy && !log.converged && !stop_requested) {
-            log.stagnated = true;
-            load_best(x);
-            break;
-        }
     }
     CK(cudaStreamSynchronize(st));
     if (B.cs) CK(cudaStreamSynchronize(B.cs));

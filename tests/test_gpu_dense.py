@@ -180,3 +180,31 @@ def test_twisted_factorisation_matches_reference(mk):
     want = ref.precond_apply(x, _abi.FWI_PRECOND_EXACT)
     got = fw.precond_apply(dev, fw.KktVector.from_host(dev, x), fw.PrecondMode.exact).to_host()
     assert rel(got, want) <= 1e-10
+
+
+@pytest.mark.parametrize("mode,restart,maxit", [("exact", 1, 12), ("exact", 2, 12), ("exact", 4, 20),
+                                                ("ilu", 3, 30)])
+def test_host_basis_returns_the_device_mode_solution(mode, restart, maxit):
+    """The host-resident basis keeps the best iterate recoverable (x + V y recomputed from
+    the basis) instead of copying it out per improvement: the returned update equals the
+    device-resident solver's bit for bit, including stagnation returns."""
+    p = c1_problem()
+    p.d_obs = po.ref_simulate(p)
+    ref = po.Ref(p, full=True, exact=True, ilu_level=4) if mode == "ilu" else po.Ref(p, full=True, exact=True)
+    q = c1_problem()
+    q.d_obs, q.u, q.r = p.d_obs, ref.u(), ref.residual()
+    dev = fw.GnState(q, exact=True, ilu_level=4 if mode == "ilu" else -1)
+    pm = _abi.FWI_PRECOND_ILU if mode == "ilu" else _abi.FWI_PRECOND_EXACT
+    ds_r, log_r = ref.fsgn(pm, restart, 0.0, maxit, 0)
+    opts = fw.FsgnOptions(mode=fw.PrecondMode.ilu if mode == "ilu" else fw.PrecondMode.exact, restart=restart,
+                          tol=0.0, maxit=maxit, ecg_stride=0)
+    ds_dev, log_dev = fw.fsgn_gmres_step(dev, opts)
+    os.environ["FWI_GMRES_HOST_BASIS"] = "1"
+    try:
+        ds_h, log_h = fw.fsgn_gmres_step(dev, opts)
+    finally:
+        del os.environ["FWI_GMRES_HOST_BASIS"]
+    assert np.array_equal(np.asarray(ds_h), np.asarray(ds_dev))
+    assert log_h.residuals() == log_dev.residuals() and log_h.stagnated == log_dev.stagnated
+    assert log_h.stagnated == log_r.stagnated
+    assert np.linalg.norm(np.asarray(ds_h) - np.asarray(ds_r)) <= 1e-6 * np.linalg.norm(np.asarray(ds_r))
