@@ -68,8 +68,19 @@ __global__ void __launch_bounds__(kRedThreads) dot_kernel(const double2* __restr
                                                           double* out) {
     __shared__ double sh[32];
     double acc = 0.0;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
-         i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    for (; i + 3 * stride < m; i += 4 * stride) {  // loads first, same accumulation order
+        double2 a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a[u] = x[i + u * stride];
+            b[u] = y[i + u * stride];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc += a[u].x * b[u].x + a[u].y * b[u].y;
+    }
+    for (; i < m; i += stride) {
         const double2 a = x[i], b = y[i];
         acc += a.x * b.x + a.y * b.y;
     }
@@ -98,6 +109,49 @@ __global__ void scal_kernel(double a, double2* __restrict__ x, int64_t m) {
     }
 }
 
+
+// One thread's share of an MGS step, w -= h_{i-1} v_{i-1}; acc += <v_i, w>, over its
+// grid-stride elements in order. The loads of U elements are issued before any of
+// them is used (memory-level parallelism); the accumulation order is unchanged.
+constexpr int kMgsUnroll = 4;
+__device__ __forceinline__ void mgs_elem(double2& wv, const double2& pv, const double2& nv, double nh, bool prev,
+                                         bool next, double& acc) {
+    if (prev) {
+        wv.x = __dadd_rn(wv.x, __dmul_rn(nh, pv.x));
+        wv.y = __dadd_rn(wv.y, __dmul_rn(nh, pv.y));
+    }
+    const double2 n = next ? nv : wv;
+    acc += n.x * wv.x + n.y * wv.y;
+}
+__device__ __forceinline__ double mgs_pass(double2* __restrict__ w, const double2* __restrict__ vprev, double nh,
+                                           const double2* __restrict__ vnext, int64_t m, int64_t t0, int64_t stride) {
+    constexpr int U = kMgsUnroll;
+    double acc = 0.0;
+    int64_t t = t0;
+    for (; t + (U - 1) * stride < m; t += U * stride) {
+        double2 wv[U], pv[U], nv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            wv[u] = w[t + u * stride];
+            pv[u] = vprev ? vprev[t + u * stride] : make_double2(0.0, 0.0);
+            nv[u] = vnext ? vnext[t + u * stride] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            mgs_elem(wv[u], pv[u], nv[u], nh, vprev != nullptr, vnext != nullptr, acc);
+            if (vprev) w[t + u * stride] = wv[u];
+        }
+    }
+    for (; t < m; t += stride) {
+        double2 wv = w[t];
+        const double2 pv = vprev ? vprev[t] : make_double2(0.0, 0.0);
+        const double2 nv = vnext ? vnext[t] : make_double2(0.0, 0.0);
+        mgs_elem(wv, pv, nv, nh, vprev != nullptr, vnext != nullptr, acc);
+        if (vprev) w[t] = wv;
+    }
+    return acc;
+}
+
 // MGS step (krylov.hpp:183-186), fused: w -= h_{i-1} v_{i-1} (h read from
 // device memory, no host round trip), then h_i = <v_i, w> (or <w, w> when
 // vnext is null, for ||w||).
@@ -109,19 +163,8 @@ __global__ void __launch_bounds__(kRedThreads) mgs_kernel(double2* __restrict__ 
                                                           double* out) {
     __shared__ double sh[32];
     const double nh = vprev ? -*hprev : 0.0;
-    double acc = 0.0;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        double2 wv = w[i];
-        if (vprev) {
-            const double2 pv = vprev[i];
-            wv.x = __dadd_rn(wv.x, __dmul_rn(nh, pv.x));
-            wv.y = __dadd_rn(wv.y, __dmul_rn(nh, pv.y));
-            w[i] = wv;
-        }
-        const double2 nv = vnext ? vnext[i] : wv;
-        acc += nv.x * wv.x + nv.y * wv.y;
-    }
+    double acc = mgs_pass(w, vprev, nh, vnext, m, blockIdx.x * int64_t(blockDim.x) + threadIdx.x,
+                          int64_t(gridDim.x) * blockDim.x);
     acc = block_sum(acc, sh);
     finish_reduction(acc, partials, ticket, out);
 }
@@ -136,19 +179,8 @@ __global__ void __launch_bounds__(kRedThreads) mgs_partial_kernel(double2* __res
                                                                   double* partials_out) {
     __shared__ double sh[32];
     const double nh = vprev ? -*hprev : 0.0;
-    double acc = 0.0;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        double2 wv = w[i];
-        if (vprev) {
-            const double2 pv = vprev[i];
-            wv.x = __dadd_rn(wv.x, __dmul_rn(nh, pv.x));
-            wv.y = __dadd_rn(wv.y, __dmul_rn(nh, pv.y));
-            w[i] = wv;
-        }
-        const double2 nv = vnext ? vnext[i] : wv;
-        acc += nv.x * wv.x + nv.y * wv.y;
-    }
+    double acc = mgs_pass(w, vprev, nh, vnext, m, blockIdx.x * int64_t(blockDim.x) + threadIdx.x,
+                          int64_t(gridDim.x) * blockDim.x);
     acc = block_sum(acc, sh);
     if (threadIdx.x == 0) partials_out[blockIdx.x] = acc;
 }
@@ -219,17 +251,7 @@ __global__ void __launch_bounds__(kRedThreads) mgs_all_kernel(double2* __restric
                 if (i + 1 < m && t < len2) nq[q] = a.v[i + 1][t];
             }
         } else {
-            for (int64_t t = t0; t < len2; t += stride) {
-                double2 wv = w[t];
-                if (vprev) {
-                    const double2 pv = vprev[t];
-                    wv.x = __dadd_rn(wv.x, __dmul_rn(nh, pv.x));
-                    wv.y = __dadd_rn(wv.y, __dmul_rn(nh, pv.y));
-                    w[t] = wv;
-                }
-                const double2 nv = vnext ? vnext[t] : wv;
-                acc += nv.x * wv.x + nv.y * wv.y;
-            }
+            acc = mgs_pass(w, vprev, nh, vnext, len2, t0, stride);
         }
         acc = block_sum(acc, sh);
         if (threadIdx.x == 0) {
@@ -293,8 +315,22 @@ __global__ void __launch_bounds__(kRedThreads) sub_norm2_kernel(const double2* _
                                                                 double* out) {
     __shared__ double sh[32];
     double acc = 0.0;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
-         i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    for (; i + 3 * stride < m; i += 4 * stride) {  // loads first, same accumulation order
+        double2 bv[4], av[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            bv[u] = b[i + u * stride];
+            av[u] = ax[i + u * stride];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double rx = __dsub_rn(bv[u].x, av[u].x), ry = __dsub_rn(bv[u].y, av[u].y);
+            acc += rx * rx + ry * ry;
+        }
+    }
+    for (; i < m; i += stride) {
         const double2 bv = b[i], av = ax[i];
         const double rx = __dsub_rn(bv.x, av.x), ry = __dsub_rn(bv.y, av.y);
         acc += rx * rx + ry * ry;

@@ -47,6 +47,8 @@ static double bench(bool bt, int M, int N, int K, int reps) {
 
 int main() {
     bench(true, 256, 1024, 1024, 50);   // C5 sweep step
+    bench(true, 512, 1024, 1024, 50);   // two sweep steps batched (twisted sweep, one launch)
+    bench(true, 1024, 1024, 1024, 20);  // large
     bench(false, 1024, 1024, 64, 100);  // C5 Gauss-Jordan update
     bench(false, 64, 1024, 64, 100);    // D^{-1} row block
     bench(true, 48, 128, 128, 200);     // C3-sized (dense path forced)
