@@ -497,11 +497,13 @@ KktPlan* build_plan(Ctx& c, bool f32) {
             tiles.push_back(make_int4(x0, std::min(W, nx - x0), z0, std::min(kRows, nz - z0)));
         }
     p->T = int(tiles.size());
-    // K-chunk per unit: enough units (~12 per SM) for dynamic balance; a power
-    // of two dividing K
+    // K-chunk per unit: the largest power of two dividing K that still gives every
+    // CTA a unit. Smaller chunks do not balance better: a tile's chunks fold in
+    // order, and each fold costs a wait (config 3, 48 tiles x K=48: KC=8 58.8 us,
+    // KC=4 64.1 us, KC=2 88.5 us per apply; tools/apply_sizes.py)
     const int G0 = sm_count() * kCtasPerSm;
     int kc = 8;
-    while (kc > 1 && (K % kc != 0 || int64_t(p->T) * (K / kc) < int64_t(4) * G0)) kc /= 2;
+    while (kc > 1 && (K % kc != 0 || int64_t(p->T) * (K / kc) < int64_t(G0))) kc /= 2;
     if (const char* e = std::getenv("FWI_KKT_KC")) {
         const int v = std::atoi(e);
         if ((v == 1 || v == 2 || v == 4 || v == 8) && K % v == 0) kc = v;
