@@ -289,6 +289,18 @@ __global__ void put_rows(int nb, int kb, int bs, const double2* R, double2* A, i
     A[int64_t(kb + t / nb) * lda + t % nb] = R[t];
 }
 
+// twisted middle line: T[k][m] = b[k][m] - e1[m] v1[k][m] - e2[m] v2[k][m]
+__global__ void sweep_middle(int nb, int nrhs, const double2* __restrict__ b, const double2* __restrict__ e1,
+                             const double2* __restrict__ v1, const double2* __restrict__ e2,
+                             const double2* __restrict__ v2, double2* __restrict__ T) {
+    const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (t >= int64_t(nb) * nrhs) return;
+    const int m = int(t % nb);
+    const double2 a = e1[m], x = v1[t], c = e2[m], y = v2[t];
+    T[t] = make_double2(b[t].x - (a.x * x.x - a.y * x.y) - (c.x * y.x - c.y * y.y),
+                        b[t].y - (a.x * x.y + a.y * x.x) - (c.x * y.y + c.y * y.x));
+}
+
 // sweep prologue: T[k][m] = bsel ? b[k][m] - e[m] v[k][m] : e[m] v[k][m]   (v may be null)
 __global__ void sweep_prologue(int nb, int nrhs, const double2* __restrict__ b, const double2* __restrict__ e,
                                const double2* __restrict__ v, double2* __restrict__ T) {
@@ -412,14 +424,164 @@ __global__ void __launch_bounds__(256) zgemm_dmma_kernel(int M, int N, int K, do
             }
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined DMMA variant (default): BM x 64 output tile per CTA (BM = 32 or 64),
+// 8 warps in a 2 x 4 grid, complex operands staged interleaved (re, im) in a
+// 3-stage cp.async ring so one 16-byte shared load yields both planes of a
+// fragment element; fragments for the next k4 step are loaded while the current
+// one issues its DMMAs. One block barrier per 16-deep K slab.
+// ---------------------------------------------------------------------------
+constexpr int kPBN = 64, kPBK = 16, kPStages = 3, kPPitchK = kPBK + 4, kPPitchN = kPBN + 2;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem), "r"(pred ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int BM, bool BT>
+constexpr int zgemm_pipe_smem() {
+    // A: [BM][kPPitchK]; B: BT ? [kPBN][kPPitchK] : [kPBK][kPPitchN]   (double2 elements)
+    return kPStages * (BM * kPPitchK + (BT ? kPBN * kPPitchK : kPBK * kPPitchN)) * 16;
+}
+
+template <int BM, bool BT>
+__global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, double alpha,
+                                                         const double2* __restrict__ A, int64_t lda,
+                                                         const double2* __restrict__ B, int64_t ldb,
+                                                         const double2* C0, int64_t ldc0, double2* C, int64_t ldc) {
+    extern __shared__ __align__(16) double2 psm[];
+    constexpr int ASZ = BM * kPPitchK, BSZ = BT ? kPBN * kPPitchK : kPBK * kPPitchN;
+    constexpr int TM = BM / 16;  // m8 tiles per warp (warp tile (BM/2) x 16)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 1, wn = warp >> 1;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * kPBN;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int KT = (K + kPBK - 1) / kPBK;
+
+    auto load_stage = [&](int stage, int k0) {
+        double2* As = psm + stage * (ASZ + BSZ);
+        double2* Bs = As + ASZ;
+#pragma unroll
+        for (int q = 0; q < BM * kPBK / 256; ++q) {
+            const int e = tid + q * 256, kk = e % kPBK, mm = e / kPBK;
+            const int m = m0 + mm, k = k0 + kk;
+            const bool ok = m < M && k < K;
+            cp_async16(As + mm * kPPitchK + kk, ok ? A + int64_t(m) * lda + k : A, ok);
+        }
+#pragma unroll
+        for (int q = 0; q < kPBN * kPBK / 256; ++q) {
+            const int e = tid + q * 256;
+            if (BT) {
+                const int kk = e % kPBK, nn = e / kPBK, n = n0 + nn, k = k0 + kk;
+                const bool ok = n < N && k < K;
+                cp_async16(Bs + nn * kPPitchK + kk, ok ? B + int64_t(n) * ldb + k : B, ok);
+            } else {
+                const int nn = e % kPBN, kk = e / kPBN, n = n0 + nn, k = k0 + kk;
+                const bool ok = n < N && k < K;
+                cp_async16(Bs + kk * kPPitchN + nn, ok ? B + int64_t(k) * ldb + n : B, ok);
+            }
+        }
+    };
+
+    double P[TM][2][2] = {}, Q[TM][2][2] = {}, I[TM][2][2] = {};
+#pragma unroll
+    for (int s = 0; s < kPStages - 1; ++s) {
+        if (s < KT) load_stage(s, s * kPBK);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < KT; ++kt) {
+        cp_async_wait<kPStages - 2>();
+        __syncthreads();  // stage kt landed for every thread; stage kt-1 is free
+        {
+            const int nk = kt + kPStages - 1;
+            if (nk < KT) load_stage(nk % kPStages, nk * kPBK);
+            cp_async_commit();
+        }
+        const double2* As = psm + (kt % kPStages) * (ASZ + BSZ);
+        const double2* Bs = As + ASZ;
+        double2 fa[2][TM], fb[2][2];
+        auto frag = [&](int buf, int ks) {
+#pragma unroll
+            for (int t = 0; t < TM; ++t) fa[buf][t] = As[(wm * (BM / 2) + t * 8 + g) * kPPitchK + ks + t4];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+                fb[buf][u] = BT ? Bs[(wn * 16 + u * 8 + g) * kPPitchK + ks + t4]
+                                : Bs[(ks + t4) * kPPitchN + wn * 16 + u * 8 + g];
+        };
+        frag(0, 0);
+#pragma unroll
+        for (int k4 = 0; k4 < kPBK / 4; ++k4) {
+            const int cur = k4 & 1;
+            if (k4 + 1 < kPBK / 4) frag(cur ^ 1, (k4 + 1) * 4);
+#pragma unroll
+            for (int t = 0; t < TM; ++t)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    dmma(P[t][u], fa[cur][t].x, fb[cur][u].x);
+                    dmma(Q[t][u], fa[cur][t].y, fb[cur][u].y);
+                    dmma(I[t][u], fa[cur][t].x, fb[cur][u].y);
+                    dmma(I[t][u], fa[cur][t].y, fb[cur][u].x);
+                }
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int t = 0; t < TM; ++t)
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int m = m0 + wm * (BM / 2) + t * 8 + g, n = n0 + wn * 16 + u * 8 + 2 * t4 + e;
+                if (m >= M || n >= N) continue;
+                double2 v = make_double2(alpha * (P[t][u][e] - Q[t][u][e]), alpha * I[t][u][e]);
+                if (C0) {
+                    const double2 c = C0[int64_t(m) * ldc0 + n];
+                    v.x += c.x;
+                    v.y += c.y;
+                }
+                C[int64_t(m) * ldc + n] = v;
+            }
+}
+
+template <int BM, bool BT>
+void zgemm_pipe_launch(cudaStream_t st, int M, int N, int K, double alpha, const double2* A, int64_t lda,
+                       const double2* B, int64_t ldb, const double2* C0, int64_t ldc0, double2* C, int64_t ldc) {
+    constexpr int smem = zgemm_pipe_smem<BM, BT>();
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(zgemm_pipe_kernel<BM, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    zgemm_pipe_kernel<BM, BT><<<dim3((N + kPBN - 1) / kPBN, (M + BM - 1) / BM), 256, smem, st>>>(
+        M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
+    CK_LAUNCH();
+}
+
 template <bool BT>
 void cgemm_launch(cudaStream_t st, int M, int N, int K, double alpha, const double2* A, int64_t lda,
                   const double2* B, int64_t ldb, const double2* C0, int64_t ldc0, double2* C, int64_t ldc) {
-    static const bool simt = [] {
+    // FWI_CGEMM: "pipe" (default), "dmma" (the unpipelined DMMA kernel), "simt"
+    static const int variant = [] {
         const char* e = std::getenv("FWI_CGEMM");
-        return e && std::string(e) == "simt";
+        if (!e) return 0;
+        const std::string v(e);
+        return v == "simt" ? 2 : v == "dmma" ? 1 : 0;
     }();
-    if (!simt) {
+    if (variant == 0) {
+        // 64-row tiles only when they still give every SM a tile
+        const int tiles64 = ((N + kPBN - 1) / kPBN) * ((M + 63) / 64);
+        if (tiles64 >= sm_count())
+            zgemm_pipe_launch<64, BT>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
+        else
+            zgemm_pipe_launch<32, BT>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
+        return;
+    }
+    if (variant == 1) {
         zgemm_dmma_kernel<BT><<<dim3((N + kTBN - 1) / kTBN, (M + kTBM - 1) / kTBM), 256, 0, st>>>(
             M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
         CK_LAUNCH();
@@ -499,6 +661,59 @@ void dense_sweep(cudaStream_t st, int L, int nb, int nrhs, const double2* G, int
         cgemm_launch<true>(st, nrhs, nb, nb, -1.0, T, nb, G + int64_t(i) * nb * gp, gp, W + i * blk, nb,
                            W + i * blk, nb);
     }
+}
+
+void dense_sweep_twisted(cudaStream_t st, cudaStream_t st2, cudaEvent_t fork, cudaEvent_t join, int L, int m, int nb,
+                         int nrhs, const double2* G, int64_t gp, const double2* coup, double2* W, double2* T,
+                         double2* T2) {
+    const int64_t blk = int64_t(nrhs) * nb;
+    const int nbk = blocks_for(blk);
+    auto Gl = [&](int i) { return G + int64_t(i) * nb * gp; };
+    auto cl = [&](int i) { return coup + int64_t(i) * nb; };  // lines i, i+1
+    CK(cudaEventRecord(fork, st));
+    CK(cudaStreamWaitEvent(st2, fork, 0));
+    // launches alternate between the chains (a full launch queue would otherwise
+    // serialise them)
+    const int R = std::max(m, L - 1 - m);
+    for (int r = 0; r < R; ++r) {
+        if (r < m) {  // top, forward: y_i = G_i (b_i - E_{i-1} y_{i-1})
+            const int i = r;
+            sweep_prologue<<<nbk, 256, 0, st>>>(nb, nrhs, W + i * blk, i > 0 ? cl(i - 1) : nullptr,
+                                                i > 0 ? W + (i - 1) * blk : nullptr, T);
+            CK_LAUNCH();
+            cgemm_launch<true>(st, nrhs, nb, nb, 1.0, T, nb, Gl(i), gp, nullptr, 0, W + i * blk, nb);
+        }
+        const int i = L - 1 - r;
+        if (i > m) {  // bottom, forward: y_i = G_i (b_i - E_i y_{i+1})
+            sweep_prologue<<<nbk, 256, 0, st2>>>(nb, nrhs, W + i * blk, i < L - 1 ? cl(i) : nullptr,
+                                                 i < L - 1 ? W + (i + 1) * blk : nullptr, T2);
+            CK_LAUNCH();
+            cgemm_launch<true>(st2, nrhs, nb, nb, 1.0, T2, nb, Gl(i), gp, nullptr, 0, W + i * blk, nb);
+        }
+    }
+    CK(cudaEventRecord(join, st2));
+    CK(cudaStreamWaitEvent(st, join, 0));
+    // middle: x_m = G_m (b_m - E_{m-1} y_{m-1} - E_m y_{m+1})
+    sweep_middle<<<nbk, 256, 0, st>>>(nb, nrhs, W + m * blk, cl(m - 1), W + (m - 1) * blk, cl(m), W + (m + 1) * blk, T);
+    CK_LAUNCH();
+    cgemm_launch<true>(st, nrhs, nb, nb, 1.0, T, nb, Gl(m), gp, nullptr, 0, W + m * blk, nb);
+    CK(cudaEventRecord(fork, st));
+    CK(cudaStreamWaitEvent(st2, fork, 0));
+    for (int r = 0; r < R; ++r) {
+        const int it = m - 1 - r, ib = m + 1 + r;
+        if (it >= 0) {  // top, backward: x_i = y_i - G_i (E_i x_{i+1})
+            sweep_prologue<<<nbk, 256, 0, st>>>(nb, nrhs, nullptr, cl(it), W + (it + 1) * blk, T);
+            CK_LAUNCH();
+            cgemm_launch<true>(st, nrhs, nb, nb, -1.0, T, nb, Gl(it), gp, W + it * blk, nb, W + it * blk, nb);
+        }
+        if (ib < L) {  // bottom, backward: x_i = y_i - G_i (E_{i-1} x_{i-1})
+            sweep_prologue<<<nbk, 256, 0, st2>>>(nb, nrhs, nullptr, cl(ib - 1), W + (ib - 1) * blk, T2);
+            CK_LAUNCH();
+            cgemm_launch<true>(st2, nrhs, nb, nb, -1.0, T2, nb, Gl(ib), gp, W + ib * blk, nb, W + ib * blk, nb);
+        }
+    }
+    CK(cudaEventRecord(join, st2));
+    CK(cudaStreamWaitEvent(st, join, 0));
 }
 
 }  // namespace fwi_b200

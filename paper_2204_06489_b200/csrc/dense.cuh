@@ -23,6 +23,13 @@ void dense_invert(cudaStream_t st, int nb, double2* A, int64_t lda, DenseWork& w
 
 // Forward/backward line sweeps for nrhs right-hand sides in W[i][k][m] (overwritten
 // in place by y, then by the solution); T is nrhs x nb scratch.
+// Twisted sweeps (factor built from both ends towards line m): the top chain
+// (lines 0..m-1) on st, the bottom chain (L-1..m+1) on st2, then the middle line,
+// then both backward chains outwards again. T, T2: nrhs x nb scratch per chain.
+void dense_sweep_twisted(cudaStream_t st, cudaStream_t st2, cudaEvent_t fork, cudaEvent_t join, int L, int m, int nb,
+                         int nrhs, const double2* G, int64_t gp, const double2* coup, double2* W, double2* T,
+                         double2* T2);
+
 void dense_sweep(cudaStream_t st, int L, int nb, int nrhs, const double2* G, int64_t gp, const double2* coup,
                  double2* W, double2* T);
 

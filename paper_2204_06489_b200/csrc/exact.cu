@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <string>
 #include <array>
+#include <chrono>
 #include <mutex>
 #include <type_traits>
 #include <cstdio>
@@ -50,6 +51,25 @@ struct ExactFactor {
     int mid = 0;
     DenseWork dwork;
     DevBuf<double2> tbuf;   // dense sweep operand (nrhs x nb)
+    // the second chain of a twisted dense factor / sweep runs on its own stream
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    DenseWork dwork2;
+    DevBuf<double2> tbuf2;
+    void ensure_side() {
+        if (s2) return;
+        CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+    ~ExactFactor() {
+        if (s2) {
+            cudaStreamSynchronize(s2);
+            cudaStreamDestroy(s2);
+        }
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+    }
 };
 
 void exact_free(ExactFactor* f) { delete f; }
@@ -1227,6 +1247,7 @@ size_t sweep_smem(int nb) {
 }  // namespace
 
 void exact_factor(Ctx& c) {
+    const auto t_host0 = std::chrono::steady_clock::now();
     auto f = std::make_unique<ExactFactor>();
     f->col_lines = c.nz <= c.nx;  // short lines by default (least factor work and storage)
     // A line step is latency-bound (fixed dependent chain + work per column), so
@@ -1270,10 +1291,13 @@ void exact_factor(Ctx& c) {
     // so a solve is two concurrent sweep chains of ~L/2 lines each (then a dense
     // solve of the middle line) instead of one chain of L: a line step is latency-
     // bound, so this halves the sweep. Used when the step model says it pays.
-    if (f->dense_factor && !f->dense && L >= 8) {
+    if (f->dense_factor && L >= 8) {
         const char* et = std::getenv("FWI_EXACT_TWISTED");
         if (et) {
             f->twisted = std::string(et) == "1";
+        } else if (f->dense) {
+            // GEMM sweeps: two concurrent chains fill the GPU (one C5 step GEMM has 128 tiles)
+            f->twisted = true;
         } else {
             WarpPlan p1, p2;
             const int m = L / 2;
@@ -1286,21 +1310,38 @@ void exact_factor(Ctx& c) {
         const int64_t nn = int64_t(nb) * nb;
         auto Gl = [&](int i) { return f->G.p + i * int64_t(nb) * f->gp; };
         auto cl = [&](int i) { return f->coup.p + int64_t(i) * nb; };  // coupling of lines i, i+1
-        auto line = [&](int i, const double2* cA, const double2* GA, const double2* cB, const double2* GB) {
-            form_schur<<<int((nn + 255) / 256), 256, 0, c.stream>>>(f->col_lines, c.nx, nb, i, c.diag.p, c.east.p,
-                                                                    c.south.p, cA, GA, cB, GB, f->gp, Gl(i));
+        auto line = [&](cudaStream_t st, DenseWork& dw, int i, const double2* cA, const double2* GA,
+                        const double2* cB, const double2* GB) {
+            form_schur<<<int((nn + 255) / 256), 256, 0, st>>>(f->col_lines, c.nx, nb, i, c.diag.p, c.east.p,
+                                                              c.south.p, cA, GA, cB, GB, f->gp, Gl(i));
             CK_LAUNCH();
-            dense_invert(c.stream, nb, Gl(i), f->gp, f->dwork, f->status.p, i * nb);
+            dense_invert(st, nb, Gl(i), f->gp, dw, f->status.p, i * nb);
         };
         if (!f->twisted) {
-            for (int i = 0; i < L; ++i) line(i, i > 0 ? cl(i - 1) : nullptr, i > 0 ? Gl(i - 1) : nullptr, nullptr, nullptr);
+            for (int i = 0; i < L; ++i)
+                line(c.stream, f->dwork, i, i > 0 ? cl(i - 1) : nullptr, i > 0 ? Gl(i - 1) : nullptr, nullptr, nullptr);
         } else {
+            // the two recursions are independent: top chain on the context stream, bottom
+            // chain on the factor's second stream, then the middle line
             const int m = L / 2;
             f->mid = m;
-            for (int i = 0; i < m; ++i) line(i, i > 0 ? cl(i - 1) : nullptr, i > 0 ? Gl(i - 1) : nullptr, nullptr, nullptr);
-            for (int i = L - 1; i > m; --i)
-                line(i, i < L - 1 ? cl(i) : nullptr, i < L - 1 ? Gl(i + 1) : nullptr, nullptr, nullptr);
-            line(m, cl(m - 1), Gl(m - 1), cl(m), Gl(m + 1));
+            f->ensure_side();
+            CK(cudaEventRecord(f->ev_fork, c.stream));
+            CK(cudaStreamWaitEvent(f->s2, f->ev_fork, 0));
+            // launches alternate between the chains: the launch queue fills up, so
+            // enqueueing one whole chain first would serialise them
+            for (int r = 0; r < std::max(m, L - 1 - m); ++r) {
+                if (r < m)
+                    line(c.stream, f->dwork, r, r > 0 ? cl(r - 1) : nullptr, r > 0 ? Gl(r - 1) : nullptr, nullptr,
+                         nullptr);
+                const int i = L - 1 - r;
+                if (i > m)
+                    line(f->s2, f->dwork2, i, i < L - 1 ? cl(i) : nullptr, i < L - 1 ? Gl(i + 1) : nullptr, nullptr,
+                         nullptr);
+            }
+            CK(cudaEventRecord(f->ev_join, f->s2));
+            CK(cudaStreamWaitEvent(c.stream, f->ev_join, 0));
+            line(c.stream, f->dwork, m, cl(m - 1), Gl(m - 1), cl(m), Gl(m + 1));
         }
     } else {
     const bool smem = nb <= 112;
@@ -1329,6 +1370,10 @@ void exact_factor(Ctx& c) {
     int st = 0;
     CK(cudaMemcpyAsync(&st, f->status.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
+    if (std::getenv("FWI_EXACT_PLAN_LOG"))
+        std::fprintf(stderr, "[fwi] exact factor nb=%d L=%d dense=%d twisted=%d: %.3f s\n", nb, L, int(f->dense),
+                     int(f->twisted),
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t_host0).count());
     if (st != 0)
         throw FwiError(FWI_ERR_SINGULAR_PIVOT,
                        "LU: singular pivot at elimination step " + std::to_string(st - 1), st - 1);
@@ -1362,7 +1407,13 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
     if (f.dense) {
         ExactFactor& fm = const_cast<ExactFactor&>(f);
         if (fm.tbuf.count < size_t(nrhs) * f.nb) fm.tbuf.alloc(size_t(nrhs) * f.nb);
-        dense_sweep(c.stream, f.L, f.nb, nrhs, f.G.p, f.gp, f.coup.p, W, fm.tbuf.p);
+        if (f.twisted) {
+            if (fm.tbuf2.count < size_t(nrhs) * f.nb) fm.tbuf2.alloc(size_t(nrhs) * f.nb);
+            dense_sweep_twisted(c.stream, fm.s2, fm.ev_fork, fm.ev_join, f.L, f.mid, f.nb, nrhs, f.G.p, f.gp,
+                                f.coup.p, W, fm.tbuf.p, fm.tbuf2.p);
+        } else {
+            dense_sweep(c.stream, f.L, f.nb, nrhs, f.G.p, f.gp, f.coup.p, W, fm.tbuf.p);
+        }
         done = true;
     }
     const char* sw = std::getenv("FWI_EXACT_SWEEP");  // "warp" (default) | "cta" | "legacy"

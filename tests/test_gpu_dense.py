@@ -18,20 +18,26 @@ def rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
-def dense_state(p, **kw):
+def dense_state(p, twisted=None, **kw):
+    """Dense (GEMM-sweep) exact solver; twisted "0"/"1" forces the one-chain or the
+    two-chain (twisted, the default for dense lines) factorisation."""
     os.environ["FWI_EXACT_DENSE"] = "1"
+    if twisted is not None:
+        os.environ["FWI_EXACT_TWISTED"] = twisted
     try:
         return fw.GnState(p, exact=True, **kw)
     finally:
         del os.environ["FWI_EXACT_DENSE"]
+        os.environ.pop("FWI_EXACT_TWISTED", None)
 
 
+@pytest.mark.parametrize("twisted", ["0", "1"])
 @pytest.mark.parametrize("mk", [small_problem, standard_instance,
                                 lambda: small_problem(nx=70, nz=90, n_pml=5, K=2, R=4)])
-def test_dense_block_solve_matches_reference_lu(mk):
+def test_dense_block_solve_matches_reference_lu(mk, twisted):
     p = mk()
     ref = po.Ref(p, full=False, exact=True)
-    dev = dense_state(p)
+    dev = dense_state(p, twisted)
     rng = np.random.default_rng(5)
     b = rng.standard_normal((3, p.n)) + 1j * rng.standard_normal((3, p.n))
     for adj in (False, True):

@@ -36,11 +36,16 @@ res = float(np.linalg.norm(la - b) / np.linalg.norm(b))
 t0 = time.perf_counter()
 sc = st.solve_count(fw.PrecondMode.exact)
 xk = fw.KktVector.from_host(st, np.random.default_rng(2).standard_normal(st.vec_len))
-t1 = time.perf_counter()
-yk = fw.precond_apply(st, xk)
-_ = fw.norm(yk)
-t_prec = time.perf_counter() - t1
+yk = fw.KktVector(st)
+times = []
+for _ in range(3):  # the first apply also allocates the solve's work buffers
+    t1 = time.perf_counter()
+    fw.precond_apply(st, xk, out=yk)
+    _ = fw.norm(yk)
+    times.append(time.perf_counter() - t1)
+t_prec = sorted(times[1:])[0]
 r = {"config": "C5 exact", "state_s": t_state, "solve_8rhs_s": t_solve8, "precond_apply_s": t_prec,
+     "precond_apply_first_s": times[0],
      "solve_residual_rel": res, "device_bytes": st.device_bytes}
 print(json.dumps(r), flush=True)
 with open("gpurun_out/c5_exact.json", "w") as f:

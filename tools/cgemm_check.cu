@@ -83,5 +83,8 @@ int main() {
     run(false, 64, 1024, 64, 1.0, false);
     run(true, 37, 70, 45, -1.0, true);
     run(false, 70, 37, 45, 1.0, false);
+    run(true, 1024, 1024, 256, -1.0, true);   // 64-row tiles
+    run(true, 150, 200, 75, 1.0, true);       // ragged
+    run(false, 1030, 1000, 70, -1.0, true);   // ragged, 64-row tiles
     return 0;
 }
