@@ -249,9 +249,12 @@ __device__ __forceinline__ void cp_wait() {
 // ld.global.cg so a CTA always sees its own earlier levels' stores) and only the
 // level metadata is staged — for vectors beyond shared memory (config 3/4:
 // n = 49,152 -> 786 KB per right-hand side).
+// x operands: shared memory (XS), or global memory through L1 (L1) or L2 only. The
+// rows of one level read what this CTA's threads wrote before the level barrier, so
+// L1-cached loads see it (CTA-scope ordering of bar.sync).
 __device__ __forceinline__ double2 xload(const double2* p, bool glob) { return glob ? __ldcg(p) : *p; }
 
-template <int KIND, bool XS>
+template <int KIND, bool XS, bool L1 = false>
 __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int4* __restrict__ lmeta,
                                                      int meta_smem, const int* __restrict__ lvl_rows,
                                                      const int* __restrict__ rstart,
@@ -313,9 +316,8 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
         for (int t = ct; t < nrow; t += cn) {
             const int i = rib[b * rcap + t];
             const int p0 = rp[t] - e0, p1 = rp[t + 1] - e0;
-            double2 s = xload(xs + i, !XS);
+            double2 s = xload(xs + i, !XS && !L1);
             double2 dg = make_double2(0.0, 0.0);
-            if constexpr (XS) {
             // Entries in the reference's order. A batch of 8 loads its indices, values and x
             // operands first, forms the 8 products independently, then runs the dependent
             // subtraction chain with selects (no per-entry branches, so the loads overlap).
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
                     av[u] = vl[pp];
                 }
 #pragma unroll
-                for (int u = 0; u < BT; ++u) xv[u] = xload(xs + kv[u], !XS);
+                for (int u = 0; u < BT; ++u) xv[u] = xload(xs + kv[u], !XS && !L1);
                 double2 tv[BT];
 #pragma unroll
                 for (int u = 0; u < BT; ++u)
@@ -348,37 +350,6 @@ __global__ void __launch_bounds__(256) ilu_sweep_smem(int n, int nlev, const int
                     const double2 sn = csub(s, tv[u]);
                     s = use ? sn : s;
                 }
-            }
-            } else {
-            // entries in the reference's order; the x operands of a batch of 8 are loaded
-            // before the dependent subtraction chain (one L2 round trip per batch, not per entry)
-            constexpr int BT = 8;
-            const int q0 = (KIND == kUbwd) ? p0 + 1 : p0;
-            for (int pb = q0; pb < p1; pb += BT) {
-                double2 xv[BT];
-#pragma unroll
-                for (int u = 0; u < BT; ++u) {
-                    const int p = pb + u;
-                    if (p < p1) {
-                        const int k = il[p];
-                        xv[u] = (KIND == kUtfwd && k == i) ? make_double2(0.0, 0.0) : xload(xs + k, !XS);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < BT; ++u) {
-                    const int p = pb + u;
-                    if (p < p1) {
-                        if (KIND == kUtfwd) {
-                            if (il[p] == i)
-                                dg = vl[p];
-                            else
-                                s = csub(s, cmulc(vl[p], xv[u]));
-                        } else {
-                            s = csub(s, (KIND == kLfwd || KIND == kUbwd) ? cmul(vl[p], xv[u]) : cmulc(vl[p], xv[u]));
-                        }
-                    }
-                }
-            }
             }
             if (KIND == kLfwd || KIND == kLtbwd)
                 xs[i] = s;
@@ -415,16 +386,24 @@ void run_sweep(const Sweep& s, int64_t n, int nrhs, double2* x, cudaStream_t st)
         CK_LAUNCH();
         return;
     }
-    if (meta <= 220 * 1024 && !mode) {  // vector in L2, level metadata staged in shared memory
+    if (meta <= 220 * 1024 && !mode) {  // vector in global memory, level metadata staged in shared memory
+        static const bool l2only = std::getenv("FWI_ILU_L2") != nullptr;  // diagnostics: bypass L1
         static size_t set = 0;
         if (meta > set) {
-            CK(cudaFuncSetAttribute(ilu_sweep_smem<KIND, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            CK(cudaFuncSetAttribute(ilu_sweep_smem<KIND, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(meta)));
+            CK(cudaFuncSetAttribute(ilu_sweep_smem<KIND, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(meta)));
             set = meta;
         }
-        ilu_sweep_smem<KIND, false><<<nrhs, nthr, meta, st>>>(int(n), s.nlev, s.lmeta.p, meta_smem,
-                                                            s.lvl_rows.p, s.rstart.p, s.lidx.p, s.lval.p, x,
-                                                            s.ecap, s.rcap);
+        if (l2only)
+            ilu_sweep_smem<KIND, false, false><<<nrhs, nthr, meta, st>>>(int(n), s.nlev, s.lmeta.p, meta_smem,
+                                                                       s.lvl_rows.p, s.rstart.p, s.lidx.p, s.lval.p,
+                                                                       x, s.ecap, s.rcap);
+        else
+            ilu_sweep_smem<KIND, false, true><<<nrhs, nthr, meta, st>>>(int(n), s.nlev, s.lmeta.p, meta_smem,
+                                                                      s.lvl_rows.p, s.rstart.p, s.lidx.p, s.lval.p,
+                                                                      x, s.ecap, s.rcap);
         CK_LAUNCH();
         return;
     }
