@@ -180,6 +180,10 @@ int fwi_dev_factor_ilu(fwi_dev_ctx* ctx, int level, double diag_shift);
  * counts them), and reset. */
 int64_t fwi_dev_solve_count(const fwi_dev_ctx* ctx, int mode);
 void fwi_dev_reset_solve_count(fwi_dev_ctx* ctx, int mode);
+/* Name of the K1 kernel the last fwi_dev_kkt_apply at this precision
+ * (FWI_C128 / FWI_C64) launched ("" before the first apply): diagnostics for
+ * benchmarks and profiles, no reference counterpart. */
+const char* fwi_dev_kkt_kernel(const fwi_dev_ctx* ctx, int precision);
 /* nrhs block solves A x = b (A^H x = b if adjoint) on host arrays of nrhs*n
  * complex, source-major. */
 int fwi_dev_solve(fwi_dev_ctx* ctx, int mode, int adjoint, int nrhs, const double* b_host,

@@ -162,6 +162,8 @@ def lib() -> C.CDLL:
             L.fwi_dev_solve_count.restype = C.c_int64
             L.fwi_dev_reset_solve_count.argtypes = [_vp, C.c_int]
             L.fwi_dev_reset_solve_count.restype = None
+            L.fwi_dev_kkt_kernel.argtypes = [_vp, C.c_int]
+            L.fwi_dev_kkt_kernel.restype = C.c_char_p
             _lib = L
     return _lib
 
@@ -277,6 +279,11 @@ class GnState:
     def factor_ilu(self, level: int, diag_shift: float = 0.0):
         _check(lib().fwi_dev_factor_ilu(self.h, level, diag_shift))
         self._info()
+
+    def kkt_kernel(self, precision=None) -> str:
+        """Name of the K1 kernel the last kkt_apply at this precision launched."""
+        prec = _abi.FWI_C128 if precision is None else precision
+        return lib().fwi_dev_kkt_kernel(self.h, int(prec)).decode()
 
     def solve_count(self, mode=PrecondMode.exact) -> int:
         return lib().fwi_dev_solve_count(self.h, int(mode))

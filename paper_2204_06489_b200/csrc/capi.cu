@@ -206,6 +206,11 @@ int64_t fwi_dev_solve_count(const fwi_dev_ctx* ctx, int mode) {
     return ctx->c->solve_count[mode];
 }
 
+const char* fwi_dev_kkt_kernel(const fwi_dev_ctx* ctx, int precision) {
+    if (!ctx) return "";
+    return ctx->c->kkt_kernel[precision == FWI_C64 ? 1 : 0];
+}
+
 void fwi_dev_reset_solve_count(fwi_dev_ctx* ctx, int mode) {
     if (ctx && (mode == FWI_PRECOND_EXACT || mode == FWI_PRECOND_ILU)) ctx->c->solve_count[mode] = 0;
 }

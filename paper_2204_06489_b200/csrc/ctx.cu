@@ -102,6 +102,8 @@ Ctx::~Ctx() {
     if (ilu) ilu_free(ilu);
     for (auto*& p : kplan)
         if (p) kkt_plan_free(p);
+    for (auto*& p : kmplan)
+        if (p) kkt_km_plan_free(p);
     for (auto& e : ev_in)
         if (e) cudaEventDestroy(e);
     for (auto& e : ev_out)
@@ -169,7 +171,7 @@ Ctx* ctx_create(const fwi_state_desc& d) {
     c->ds_stride = (n + 31) / 32 * 32;
     c->vec_len = 4 * int64_t(c->K) * n + c->ds_stride;
     c->precision_mask = d.precision_mask;
-    if (const char* v = std::getenv("FWI_KKT_KERNEL")) c->kkt_variant = std::string(v) == "plain" ? 1 : 0;
+    if (const char* v = std::getenv("FWI_KKT_KERNEL")) c->kkt_variant = std::string(v) == "plain" ? 1 : std::string(v) == "tile" ? 2 : 0;
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     cudaStream_t st = c->stream;
 

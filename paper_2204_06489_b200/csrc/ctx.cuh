@@ -25,6 +25,7 @@ struct ExactFactor;  // exact.cu
 struct IluFactor;    // ilu.cu
 struct GmresWork;    // gmres.cu
 struct KktPlan;      // kkt_tma.cu
+struct KktKmPlan;    // kkt_tma.cu
 
 struct Ctx {
     // geometry / scalars
@@ -58,8 +59,12 @@ struct Ctx {
     IluFactor* ilu = nullptr;      // owned (ilu_free)
     GmresWork* gmres_work = nullptr;  // owned (gmres_work_free): Krylov buffers reused across solves
     int64_t solve_count[2] = {0, 0};
-    KktPlan* kplan[2] = {nullptr, nullptr};  // TMA apply plans (c128, c64), built lazily
-    int kkt_variant = 0;                      // 0: TMA persistent kernel, 1: plain kernel (FWI_KKT_KERNEL=plain)
+    KktPlan* kplan[2] = {nullptr, nullptr};      // tile-TMA apply plans (c128, c64), built lazily
+    KktKmPlan* kmplan[2] = {nullptr, nullptr};   // source-major TMA apply plans (c128, c64), built lazily
+    // 0: source-major TMA kernel (falling back to the tile-TMA kernel, then the plain kernel),
+    // 1: plain kernel (FWI_KKT_KERNEL=plain), 2: tile-TMA kernel (FWI_KKT_KERNEL=tile)
+    int kkt_variant = 0;
+    const char* kkt_kernel[2] = {"", ""};  // K1 kernel of the last apply (c128, c64), fwi_dev_kkt_kernel
     // host copy of the stencil for the ILU factorisation (lazily)
     std::vector<double> h_s;
 
@@ -105,6 +110,7 @@ void kkt_apply_raw(Ctx& c, const double* xi, double* out);  // c128 flat device 
 bool kkt_apply_tma(Ctx& c, bool f32, const void* xi, void* out);
 void kkt_apply_host(Ctx& c, const double* in, double* out);
 void kkt_plan_free(KktPlan*);
+void kkt_km_plan_free(KktKmPlan*);
 
 // ---- vec.cu  (flat device arrays of len doubles; deterministic reductions)
 double dev_dot(Ctx* c, cudaStream_t st, const double* x, const double* y, int64_t len);

@@ -134,7 +134,7 @@ __global__ void kkt_rhs_ds(int64_t n, double neg_eps, const double* __restrict__
 }  // namespace
 
 void kkt_apply_raw(Ctx& c, const double* xi, double* out) {
-    if (c.kkt_variant == 0 && kkt_apply_tma(c, false, xi, out)) return;
+    if (c.kkt_variant != 1 && kkt_apply_tma(c, false, xi, out)) return;
     dim3 blk(32, 8), grd((c.nx + 31) / 32, (c.nz + 7) / 8);
     double* x = const_cast<double*>(xi);
     kkt_apply_kernel<F64><<<grd, blk, 0, c.stream>>>(
@@ -142,6 +142,7 @@ void kkt_apply_raw(Ctx& c, const double* xi, double* out) {
         c.nrec_k.p, c.nrec_w2.p, c.du_of(x), c.ds_of(x), c.la_of(x), c.du_of(out), c.ds_of(out),
         c.la_of(out), 0, c.K, nullptr);
     CK_LAUNCH();
+    c.kkt_kernel[0] = "kkt_apply_kernel<F64> (plain K1, csrc/kkt.cu)";
 }
 
 // kkt_apply on host buffers (the reference's own signature,
@@ -207,7 +208,7 @@ void kkt_apply(Ctx& c, const Vec& xi, Vec& out) {
         return;
     }
     require(c.u32.p != nullptr, "kkt_apply: context was created without the complex64 copy");
-    if (c.kkt_variant == 0 && kkt_apply_tma(c, true, xi.f.p, out.f.p)) return;
+    if (c.kkt_variant != 1 && kkt_apply_tma(c, true, xi.f.p, out.f.p)) return;
     dim3 blk(32, 8), grd((c.nx + 31) / 32, (c.nz + 7) / 8);
     const int64_t kn2 = 2 * int64_t(c.K) * c.n;
     float* x = const_cast<float*>(xi.f.p);
@@ -218,6 +219,7 @@ void kkt_apply(Ctx& c, const Vec& xi, Vec& out) {
         reinterpret_cast<float2*>(x + kn2 + c.ds_stride), reinterpret_cast<float2*>(o), o + kn2,
         reinterpret_cast<float2*>(o + kn2 + c.ds_stride), 0, c.K, nullptr);
     CK_LAUNCH();
+    c.kkt_kernel[1] = "kkt_apply_kernel<F32> (plain K1, csrc/kkt.cu)";
 }
 
 void kkt_rhs(Ctx& c, Vec& out) {

@@ -601,6 +601,301 @@ bool launch(Ctx& c, KktPlan* p, const typename A::T* du, const typename A::R* ds
     FWI_KKT_DISPATCH(p->KC, p->stages, FWI_LAUNCH)
 #undef FWI_LAUNCH
     CK_LAUNCH();
+    c.kkt_kernel[f32 ? 1 : 0] = f32 ? "kkt_tma_kernel<F32> (chunked tile-TMA K1, csrc/kkt_tma.cu)"
+                                    : "kkt_tma_kernel<F64> (chunked tile-TMA K1, csrc/kkt_tma.cu)";
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// Source-major K1 (`kkt_km_kernel`, the default when every CTA's share of the
+// grid fits its threads). The grid is cut into G ~= #SMs rectangles of W <= COLS
+// columns and h or h+1 rows (equal areas to one row), one per CTA, 512 threads
+// = COLS columns x (512/COLS) row slots, two rows per thread. Every CTA walks
+// the K sources in order over its own rectangle, so:
+//  * the ds row's K-sum stays in a register per node (the reference's
+//    sequential sum, bit-identical) — no cross-CTA ordering, no fold;
+//  * the stencil, ds and receiver pointers are loaded once per apply;
+//  * at any moment all SMs read the same few source planes, so the DRAM
+//    stream stays coherent and the halo rows a CTA shares with its neighbours
+//    are L2 hits.
+// Per source one elected thread issues three TMA boxes (du_k, la_k with a
+// one-node halo, u_k) into an S-stage ring, one block barrier per step.
+// ---------------------------------------------------------------------------
+template <class A>
+struct KmArgs {
+    using T = typename A::T;
+    using R = typename A::R;
+    int nx, nz, K, per_strip, W, gr, RP;
+    int64_t n;
+    R w2, eps;
+    const T *diag, *east, *south;
+    const int *nrec_ptr, *nrec_k;
+    const double* nrec_w2;
+    const R* ds;
+    T *odu, *ola;
+    R* ods;
+    int hlo;                          // rectangle heights are hlo or hlo + 1
+    uint32_t hb[2], ub[2], tx[2];     // halo box bytes (128-aligned), u box bytes, stage fill (h = hlo, hlo+1)
+    uint32_t stage_bytes;
+};
+
+template <class A, int COLS, int S>
+__global__ void __launch_bounds__(512, 1)
+    kkt_km_kernel(const __grid_constant__ CUtensorMap tdu0, const __grid_constant__ CUtensorMap tla0,
+                  const __grid_constant__ CUtensorMap tu0, const __grid_constant__ CUtensorMap tdu1,
+                  const __grid_constant__ CUtensorMap tla1, const __grid_constant__ CUtensorMap tu1,
+                  const KmArgs<A> P) {
+    using T = typename A::T;
+    using R = typename A::R;
+    constexpr int kSl = 512 / COLS;  // row slots; a thread owns rows slot and slot + kSl
+    extern __shared__ __align__(1024) unsigned char sm[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + size_t(S) * P.stage_bytes);
+    const int tid = threadIdx.x, lx = tid % COLS, zs = tid / COLS;
+    const int nx = P.nx, nz = P.nz, K = P.K, RP = P.RP;
+    const int64_t n = P.n;
+    // this CTA's rectangle: strip b / per_strip, rows [z0, z1) of it
+    const int strip = blockIdx.x / P.per_strip, i = blockIdx.x % P.per_strip;
+    const int z0 = int(int64_t(i) * nz / P.per_strip), z1 = int(int64_t(i + 1) * nz / P.per_strip);
+    const int hi = (z1 - z0) - P.hlo;  // 0 or 1: which box shape
+    const int x0 = strip * P.W, w = min(P.W, nx - x0), h = z1 - z0;
+    const CUtensorMap* tdu = hi ? &tdu1 : &tdu0;
+    const CUtensorMap* tla = hi ? &tla1 : &tla0;
+    const CUtensorMap* tu = hi ? &tu1 : &tu0;
+    const uint32_t hb = P.hb[hi], tx = P.tx[hi];
+    auto issue = [&](int k) {
+        const int s = k % S;
+        unsigned char* st = sm + size_t(s) * P.stage_bytes;
+        mbar_expect_tx(&bar[s], tx);
+        tma_load_4d(st, tdu, 0, x0 / P.gr - 1, z0 - 1, k, &bar[s]);
+        tma_load_4d(st + hb, tla, 0, x0 / P.gr - 1, z0 - 1, k, &bar[s]);
+        tma_load_4d(st + 2 * hb, tu, 0, x0 / P.gr, z0, k, &bar[s]);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int k = 0; k < S && k < K; ++k) issue(k);
+    }
+    bool act[2], hN[2], hW[2], hE[2], hS[2];
+    T cD[2], cN[2], cW[2], cE[2], cS[2];
+    R dsv[2], pl[2];
+    int qr[2], qe[2];
+    int64_t cnode[2];
+    bool full = true;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int row = zs + kSl * r;
+        act[r] = lx < w && row < h;
+        const int ix = x0 + lx, iz = z0 + row;
+        const int64_t cc = act[r] ? int64_t(iz) * nx + ix : 0;
+        cnode[r] = cc;
+        const bool bnd = on_boundary(ix, iz, nx, nz);
+        hN[r] = act[r] && !bnd && !on_boundary(ix, iz - 1, nx, nz);
+        hW[r] = act[r] && !bnd && !on_boundary(ix - 1, iz, nx, nz);
+        hE[r] = act[r] && !bnd && !on_boundary(ix + 1, iz, nx, nz);
+        hS[r] = act[r] && !bnd && !on_boundary(ix, iz + 1, nx, nz);
+        full = full && act[r] && hN[r] && hW[r] && hE[r] && hS[r];
+        cD[r] = act[r] ? P.diag[cc] : A::zero();
+        cN[r] = hN[r] ? P.south[cc - nx] : A::zero();
+        cW[r] = hW[r] ? P.east[cc - 1] : A::zero();
+        cE[r] = hE[r] ? P.east[cc] : A::zero();
+        cS[r] = hS[r] ? P.south[cc] : A::zero();
+        dsv[r] = act[r] ? P.ds[cc] : R(0);
+        qr[r] = act[r] ? P.nrec_ptr[cc] : 0;
+        qe[r] = act[r] ? P.nrec_ptr[cc + 1] : 0;
+        pl[r] = R(0);
+    }
+    const bool warp_full = __all_sync(0xffffffffu, full);
+    const int UP = P.W;  // u box row pitch (complex)
+    __syncthreads();
+    for (int k = 0; k < K; ++k) {
+        const int s = k % S;
+        mbar_wait(&bar[s], (k / S) & 1);
+        const unsigned char* st = sm + size_t(s) * P.stage_bytes;
+        const T* dus = reinterpret_cast<const T*>(st) + P.gr + lx;
+        const T* las = reinterpret_cast<const T*>(st + hb) + P.gr + lx;
+        const T* us = reinterpret_cast<const T*>(st + 2 * hb) + lx;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int row = zs + kSl * r;
+            if (row >= h) continue;  // CTA-uniform per slot: the rectangle's last rows
+            T s_, t_;
+            const T* dr = dus + (row + 1) * RP;
+            const T* lr = las + (row + 1) * RP;
+            if (warp_full)
+                node_step<A, true>(dr, lr, RP, true, true, true, true, cD[r], cN[r], cW[r], cE[r], cS[r], s_, t_);
+            else
+                node_step<A, false>(dr, lr, RP, hN[r], hW[r], hE[r], hS[r], cD[r], cN[r], cW[r], cE[r], cS[r], s_,
+                                    t_);
+            const T duc = dr[0], lac = lr[0], uc = us[row * UP];
+            pl[r] = A::radd(pl[r], A::re_pconj(P.w2, uc, lac));
+            if (!act[r]) continue;
+            const int64_t o = int64_t(k) * n + cnode[r];
+            st_stream(P.ola + o, A::sub(s_, A::pmul(P.w2, uc, dsv[r])));
+            if (qr[r] < qe[r] && P.nrec_k[qr[r]] == k) {
+                T f = A::zero();
+                while (qr[r] < qe[r] && P.nrec_k[qr[r]] == k) {
+                    f = A::add(f, A::rm(R(P.nrec_w2[qr[r]]), duc));
+                    ++qr[r];
+                }
+                t_ = A::add(f, t_);
+            }
+            st_stream(P.odu + o, t_);
+        }
+        __syncthreads();  // every thread is done with stage s
+        if (tid == 0 && k + S < K) issue(k + S);
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+        if (act[r]) P.ods[cnode[r]] = A::rsub(A::rmulr(P.eps, dsv[r]), pl[r]);
+}
+
+}  // namespace
+
+struct KktKmPlan {
+    bool ok = false;
+    int cols = 128, stages = 0, G = 0, per_strip = 0, W = 0, gr = 8, RP = 0, hlo = 0;
+    uint32_t hb[2] = {0, 0}, ub[2] = {0, 0}, tx[2] = {0, 0}, stage_bytes = 0;
+    size_t smem = 0;
+    CUtensorMap tm_u[2];
+};
+
+void kkt_km_plan_free(KktKmPlan* p) { delete p; }
+
+namespace {
+
+// (COLS, S) instantiations
+#define FWI_KM_DISPATCH(COLSv, Sv, CALL)        \
+    switch (COLSv * 16 + Sv) {                  \
+        case 128 * 16 + 1: CALL(128, 1); break; \
+        case 64 * 16 + 1: CALL(64, 1); break;   \
+        case 32 * 16 + 2: CALL(32, 2); break;   \
+        case 32 * 16 + 3: CALL(32, 3); break;   \
+        case 128 * 16 + 2: CALL(128, 2); break; \
+        case 128 * 16 + 3: CALL(128, 3); break; \
+        case 128 * 16 + 4: CALL(128, 4); break; \
+        case 64 * 16 + 2: CALL(64, 2); break;   \
+        case 64 * 16 + 3: CALL(64, 3); break;   \
+        case 64 * 16 + 4: CALL(64, 4); break;   \
+        default: CALL(64, 6); break;            \
+    }
+
+template <class A>
+KktKmPlan* build_km_plan(Ctx& c, bool f32) {
+    auto p = std::make_unique<KktKmPlan>();
+    const int nx = c.nx, nz = c.nz, K = c.K;
+    const int es = f32 ? 8 : 16;
+    if (nx % 2 != 0 || !encode_fn()) return p.release();
+    const int sms = sm_count();
+    // rectangles: per_strip = SMs / strips per strip, heights <= 2 x (512 / COLS) rows. 64-column
+    // strips (measured best on C2: 128 us per apply against 142 us with 128 columns and 131 us with
+    // 32); the kernel is chosen only when the rectangles have >= 8 rows — shorter ones spend too
+    // much on halo rows, and the chunked tile kernel does as well or better there (config 3).
+    auto shape = [&](int cols, int& nsx, int& per, int& hmax) {
+        nsx = (nx + cols - 1) / cols;
+        per = std::min(sms / nsx, nz);
+        if (per < 1) return false;
+        hmax = (nz + per - 1) / per;
+        return hmax <= 2 * (512 / cols);
+    };
+    int cols = 64, nsx = 0, per = 0, hmax = 0;
+    if (const char* e = std::getenv("FWI_KKT_KM_COLS")) cols = std::atoi(e) == 128 ? 128 : std::atoi(e) == 32 ? 32 : 64;
+    if (!shape(cols, nsx, per, hmax)) return p.release();
+    if (nz / per < 8 && !std::getenv("FWI_KKT_KM_FORCE")) return p.release();
+    const int W = ((nx + nsx - 1) / nsx + 1) / 2 * 2;  // even strip width <= cols
+    if (W > cols) return p.release();
+    int gr = 8;
+    if (const char* e = std::getenv("FWI_KKT_GRP")) gr = std::max(1, std::atoi(e));
+    if (nx % gr != 0 || W % gr != 0) gr = 2;
+    p->cols = cols;
+    p->per_strip = per;
+    p->G = nsx * per;
+    p->W = W;
+    p->gr = gr;
+    p->RP = W + 2 * gr;
+    p->hlo = nz / per;
+    for (int v = 0; v < 2; ++v) {
+        const int h = p->hlo + v;
+        p->hb[v] = align128(size_t(p->RP) * (h + 2) * es);
+        p->ub[v] = align128(size_t(W) * h * es);
+        p->tx[v] = uint32_t(2 * size_t(p->RP) * (h + 2) * es + size_t(W) * h * es);
+        p->stage_bytes = std::max(p->stage_bytes, 2 * p->hb[v] + p->ub[v]);
+    }
+    const size_t budget = 227 * 1024 - 128;
+    // two stages in flight (three for complex64, half the bytes per stage): deeper rings are
+    // measurably slower with the output stores sharing the memory system (C2: 3 stages 181 us,
+    // 4 stages 209 us against 129 us)
+    int st = f32 ? 3 : 2;
+    if (const char* e = std::getenv("FWI_KKT_KM_STAGES")) st = std::atoi(e);
+    auto valid = [&](int v) {
+        return cols == 32 ? (v == 2 || v == 3) : (v >= 1 && v <= 4) || (cols == 64 && v == 6);
+    };
+    while (st > 1 && (!valid(st) || size_t(st) * p->stage_bytes > budget)) --st;
+    if (!valid(st)) return p.release();
+    if (size_t(st) * p->stage_bytes > budget) return p.release();
+    p->stages = st;
+    p->smem = size_t(st) * p->stage_bytes + 128;
+#define FWI_KM_ATTR(COLSc, Sc)                                                                           \
+    CK(cudaFuncSetAttribute(kkt_km_kernel<A, COLSc, Sc>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                            int(p->smem)))
+    FWI_KM_DISPATCH(cols, st, FWI_KM_ATTR);
+#undef FWI_KM_ATTR
+    const void* ubase = f32 ? static_cast<const void*>(c.u32.p) : static_cast<const void*>(c.u.p);
+    for (int v = 0; v < 2; ++v)
+        if (!ubase || !encode(&p->tm_u[v], f32, ubase, nx, nz, K, gr, W / gr, p->hlo + v)) return p.release();
+    p->ok = true;
+    return p.release();
+}
+
+template <class A>
+bool launch_km(Ctx& c, KktKmPlan* p, const typename A::T* du, const typename A::R* ds, const typename A::T* la,
+               typename A::T* odu, typename A::R* ods, typename A::T* ola, bool f32) {
+    CUtensorMap tdu[2], tla[2];
+    for (int v = 0; v < 2; ++v) {
+        if (!encode(&tdu[v], f32, du, c.nx, c.nz, c.K, p->gr, p->RP / p->gr, p->hlo + v + 2)) return false;
+        if (!encode(&tla[v], f32, la, c.nx, c.nz, c.K, p->gr, p->RP / p->gr, p->hlo + v + 2)) return false;
+    }
+    KmArgs<A> a;
+    a.nx = c.nx;
+    a.nz = c.nz;
+    a.K = c.K;
+    a.per_strip = p->per_strip;
+    a.W = p->W;
+    a.gr = p->gr;
+    a.RP = p->RP;
+    a.n = c.n;
+    a.w2 = typename A::R(c.w2);
+    a.eps = typename A::R(c.eps);
+    if (f32) {
+        a.diag = reinterpret_cast<const typename A::T*>(c.diag32.p);
+        a.east = reinterpret_cast<const typename A::T*>(c.east32.p);
+        a.south = reinterpret_cast<const typename A::T*>(c.south32.p);
+    } else {
+        a.diag = reinterpret_cast<const typename A::T*>(c.diag.p);
+        a.east = reinterpret_cast<const typename A::T*>(c.east.p);
+        a.south = reinterpret_cast<const typename A::T*>(c.south.p);
+    }
+    a.nrec_ptr = c.nrec_ptr.p;
+    a.nrec_k = c.nrec_k.p;
+    a.nrec_w2 = c.nrec_w2.p;
+    a.ds = ds;
+    a.odu = odu;
+    a.ola = ola;
+    a.ods = ods;
+    a.hlo = p->hlo;
+    for (int v = 0; v < 2; ++v) {
+        a.hb[v] = p->hb[v];
+        a.ub[v] = p->ub[v];
+        a.tx[v] = p->tx[v];
+    }
+    a.stage_bytes = p->stage_bytes;
+#define FWI_KM_LAUNCH(COLSc, Sc)                                                                          \
+    (kkt_km_kernel<A, COLSc, Sc><<<p->G, 512, p->smem, c.stream>>>(tdu[0], tla[0], p->tm_u[0], tdu[1], tla[1], \
+                                                                  p->tm_u[1], a),                             \
+     c.kkt_kernel[f32 ? 1 : 0] = f32 ? "kkt_km_kernel<F32, " #COLSc ", " #Sc "> (source-major TMA K1, csrc/kkt_tma.cu)" \
+                                    : "kkt_km_kernel<F64, " #COLSc ", " #Sc "> (source-major TMA K1, csrc/kkt_tma.cu)")
+    FWI_KM_DISPATCH(p->cols, p->stages, FWI_KM_LAUNCH);
+#undef FWI_KM_LAUNCH
+    CK_LAUNCH();
     return true;
 }
 
@@ -616,6 +911,27 @@ bool kkt_apply_tma(Ctx& c, bool f32, const void* xi, void* out) {
         if (e && std::atoi(e) == 0) return false;
     }
     if (int64_t(c.K) * c.n < (int64_t(1) << 21) && !std::getenv("FWI_KKT_FORCE_TMA")) return false;
+    const int64_t kn2s = 2 * int64_t(c.K) * c.n;
+    if (c.kkt_variant == 0) {  // source-major kernel first
+        KktKmPlan*& sp = c.kmplan[f32 ? 1 : 0];
+        if (!sp) sp = f32 ? build_km_plan<F32>(c, true) : build_km_plan<F64>(c, false);
+        if (sp->ok) {
+            if (f32) {
+                const float* x = static_cast<const float*>(xi);
+                float* o = static_cast<float*>(out);
+                return launch_km<F32>(c, sp, reinterpret_cast<const float2*>(x), x + kn2s,
+                                      reinterpret_cast<const float2*>(x + kn2s + c.ds_stride),
+                                      reinterpret_cast<float2*>(o), o + kn2s,
+                                      reinterpret_cast<float2*>(o + kn2s + c.ds_stride), true);
+            }
+            const double* x = static_cast<const double*>(xi);
+            double* o = static_cast<double*>(out);
+            return launch_km<F64>(c, sp, reinterpret_cast<const double2*>(x), x + kn2s,
+                                  reinterpret_cast<const double2*>(x + kn2s + c.ds_stride),
+                                  reinterpret_cast<double2*>(o), o + kn2s,
+                                  reinterpret_cast<double2*>(o + kn2s + c.ds_stride), false);
+        }
+    }
     KktPlan*& p = c.kplan[f32 ? 1 : 0];
     if (!p) p = f32 ? build_plan<F32>(c, true) : build_plan<F64>(c, false);
     if (!p->ok) return false;

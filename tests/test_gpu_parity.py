@@ -123,11 +123,18 @@ def test_kkt_apply_c2_parity():
     assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("variant", ["plain", "tma"])
-@pytest.mark.parametrize("mk", PROBLEMS + [lambda: c2_problem(K=5, R=17)])
+@pytest.mark.parametrize("variant", ["plain", "tma", "tile"])
+@pytest.mark.parametrize("mk", PROBLEMS + [lambda: c2_problem(K=5, R=17),
+                                           lambda: small_problem(nx=70, nz=42, n_pml=5, K=3, R=11,
+                                                                 duplicate_receiver=True, seed=7)])
 def test_kkt_apply_kernel_variants_bit_exact(mk, variant, monkeypatch):
-    """Both K1 kernels (TMA-pipelined persistent, plain) reproduce the reference."""
+    """Every K1 kernel (source-major TMA = "tma", the chunked tile-TMA kernel, plain) reproduces
+    the reference; the TMA kernels are forced on these small grids (partial strips and rectangles,
+    duplicate receivers; odd widths fall back to the plain kernel)."""
     monkeypatch.setenv("FWI_KKT_KERNEL", variant)
+    if variant != "plain":
+        monkeypatch.setenv("FWI_KKT_FORCE_TMA", "1")
+        monkeypatch.setenv("FWI_KKT_KM_FORCE", "1")  # source-major kernel even for 1-row rectangles
     p = mk()
     ref, dev = pair_direct(p)
     x = random_kkt(p, 5)
@@ -270,7 +277,9 @@ def test_zero_receivers_converge_in_one_iteration():
     assert log.converged and log.iterations() == 1 and log.final_residual() < 1e-10
 
 
-def test_c64_apply_deviation():
+@pytest.mark.parametrize("variant", ["tma", "tile", "plain"])
+def test_c64_apply_deviation(variant, monkeypatch):
+    monkeypatch.setenv("FWI_KKT_KERNEL", variant)
     p = c2_problem()
     ref = po.Ref(p, full=False, exact=False)
     dev = fw.GnState(p, exact=False, c64=True)
