@@ -706,14 +706,15 @@ __global__ void __launch_bounds__(512, 1)
     }
     const bool warp_full = __all_sync(0xffffffffu, full);
     const int UP = P.W;  // u box row pitch (complex)
+    const int lxs = min(lx, P.W - 1);  // lanes beyond the strip read (and drop) its last column
     __syncthreads();
     for (int k = 0; k < K; ++k) {
         const int s = k % S;
         mbar_wait(&bar[s], (k / S) & 1);
         const unsigned char* st = sm + size_t(s) * P.stage_bytes;
-        const T* dus = reinterpret_cast<const T*>(st) + P.gr + lx;
-        const T* las = reinterpret_cast<const T*>(st + hb) + P.gr + lx;
-        const T* us = reinterpret_cast<const T*>(st + 2 * hb) + lx;
+        const T* dus = reinterpret_cast<const T*>(st) + P.gr + lxs;
+        const T* las = reinterpret_cast<const T*>(st + hb) + P.gr + lxs;
+        const T* us = reinterpret_cast<const T*>(st + 2 * hb) + lxs;
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             const int row = zs + kSl * r;
