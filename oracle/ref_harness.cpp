@@ -20,6 +20,7 @@
 
 #include "fwi/driver.hpp"
 #include "fwi/kkt.hpp"
+#include "fwi/model_io.hpp"
 #include "fwi_b200.h"  // shared plain-C descriptor structs only
 
 using namespace fwi;
@@ -46,6 +47,16 @@ int fail(const std::exception& e) {
     }
     if (dynamic_cast<const std::invalid_argument*>(&e)) return FWI_ERR_INVALID_ARGUMENT;
     return FWI_ERR_NOT_SUPPORTED;
+}
+
+template <class F>
+static int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
 }
 
 Grid2D grid_of(const fwi_grid_desc& g) { return build_grid(g.nx, g.nz, g.h, g.n_pml); }
@@ -464,6 +475,190 @@ int ref_kkt_apply_bench(void* h, const double* in, int nthreads, int napplies, d
         return failed ? FWI_ERR_NOT_SUPPORTED : FWI_OK;
     } catch (const std::exception& e) {
         return fail(e);
+    }
+}
+
+
+// ---- on-disk formats (src/model_io.cpp): the reference's own writers and
+// readers, for parity of paper_2204_06489_b200/model_io.py
+int ref_format_double(double v, char* buf, int cap) {
+    const std::string s = format_double(v);
+    if (int(s.size()) + 1 > cap) return -1;
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return int(s.size());
+}
+
+int ref_write_model(const char* path, int nx, int nz, double h, int n_pml, int kind, const double* values) {
+    return guard([&] {
+        ModelFile m;
+        m.grid = build_grid(nx, nz, h, n_pml);
+        m.kind = kind ? ModelKind::slowness_sq : ModelKind::velocity_mps;
+        m.values.assign(values, values + std::size_t(nx) * nz);
+        write_model(path, m);
+    });
+}
+
+// status: 0 ok, 1 ParseError, 2 IoError, 3 other; header out = nx, nz, n_pml, kind; h; values (cap doubles)
+int ref_read_model(const char* path, int* hdr, double* h, double* values, long cap) {
+    try {
+        const ModelFile m = read_model(path);
+        hdr[0] = m.grid.nx;
+        hdr[1] = m.grid.nz;
+        hdr[2] = m.grid.n_pml;
+        hdr[3] = m.kind == ModelKind::slowness_sq ? 1 : 0;
+        *h = m.grid.h;
+        if (values && long(m.values.size()) <= cap) std::memcpy(values, m.values.data(), m.values.size() * 8);
+        return 0;
+    } catch (const ParseError& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+namespace {
+Survey survey_from(int nf, const double* freqs, int weight_mode, int K, const int* sx, const int* sz,
+                   const double* amp, const int* off, const int* rx, const int* rz) {
+    Survey s;
+    s.frequencies_hz.assign(freqs, freqs + nf);
+    s.weight_mode = weight_mode ? WeightMode::offset : WeightMode::identity;
+    for (int k = 0; k < K; ++k) {
+        Survey::Source src;
+        src.ix = sx[k];
+        src.iz = sz[k];
+        if (amp) src.amplitude = amp[k];
+        for (int j = off[k]; j < off[k + 1]; ++j) src.receivers.emplace_back(rx[j], rz[j]);
+        s.sources.push_back(src);
+    }
+    return s;
+}
+}  // namespace
+
+int ref_write_survey(const char* path, int nf, const double* freqs, int weight_mode, int K, const int* sx,
+                     const int* sz, const double* amp, const int* off, const int* rx, const int* rz) {
+    return guard([&] { write_survey(path, survey_from(nf, freqs, weight_mode, K, sx, sz, amp, off, rx, rz)); });
+}
+
+// counts[0..3] = nf, weight_mode, K, num_data; arrays filled when non-null (capacities from a first call)
+int ref_read_survey(const char* path, int* counts, double* freqs, int* sx, int* sz, double* amp, int* off, int* rx,
+                    int* rz) {
+    try {
+        const Survey s = read_survey(path);
+        counts[0] = int(s.frequencies_hz.size());
+        counts[1] = s.weight_mode == WeightMode::offset ? 1 : 0;
+        counts[2] = s.num_sources();
+        counts[3] = s.num_data();
+        if (freqs) {
+            int j = 0;
+            for (std::size_t i = 0; i < s.frequencies_hz.size(); ++i) freqs[i] = s.frequencies_hz[i];
+            for (int k = 0; k < s.num_sources(); ++k) {
+                sx[k] = s.sources[k].ix;
+                sz[k] = s.sources[k].iz;
+                amp[k] = s.sources[k].amplitude;
+                off[k] = j;
+                for (const auto& [a, b] : s.sources[k].receivers) {
+                    rx[j] = a;
+                    rz[j] = b;
+                    ++j;
+                }
+            }
+            off[s.num_sources()] = j;
+        }
+        return 0;
+    } catch (const ParseError& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+// blocks: nf x num_data complex (re, im)
+int ref_write_data(const char* path, const char* survey_path, const double* blocks) {
+    return guard([&] {
+        const Survey s = read_survey(survey_path);
+        std::vector<DataVector> b(s.frequencies_hz.size());
+        const int nd = s.num_data();
+        for (std::size_t f = 0; f < b.size(); ++f) {
+            b[f].resize(nd);
+            for (int j = 0; j < nd; ++j)
+                b[f][j] = Complex(blocks[2 * (f * nd + j)], blocks[2 * (f * nd + j) + 1]);
+        }
+        write_data(path, s, b);
+    });
+}
+
+int ref_read_data(const char* path, const char* survey_path, double* blocks) {
+    try {
+        const Survey s = read_survey(survey_path);
+        const auto b = read_data(path, s);
+        const int nd = s.num_data();
+        for (std::size_t f = 0; f < b.size(); ++f)
+            for (int j = 0; j < nd; ++j) {
+                blocks[2 * (f * nd + j)] = b[f][j].real();
+                blocks[2 * (f * nd + j) + 1] = b[f][j].imag();
+            }
+        return 0;
+    } catch (const ParseError& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+// FwiConfig fields: d[0..10] = epsilon_start, epsilon_end, inner_tol, ilu_diag_shift, v_min, v_max,
+// ecg_stop_tol, pml_power, pml_c_ref (NaN if unset), pml_sigma_max (NaN if unset), unused;
+// i[0..7] = solver, max_inner, gmres_restart, ilu_level, drop_reg_term, weight_mode (-1 unset),
+// ecg_stride, nfreq; i[8] = neps; freqs / eps (capacity 64 each)
+int ref_read_config(const char* path, double* d, int* i, double* freqs, double* eps) {
+    try {
+        const FwiConfig c = read_config(path);
+        const double nan = std::nan("");
+        d[0] = c.epsilon_start;
+        d[1] = c.epsilon_end;
+        d[2] = c.inner_tol;
+        d[3] = c.ilu_diag_shift;
+        d[4] = c.v_min;
+        d[5] = c.v_max;
+        d[6] = c.ecg_stop_tol;
+        d[7] = c.pml_power;
+        d[8] = c.pml_c_ref.value_or(nan);
+        d[9] = c.pml_sigma_max.value_or(nan);
+        i[0] = int(c.solver);
+        i[1] = c.max_inner;
+        i[2] = c.gmres_restart;
+        i[3] = c.ilu_level;
+        i[4] = c.drop_reg_term ? 1 : 0;
+        i[5] = c.weight_mode ? (*c.weight_mode == WeightMode::offset ? 1 : 0) : -1;
+        i[6] = c.ecg_stride;
+        i[7] = int(c.frequencies_hz.size());
+        i[8] = int(c.epsilon_list.size());
+        for (std::size_t k = 0; k < c.frequencies_hz.size() && k < 64; ++k) freqs[k] = c.frequencies_hz[k];
+        for (std::size_t k = 0; k < c.epsilon_list.size() && k < 64; ++k) eps[k] = c.epsilon_list[k];
+        return 0;
+    } catch (const ParseError& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
     }
 }
 
