@@ -637,7 +637,26 @@ struct KmArgs {
     int hlo;                          // rectangle heights are hlo or hlo + 1
     uint32_t hb[2], ub[2], tx[2];     // halo box bytes (128-aligned), u box bytes, stage fill (h = hlo, hlo+1)
     uint32_t stage_bytes;
+    const T* u;                       // u through registers instead of a TMA box (ul = 1)
+    int ul;
 };
+
+// u_k at one node, read once: non-coherent, no L1 allocation (the L1 space is what
+// keeps the TMA loads in flight)
+template <class T>
+__device__ __forceinline__ T ldg_na(const T* p);
+template <>
+__device__ __forceinline__ double2 ldg_na<double2>(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+template <>
+__device__ __forceinline__ float2 ldg_na<float2>(const float2* p) {
+    float2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return v;
+}
 
 template <class A, int COLS, int S>
 __global__ void __launch_bounds__(512, 1)
@@ -668,7 +687,7 @@ __global__ void __launch_bounds__(512, 1)
         mbar_expect_tx(&bar[s], tx);
         tma_load_4d(st, tdu, 0, x0 / P.gr - 1, z0 - 1, k, &bar[s]);
         tma_load_4d(st + hb, tla, 0, x0 / P.gr - 1, z0 - 1, k, &bar[s]);
-        tma_load_4d(st + 2 * hb, tu, 0, x0 / P.gr, z0, k, &bar[s]);
+        if (!P.ul) tma_load_4d(st + 2 * hb, tu, 0, x0 / P.gr, z0, k, &bar[s]);
     };
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
@@ -707,8 +726,18 @@ __global__ void __launch_bounds__(512, 1)
     const bool warp_full = __all_sync(0xffffffffu, full);
     const int UP = P.W;  // u box row pitch (complex)
     const int lxs = min(lx, P.W - 1);  // lanes beyond the strip read (and drop) its last column
+    T un[2] = {A::zero(), A::zero()};  // ul: u_k of the next step, loaded one step ahead
+    if (P.ul)
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+            if (act[r]) un[r] = ldg_na(P.u + cnode[r]);
     __syncthreads();
     for (int k = 0; k < K; ++k) {
+        T ucur[2] = {un[0], un[1]};
+        if (P.ul && k + 1 < K)
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+                if (act[r]) un[r] = ldg_na(P.u + int64_t(k + 1) * n + cnode[r]);
         const int s = k % S;
         mbar_wait(&bar[s], (k / S) & 1);
         const unsigned char* st = sm + size_t(s) * P.stage_bytes;
@@ -727,7 +756,7 @@ __global__ void __launch_bounds__(512, 1)
             else
                 node_step<A, false>(dr, lr, RP, hN[r], hW[r], hE[r], hS[r], cD[r], cN[r], cW[r], cE[r], cS[r], s_,
                                     t_);
-            const T duc = dr[0], lac = lr[0], uc = us[row * UP];
+            const T duc = dr[0], lac = lr[0], uc = P.ul ? ucur[r] : us[row * UP];
             pl[r] = A::radd(pl[r], A::re_pconj(P.w2, uc, lac));
             if (!act[r]) continue;
             const int64_t o = int64_t(k) * n + cnode[r];
@@ -754,7 +783,7 @@ __global__ void __launch_bounds__(512, 1)
 
 struct KktKmPlan {
     bool ok = false;
-    int cols = 128, stages = 0, G = 0, per_strip = 0, W = 0, gr = 8, RP = 0, hlo = 0;
+    int cols = 128, stages = 0, G = 0, per_strip = 0, W = 0, gr = 8, RP = 0, hlo = 0, ul = 1;
     uint32_t hb[2] = {0, 0}, ub[2] = {0, 0}, tx[2] = {0, 0}, stage_bytes = 0;
     size_t smem = 0;
     CUtensorMap tm_u[2];
@@ -814,11 +843,16 @@ KktKmPlan* build_km_plan(Ctx& c, bool f32) {
     p->gr = gr;
     p->RP = W + 2 * gr;
     p->hlo = nz / per;
+    // u through registers (non-allocating loads) rather than a third TMA box: shared memory is
+    // carved out of the L1, and the L1 space is what keeps the TMA loads in flight (unused extra
+    // shared memory alone slows the C2 apply: +30 KB 128 -> 140 us, +60 KB 154 us)
+    p->ul = 1;
+    if (const char* e = std::getenv("FWI_KKT_KM_ULDG")) p->ul = std::atoi(e) != 0;
     for (int v = 0; v < 2; ++v) {
         const int h = p->hlo + v;
         p->hb[v] = align128(size_t(p->RP) * (h + 2) * es);
-        p->ub[v] = align128(size_t(W) * h * es);
-        p->tx[v] = uint32_t(2 * size_t(p->RP) * (h + 2) * es + size_t(W) * h * es);
+        p->ub[v] = p->ul ? 0 : align128(size_t(W) * h * es);
+        p->tx[v] = uint32_t(2 * size_t(p->RP) * (h + 2) * es + (p->ul ? 0 : size_t(W) * h * es));
         p->stage_bytes = std::max(p->stage_bytes, 2 * p->hb[v] + p->ub[v]);
     }
     const size_t budget = 227 * 1024 - 128;
@@ -835,6 +869,8 @@ KktKmPlan* build_km_plan(Ctx& c, bool f32) {
     if (size_t(st) * p->stage_bytes > budget) return p.release();
     p->stages = st;
     p->smem = size_t(st) * p->stage_bytes + 128;
+    if (const char* e = std::getenv("FWI_KKT_KM_PAD_KB"))  // diagnostics: unused extra shared memory
+        p->smem = std::min<size_t>(227 * 1024, p->smem + size_t(std::atoi(e)) * 1024);
 #define FWI_KM_ATTR(COLSc, Sc)                                                                           \
     CK(cudaFuncSetAttribute(kkt_km_kernel<A, COLSc, Sc>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                             int(p->smem)))
@@ -889,6 +925,9 @@ bool launch_km(Ctx& c, KktKmPlan* p, const typename A::T* du, const typename A::
         a.tx[v] = p->tx[v];
     }
     a.stage_bytes = p->stage_bytes;
+    a.ul = p->ul;
+    a.u = reinterpret_cast<const typename A::T*>(f32 ? static_cast<const void*>(c.u32.p)
+                                                    : static_cast<const void*>(c.u.p));
 #define FWI_KM_LAUNCH(COLSc, Sc)                                                                          \
     (kkt_km_kernel<A, COLSc, Sc><<<p->G, 512, p->smem, c.stream>>>(tdu[0], tla[0], p->tm_u[0], tdu[1], tla[1], \
                                                                   p->tm_u[1], a),                             \
