@@ -1,7 +1,4 @@
-# Source-major K1 on C2: u via registers (default) vs a third TMA box; ring depth
-timeout 120 python tools/apply_sizes.py c2
-FWI_KKT_KM_ULDG=0 timeout 120 python tools/apply_sizes.py c2
-FWI_KKT_KM_STAGES=3 timeout 120 python tools/apply_sizes.py c2
-FWI_KKT_GRP=4 timeout 120 python tools/apply_sizes.py c2
-timeout 200 python bench.py --skip-cpu --skip-krylov --steps 300 | python -c "import json,sys; d=json.load(sys.stdin); print('bench', d['ms_per_step'], d['roofline']['frac'], d['c64'])"
-FWI_KKT_KM_STAGES=2 timeout 200 python bench.py --skip-cpu --skip-krylov --steps 300 | python -c "import json,sys; d=json.load(sys.stdin); print('bench c64 S=2', d['c64'])"
+# Source-major K1: complex64 sources per stage x ring depth (bench c64 line); complex128 default
+for sps in 2 1; do for st in 2 3; do
+  FWI_KKT_KM_SPS=$sps FWI_KKT_KM_STAGES=$st timeout 200 python bench.py --skip-cpu --skip-krylov --steps 300 | python -c "import json,sys; d=json.load(sys.stdin); print('sps=$sps S=$st', round(d['ms_per_step'],4), round(d['roofline']['frac'],3), round(d['c64']['ms_per_apply'],4), round(d['c64']['frac'],3), d['c64']['kernel'][:40])"
+done; done
