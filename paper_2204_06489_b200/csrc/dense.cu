@@ -449,7 +449,9 @@ constexpr int zgemm_pipe_smem() {
     return kPStages * (BM * kPPitchK + (BT ? kPBN * kPPitchK : kPBK * kPPitchN)) * 16;
 }
 
-template <int BM, bool BT>
+// G3: Gauss's three-product form, S = (Ar+Ai)(Br+Bi): real = P - Q, imag = S - P - Q
+// (3 DMMA per complex k-step instead of 4; operand sums formed as the fragments load)
+template <int BM, bool BT, bool G3>
 __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, double alpha,
                                                          const double2* __restrict__ A, int64_t lda,
                                                          const double2* __restrict__ B, int64_t ldb,
@@ -505,13 +507,19 @@ __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, do
         const double2* As = psm + (kt % kPStages) * (ASZ + BSZ);
         const double2* Bs = As + ASZ;
         double2 fa[2][TM], fb[2][2];
+        double sa[2][TM], sb[2][2];  // G3 operand sums
         auto frag = [&](int buf, int ks) {
 #pragma unroll
-            for (int t = 0; t < TM; ++t) fa[buf][t] = As[(wm * (BM / 2) + t * 8 + g) * kPPitchK + ks + t4];
+            for (int t = 0; t < TM; ++t) {
+                fa[buf][t] = As[(wm * (BM / 2) + t * 8 + g) * kPPitchK + ks + t4];
+                if (G3) sa[buf][t] = fa[buf][t].x + fa[buf][t].y;
+            }
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
+            for (int u = 0; u < 2; ++u) {
                 fb[buf][u] = BT ? Bs[(wn * 16 + u * 8 + g) * kPPitchK + ks + t4]
                                 : Bs[(ks + t4) * kPPitchN + wn * 16 + u * 8 + g];
+                if (G3) sb[buf][u] = fb[buf][u].x + fb[buf][u].y;
+            }
         };
         frag(0, 0);
 #pragma unroll
@@ -524,8 +532,12 @@ __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, do
                 for (int u = 0; u < 2; ++u) {
                     dmma(P[t][u], fa[cur][t].x, fb[cur][u].x);
                     dmma(Q[t][u], fa[cur][t].y, fb[cur][u].y);
-                    dmma(I[t][u], fa[cur][t].x, fb[cur][u].y);
-                    dmma(I[t][u], fa[cur][t].y, fb[cur][u].x);
+                    if (G3) {
+                        dmma(I[t][u], sa[cur][t], sb[cur][u]);
+                    } else {
+                        dmma(I[t][u], fa[cur][t].x, fb[cur][u].y);
+                        dmma(I[t][u], fa[cur][t].y, fb[cur][u].x);
+                    }
                 }
         }
     }
@@ -538,7 +550,8 @@ __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, do
             for (int e = 0; e < 2; ++e) {
                 const int m = m0 + wm * (BM / 2) + t * 8 + g, n = n0 + wn * 16 + u * 8 + 2 * t4 + e;
                 if (m >= M || n >= N) continue;
-                double2 v = make_double2(alpha * (P[t][u][e] - Q[t][u][e]), alpha * I[t][u][e]);
+                const double im = G3 ? I[t][u][e] - P[t][u][e] - Q[t][u][e] : I[t][u][e];
+                double2 v = make_double2(alpha * (P[t][u][e] - Q[t][u][e]), alpha * im);
                 if (C0) {
                     const double2 c = C0[int64_t(m) * ldc0 + n];
                     v.x += c.x;
@@ -548,16 +561,16 @@ __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, do
             }
 }
 
-template <int BM, bool BT>
+template <int BM, bool BT, bool G3>
 void zgemm_pipe_launch(cudaStream_t st, int M, int N, int K, double alpha, const double2* A, int64_t lda,
                        const double2* B, int64_t ldb, const double2* C0, int64_t ldc0, double2* C, int64_t ldc) {
     constexpr int smem = zgemm_pipe_smem<BM, BT>();
     static bool attr = false;
     if (!attr) {
-        CK(cudaFuncSetAttribute(zgemm_pipe_kernel<BM, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CK(cudaFuncSetAttribute(zgemm_pipe_kernel<BM, BT, G3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
     }
-    zgemm_pipe_kernel<BM, BT><<<dim3((N + kPBN - 1) / kPBN, (M + BM - 1) / BM), 256, smem, st>>>(
+    zgemm_pipe_kernel<BM, BT, G3><<<dim3((N + kPBN - 1) / kPBN, (M + BM - 1) / BM), 256, smem, st>>>(
         M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
     CK_LAUNCH();
 }
@@ -565,20 +578,29 @@ void zgemm_pipe_launch(cudaStream_t st, int M, int N, int K, double alpha, const
 template <bool BT>
 void cgemm_launch(cudaStream_t st, int M, int N, int K, double alpha, const double2* A, int64_t lda,
                   const double2* B, int64_t ldb, const double2* C0, int64_t ldc0, double2* C, int64_t ldc) {
-    // FWI_CGEMM: "pipe" (default), "dmma" (the unpipelined DMMA kernel), "simt"
+    // FWI_CGEMM: "pipe3" (default: Gauss's 3-product form, 3 DMMA per complex k-step; sweep shape
+    // 85.5 -> 78.4 us, 1024^3 27.4 -> 32.2 TFLOP/s, relative error 1.9e-15 against 1.7e-15),
+    // "pipe" (4-product form), "dmma" (the unpipelined DMMA kernel), "simt"
     static const int variant = [] {
         const char* e = std::getenv("FWI_CGEMM");
-        if (!e) return 0;
+        if (!e) return 3;
         const std::string v(e);
-        return v == "simt" ? 2 : v == "dmma" ? 1 : 0;
+        return v == "simt" ? 2 : v == "dmma" ? 1 : v == "pipe" ? 0 : 3;
     }();
-    if (variant == 0) {
+    if (variant == 0 || variant == 3) {
         // 64-row tiles only when they still give every SM a tile
         const int tiles64 = ((N + kPBN - 1) / kPBN) * ((M + 63) / 64);
+        if (variant == 3) {
+            if (tiles64 >= sm_count())
+                zgemm_pipe_launch<64, BT, true>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
+            else
+                zgemm_pipe_launch<32, BT, true>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
+            return;
+        }
         if (tiles64 >= sm_count())
-            zgemm_pipe_launch<64, BT>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
+            zgemm_pipe_launch<64, BT, false>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
         else
-            zgemm_pipe_launch<32, BT>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
+            zgemm_pipe_launch<32, BT, false>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
         return;
     }
     if (variant == 1) {
