@@ -118,7 +118,14 @@ struct TmaArgs {
 template <class T>
 __device__ __forceinline__ void st_stream(T* p, T v);
 template <>
-__device__ __forceinline__ void st_stream<double2>(double2* p, double2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream<double2>(double2* p, double2 v) {
+#ifdef FWI_TILE_STCS
+    __stcs(p, v);
+#else
+    // not allocated in the L1 (the chunked kernel's shared memory leaves little of it)
+    asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+#endif
+}
 template <>
 __device__ __forceinline__ void st_stream<float2>(float2* p, float2 v) { __stcs(p, v); }
 
