@@ -142,8 +142,18 @@ __device__ __forceinline__ double2 ld_hint(const double2* p, uint64_t pol) {
     return v;
 }
 __device__ __forceinline__ void st_hint(double2* p, double2 v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
+                 "l"(pol)
                  : "memory");
+}
+// streamed once: no L1 allocation (stores allocating in the L1 cost bandwidth on this part)
+__device__ __forceinline__ void st_na(double2* p, double2 v) {
+    asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ double2 ld_na(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
 }
 
 template <bool HINT = false>
@@ -333,14 +343,14 @@ __global__ void multi_axpy_kernel(double2* __restrict__ out, const double2* __re
                                   int64_t m) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
          i += int64_t(gridDim.x) * blockDim.x) {
-        double2 acc = x ? x[i] : make_double2(0.0, 0.0);
+        double2 acc = x ? ld_na(x + i) : make_double2(0.0, 0.0);
         for (int j = 0; j < mvec; ++j) {
             const double yj = y[j];
-            const double2 v = args.v[j][i];
+            const double2 v = ld_na(args.v[j] + i);
             acc.x = __dadd_rn(acc.x, __dmul_rn(yj, v.x));
             acc.y = __dadd_rn(acc.y, __dmul_rn(yj, v.y));
         }
-        out[i] = acc;
+        st_na(out + i, acc);
     }
 }
 
