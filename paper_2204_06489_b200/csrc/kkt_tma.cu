@@ -632,7 +632,7 @@ template <class A>
 struct KmArgs {
     using T = typename A::T;
     using R = typename A::R;
-    int nx, nz, K, per_strip, W, gr, RP;
+    int nx, nz, K, per_strip, W, gr, RP, nbands;
     int64_t n;
     R w2, eps;
     const T *diag, *east, *south;
@@ -689,9 +689,11 @@ __device__ __forceinline__ float2 ldg_na<float2>(const float2* p) {
     return v;
 }
 
+// One band per CTA (config 2): the single-band form of kkt_km_kernel below, kept separate because
+// the band loop costs it ~2.5 % (127.5 against 124.5 us on config 2)
 template <class A, int COLS, int S>
 __global__ void __launch_bounds__(512, 1)
-    kkt_km_kernel(const __grid_constant__ CUtensorMap tdu0, const __grid_constant__ CUtensorMap tla0,
+    kkt_km1_kernel(const __grid_constant__ CUtensorMap tdu0, const __grid_constant__ CUtensorMap tla0,
                   const __grid_constant__ CUtensorMap tu0, const __grid_constant__ CUtensorMap tdu1,
                   const __grid_constant__ CUtensorMap tla1, const __grid_constant__ CUtensorMap tu1,
                   const KmArgs<A> P) {
@@ -810,11 +812,161 @@ __global__ void __launch_bounds__(512, 1)
         if (act[r]) P.ods[cnode[r]] = A::rsub(A::rmulr(P.eps, dsv[r]), pl[r]);
 }
 
+template <class A, int COLS, int S, bool MB>
+__global__ void __launch_bounds__(512, 1)
+    kkt_km_kernel(const __grid_constant__ CUtensorMap tdu0, const __grid_constant__ CUtensorMap tla0,
+                  const __grid_constant__ CUtensorMap tu0, const __grid_constant__ CUtensorMap tdu1,
+                  const __grid_constant__ CUtensorMap tla1, const __grid_constant__ CUtensorMap tu1,
+                  const KmArgs<A> P) {
+    using T = typename A::T;
+    using R = typename A::R;
+    constexpr int kSl = 512 / COLS;  // row slots; a thread owns rows slot and slot + kSl
+    extern __shared__ __align__(1024) unsigned char sm[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + size_t(S) * P.stage_bytes);
+    const int tid = threadIdx.x, lx = tid % COLS, zs = tid / COLS;
+    const int nx = P.nx, nz = P.nz, K = P.K, RP = P.RP;
+    const int64_t n = P.n;
+    // bands of this CTA: q = blockIdx.x + j * gridDim.x, band q = strip q / per_strip, rows
+    // [z0, z1) of it; one band per CTA when the grid is small enough (config 2), several otherwise
+    const int nmine = MB ? (P.nbands - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x) : 1;
+    const int64_t nsteps = int64_t(nmine) * K;
+    struct Band {
+        int x0, w, z0, h, hi;
+    };
+    auto band = [&](int j) {
+        const int q = int(blockIdx.x) + j * int(gridDim.x);
+        const int strip = q / P.per_strip, i = q % P.per_strip;
+        Band bd;
+        bd.z0 = int(int64_t(i) * nz / P.per_strip);
+        bd.h = int(int64_t(i + 1) * nz / P.per_strip) - bd.z0;
+        bd.hi = bd.h - P.hlo;  // 0 or 1: which box shape
+        bd.x0 = strip * P.W;
+        bd.w = min(P.W, nx - bd.x0);
+        return bd;
+    };
+    // producer state (thread 0): the next step to issue, walked in order
+    int ij = 0, ik = 0, is = 0;
+    Band ib = band(0);
+    auto issue_next = [&]() {
+        unsigned char* st = sm + size_t(is) * P.stage_bytes;
+        const uint32_t hbi = P.hb[ib.hi];
+        mbar_expect_tx(&bar[is], P.tx[ib.hi]);
+        tma_load_4d(st, ib.hi ? &tdu1 : &tdu0, 0, ib.x0 / P.gr - 1, ib.z0 - 1, ik, &bar[is]);
+        tma_load_4d(st + hbi, ib.hi ? &tla1 : &tla0, 0, ib.x0 / P.gr - 1, ib.z0 - 1, ik, &bar[is]);
+        if (!P.ul) tma_load_4d(st + 2 * hbi, ib.hi ? &tu1 : &tu0, 0, ib.x0 / P.gr, ib.z0, ik, &bar[is]);
+        is = is + 1 == S ? 0 : is + 1;
+        if (++ik == K) {
+            ik = 0;
+            if (++ij < nmine) ib = band(ij);
+        }
+    };
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int64_t g = 0; g < S && g < nsteps; ++g) issue_next();
+    }
+    int cs = 0;        // consumer: stage of the next step
+    uint32_t cph = 0;  // and its phase
+    __syncthreads();
+    const int UP = P.W;                // u box row pitch (complex)
+    const int lxs = min(lx, P.W - 1);  // lanes beyond the strip read (and drop) its last column
+    for (int j = 0; j < nmine; ++j) {
+        const Band bd = band(j);
+        const int x0 = bd.x0, w = bd.w, z0 = bd.z0, h = bd.h;
+        const uint32_t hb = P.hb[bd.hi];
+        bool act[2], hN[2], hW[2], hE[2], hS[2];
+        T cD[2], cN[2], cW[2], cE[2], cS[2];
+        R dsv[2], pl[2];
+        int qr[2], qe[2];
+        int64_t cnode[2];
+        bool full = true;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int row = zs + kSl * r;
+            act[r] = lx < w && row < h;
+            const int ix = x0 + lx, iz = z0 + row;
+            const int64_t cc = act[r] ? int64_t(iz) * nx + ix : 0;
+            cnode[r] = cc;
+            const bool bnd = on_boundary(ix, iz, nx, nz);
+            hN[r] = act[r] && !bnd && !on_boundary(ix, iz - 1, nx, nz);
+            hW[r] = act[r] && !bnd && !on_boundary(ix - 1, iz, nx, nz);
+            hE[r] = act[r] && !bnd && !on_boundary(ix + 1, iz, nx, nz);
+            hS[r] = act[r] && !bnd && !on_boundary(ix, iz + 1, nx, nz);
+            full = full && act[r] && hN[r] && hW[r] && hE[r] && hS[r];
+            cD[r] = act[r] ? P.diag[cc] : A::zero();
+            cN[r] = hN[r] ? P.south[cc - nx] : A::zero();
+            cW[r] = hW[r] ? P.east[cc - 1] : A::zero();
+            cE[r] = hE[r] ? P.east[cc] : A::zero();
+            cS[r] = hS[r] ? P.south[cc] : A::zero();
+            dsv[r] = act[r] ? P.ds[cc] : R(0);
+            qr[r] = act[r] ? P.nrec_ptr[cc] : 0;
+            qe[r] = act[r] ? P.nrec_ptr[cc + 1] : 0;
+            pl[r] = R(0);
+        }
+        const bool warp_full = __all_sync(0xffffffffu, full);
+        T un[2] = {A::zero(), A::zero()};  // ul: u_k of the next step, loaded one step ahead
+        if (P.ul)
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+                if (act[r]) un[r] = ldg_na(P.u + cnode[r]);
+        for (int k = 0; k < K; ++k) {
+            T ucur[2] = {un[0], un[1]};
+            if (P.ul && k + 1 < K)
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+                    if (act[r]) un[r] = ldg_na(P.u + int64_t(k + 1) * n + cnode[r]);
+            const int64_t g = int64_t(j) * K + k;
+            const int s = cs;
+            mbar_wait(&bar[s], cph);
+            if (++cs == S) {
+                cs = 0;
+                cph ^= 1u;
+            }
+            const unsigned char* st = sm + size_t(s) * P.stage_bytes;
+            const T* dus = reinterpret_cast<const T*>(st) + P.gr + lxs;
+            const T* las = reinterpret_cast<const T*>(st + hb) + P.gr + lxs;
+            const T* us = reinterpret_cast<const T*>(st + 2 * hb) + lxs;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int row = zs + kSl * r;
+            if (row >= h) continue;  // CTA-uniform per slot: the rectangle's last rows
+            T s_, t_;
+            const T* dr = dus + (row + 1) * RP;
+            const T* lr = las + (row + 1) * RP;
+            if (warp_full)
+                node_step<A, true>(dr, lr, RP, true, true, true, true, cD[r], cN[r], cW[r], cE[r], cS[r], s_, t_);
+            else
+                node_step<A, false>(dr, lr, RP, hN[r], hW[r], hE[r], hS[r], cD[r], cN[r], cW[r], cE[r], cS[r], s_,
+                                    t_);
+            const T duc = dr[0], lac = lr[0], uc = P.ul ? ucur[r] : us[row * UP];
+            pl[r] = A::radd(pl[r], A::re_pconj(P.w2, uc, lac));
+            if (!act[r]) continue;
+            const int64_t o = int64_t(k) * n + cnode[r];
+            st_mode(P.ola + o, A::sub(s_, A::pmul(P.w2, uc, dsv[r])), P.stmode);
+            if (qr[r] < qe[r] && P.nrec_k[qr[r]] == k) {
+                T f = A::zero();
+                while (qr[r] < qe[r] && P.nrec_k[qr[r]] == k) {
+                    f = A::add(f, A::rm(R(P.nrec_w2[qr[r]]), duc));
+                    ++qr[r];
+                }
+                t_ = A::add(f, t_);
+            }
+            st_mode(P.odu + o, t_, P.stmode);
+        }
+            __syncthreads();  // every thread is done with stage s
+            if (tid == 0 && g + S < nsteps) issue_next();
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+            if (act[r]) P.ods[cnode[r]] = A::rsub(A::rmulr(P.eps, dsv[r]), pl[r]);
+    }
+}
+
 }  // namespace
 
 struct KktKmPlan {
     bool ok = false;
-    int cols = 128, stages = 0, G = 0, per_strip = 0, W = 0, gr = 8, RP = 0, hlo = 0, ul = 1;
+    int cols = 128, stages = 0, G = 0, per_strip = 0, W = 0, gr = 8, RP = 0, hlo = 0, ul = 1, nbands = 0;
     uint32_t hb[2] = {0, 0}, ub[2] = {0, 0}, tx[2] = {0, 0}, stage_bytes = 0;
     size_t smem = 0;
     CUtensorMap tm_u[2];
@@ -824,20 +976,18 @@ void kkt_km_plan_free(KktKmPlan* p) { delete p; }
 
 namespace {
 
-// (COLS, S) instantiations
-#define FWI_KM_DISPATCH(COLSv, Sv, CALL)        \
-    switch (COLSv * 16 + Sv) {                  \
-        case 128 * 16 + 1: CALL(128, 1); break; \
-        case 64 * 16 + 1: CALL(64, 1); break;   \
-        case 32 * 16 + 2: CALL(32, 2); break;   \
-        case 32 * 16 + 3: CALL(32, 3); break;   \
-        case 128 * 16 + 2: CALL(128, 2); break; \
-        case 128 * 16 + 3: CALL(128, 3); break; \
-        case 128 * 16 + 4: CALL(128, 4); break; \
-        case 64 * 16 + 2: CALL(64, 2); break;   \
-        case 64 * 16 + 3: CALL(64, 3); break;   \
-        case 64 * 16 + 4: CALL(64, 4); break;   \
-        default: CALL(64, 6); break;            \
+// (COLS, S, MB) instantiations; MB: several bands per CTA
+#define FWI_KM_DISPATCH(COLSv, Sv, MBv, CALL)                \
+    switch ((COLSv * 16 + Sv) * 2 + (MBv)) {                 \
+        case (128 * 16 + 2) * 2: CALL(128, 2, false); break; \
+        case (128 * 16 + 3) * 2: CALL(128, 3, false); break; \
+        case (64 * 16 + 3) * 2: CALL(64, 3, false); break;   \
+        case (64 * 16 + 4) * 2: CALL(64, 4, false); break;   \
+        case (32 * 16 + 2) * 2: CALL(32, 2, false); break;   \
+        case (32 * 16 + 3) * 2: CALL(32, 3, false); break;   \
+        case (64 * 16 + 2) * 2 + 1: CALL(64, 2, true); break; \
+        case (64 * 16 + 3) * 2 + 1: CALL(64, 3, true); break; \
+        default: CALL(64, 2, false); break;                  \
     }
 
 template <class A>
@@ -851,16 +1001,20 @@ KktKmPlan* build_km_plan(Ctx& c, bool f32) {
     // strips (measured best on C2: 128 us per apply against 142 us with 128 columns and 131 us with
     // 32); the kernel is chosen only when the rectangles have >= 8 rows — shorter ones spend too
     // much on halo rows, and the chunked tile kernel does as well or better there (config 3).
-    auto shape = [&](int cols, int& nsx, int& per, int& hmax) {
-        nsx = (nx + cols - 1) / cols;
-        per = std::min(sms / nsx, nz);
-        if (per < 1) return false;
-        hmax = (nz + per - 1) / per;
-        return hmax <= 2 * (512 / cols);
-    };
-    int cols = 64, nsx = 0, per = 0, hmax = 0;
+    // One band per CTA when every SM's share fits a band of <= 2 x 512/COLS rows (config 2: 8
+    // strips x 18 bands of 14-15 rows); otherwise bands of ~15 rows, several per CTA, each walked
+    // over all sources (config 5: 32 strips x 69 bands on 148 CTAs). FWI_KKT_KM_ROWS sets the band
+    // height (tests: several bands per CTA on small grids).
+    int cols = 64;
     if (const char* e = std::getenv("FWI_KKT_KM_COLS")) cols = std::atoi(e) == 128 ? 128 : std::atoi(e) == 32 ? 32 : 64;
-    if (!shape(cols, nsx, per, hmax)) return p.release();
+    const int maxrows = 2 * (512 / cols);
+    const int nsx = (nx + cols - 1) / cols;
+    int per = std::min(sms / nsx, nz);
+    if (per < 1 || (nz + per - 1) / per > maxrows) per = (nz + 14) / 15;
+    if (const char* e = std::getenv("FWI_KKT_KM_ROWS")) per = (nz + std::max(1, std::atoi(e)) - 1) / std::max(1, std::atoi(e));
+    per = std::max(1, std::min(per, nz));
+    const int hmax = (nz + per - 1) / per;
+    if (hmax > maxrows) return p.release();
     if (nz / per < 8 && !std::getenv("FWI_KKT_KM_FORCE")) return p.release();
     const int W = ((nx + nsx - 1) / nsx + 1) / 2 * 2;  // even strip width <= cols
     if (W > cols) return p.release();
@@ -869,7 +1023,9 @@ KktKmPlan* build_km_plan(Ctx& c, bool f32) {
     if (nx % gr != 0 || W % gr != 0) gr = 2;
     p->cols = cols;
     p->per_strip = per;
-    p->G = nsx * per;
+    p->nbands = nsx * per;
+    p->G = std::min(sms, p->nbands);
+    if (const char* e = std::getenv("FWI_KKT_KM_G")) p->G = std::max(1, std::min(p->G, std::atoi(e)));  // tests
     p->W = W;
     p->gr = gr;
     p->RP = W + 2 * gr;
@@ -892,20 +1048,24 @@ KktKmPlan* build_km_plan(Ctx& c, bool f32) {
     // 4 stages 209 us against 129 us)
     int st = f32 ? 3 : 2;
     if (const char* e = std::getenv("FWI_KKT_KM_STAGES")) st = std::atoi(e);
+    const bool mb = p->G < p->nbands;
     auto valid = [&](int v) {
-        return cols == 32 ? (v == 2 || v == 3) : (v >= 1 && v <= 4) || (cols == 64 && v == 6);
+        if (mb) return cols == 64 && (v == 2 || v == 3);
+        return cols == 32 ? (v == 2 || v == 3) : cols == 128 ? (v == 2 || v == 3) : (v >= 2 && v <= 4);
     };
-    while (st > 1 && (!valid(st) || size_t(st) * p->stage_bytes > budget)) --st;
+    while (st > 2 && (!valid(st) || size_t(st) * p->stage_bytes > budget)) --st;
     if (!valid(st)) return p.release();
     if (size_t(st) * p->stage_bytes > budget) return p.release();
     p->stages = st;
     p->smem = size_t(st) * p->stage_bytes + 128;
     if (const char* e = std::getenv("FWI_KKT_KM_PAD_KB"))  // diagnostics: unused extra shared memory
         p->smem = std::min<size_t>(227 * 1024, p->smem + size_t(std::atoi(e)) * 1024);
-#define FWI_KM_ATTR(COLSc, Sc)                                                                           \
-    CK(cudaFuncSetAttribute(kkt_km_kernel<A, COLSc, Sc>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                            int(p->smem)))
-    FWI_KM_DISPATCH(cols, st, FWI_KM_ATTR);
+#define FWI_KM_ATTR(COLSc, Sc, MBc)                                                                       \
+    CK(MBc ? cudaFuncSetAttribute(kkt_km_kernel<A, COLSc, Sc, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                  int(p->smem))                                                             \
+           : cudaFuncSetAttribute(kkt_km1_kernel<A, COLSc, Sc>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                  int(p->smem)))
+    FWI_KM_DISPATCH(cols, st, mb ? 1 : 0, FWI_KM_ATTR);
 #undef FWI_KM_ATTR
     const void* ubase = f32 ? static_cast<const void*>(c.u32.p) : static_cast<const void*>(c.u.p);
     for (int v = 0; v < 2; ++v)
@@ -927,6 +1087,7 @@ bool launch_km(Ctx& c, KktKmPlan* p, const typename A::T* du, const typename A::
     a.nz = c.nz;
     a.K = c.K;
     a.per_strip = p->per_strip;
+    a.nbands = p->nbands;
     a.W = p->W;
     a.gr = p->gr;
     a.RP = p->RP;
@@ -964,12 +1125,16 @@ bool launch_km(Ctx& c, KktKmPlan* p, const typename A::T* du, const typename A::
     if (const char* e = std::getenv("FWI_KKT_KM_ST")) a.stmode = std::atoi(e);
     a.u = reinterpret_cast<const typename A::T*>(f32 ? static_cast<const void*>(c.u32.p)
                                                     : static_cast<const void*>(c.u.p));
-#define FWI_KM_LAUNCH(COLSc, Sc)                                                                          \
-    (kkt_km_kernel<A, COLSc, Sc><<<p->G, 512, p->smem, c.stream>>>(tdu[0], tla[0], p->tm_u[0], tdu[1], tla[1], \
-                                                                  p->tm_u[1], a),                             \
-     c.kkt_kernel[f32 ? 1 : 0] = f32 ? "kkt_km_kernel<F32, " #COLSc ", " #Sc "> (source-major TMA K1, csrc/kkt_tma.cu)" \
-                                    : "kkt_km_kernel<F64, " #COLSc ", " #Sc "> (source-major TMA K1, csrc/kkt_tma.cu)")
-    FWI_KM_DISPATCH(p->cols, p->stages, FWI_KM_LAUNCH);
+#define FWI_KM_LAUNCH(COLSc, Sc, MBc)                                                                      \
+    ((MBc ? kkt_km_kernel<A, COLSc, Sc, true><<<p->G, 512, p->smem, c.stream>>>(tdu[0], tla[0], p->tm_u[0],     \
+                                                                              tdu[1], tla[1], p->tm_u[1], a)  \
+          : kkt_km1_kernel<A, COLSc, Sc><<<p->G, 512, p->smem, c.stream>>>(tdu[0], tla[0], p->tm_u[0], tdu[1],   \
+                                                                         tla[1], p->tm_u[1], a)),             \
+     c.kkt_kernel[f32 ? 1 : 0] = MBc ? (f32 ? "kkt_km_kernel<F32, " #COLSc ", " #Sc ", bands> (source-major TMA K1, csrc/kkt_tma.cu)" \
+                                           : "kkt_km_kernel<F64, " #COLSc ", " #Sc ", bands> (source-major TMA K1, csrc/kkt_tma.cu)") \
+                                     : (f32 ? "kkt_km_kernel<F32, " #COLSc ", " #Sc "> (source-major TMA K1, csrc/kkt_tma.cu)"     \
+                                           : "kkt_km_kernel<F64, " #COLSc ", " #Sc "> (source-major TMA K1, csrc/kkt_tma.cu)"))
+    FWI_KM_DISPATCH(p->cols, p->stages, p->G < p->nbands ? 1 : 0, FWI_KM_LAUNCH);
 #undef FWI_KM_LAUNCH
     CK_LAUNCH();
     return true;
