@@ -5,8 +5,11 @@ Default (N=1): BASELINE config 2 — the isolated, source-batched KKT operator
 apply on a 512x256 grid (20-cell PML), K=64 sources, 256 receivers, complex128.
 One step = one fused KKT apply over all sources with inputs resident in HBM.
 The JSON line also carries the complex64 apply, the Krylov iteration
-throughput of BASELINE config 1 (exact and ILU(4) preconditioners) and the
-end-to-end number through the C ABI with host buffers.
+throughput of BASELINE config 1 (exact, ILU(4) and ILU(21) preconditioners)
+and config 3 (exact) with its algorithmic HBM fraction, the end-to-end number
+through the C ABI with host buffers, and the reference's CPU baselines (its
+kkt_apply on all host threads and its fsgn_gmres_step on config 1, serial),
+timed on the same host in the same run.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -145,6 +148,38 @@ def load_traffic():
         return {}
 
 
+def bench_config(ws, n):
+    """The config dict both arms print (identical keys and values)."""
+    return {"workload": "C2: isolated batched KKT apply, 512x256 grid, 20-cell PML, "
+                        "K=64 sources, R=256 receivers, complex128",
+            "nx": 512, "nz": 256, "K": 64, "R": 256, "n": n,
+            "l2": "inputs larger than L2 (2 alternating 270 MB input vectors + 134 MB u "
+                  "+ 2 outputs per step pair)",
+            "parallelism": f"replicas x{ws}"}
+
+
+def krylov_alg_bytes(st, log, restart, mode):
+    """Algorithmic HBM bytes of one fsgn_gmres_step solve: per iteration j
+    (0-based in its restart cycle) 2 KKT applies + 1 preconditioner apply + (5j + 11) KKT
+    vectors (fused MGS 4(j+1), norm/scale 3, x_cand j+3, b for the true residual 1); per
+    cycle one apply + preconditioner + 3 vectors; once the preconditioned b. Preconditioner
+    = factor bytes read once per batched sweep (exact: 2 sweeps x 2 solves over the block
+    factor; ILU: the 4 stored sweeps L, U, U^T, L^T once) + 64 K n (RHS and solution of both
+    solves) + 16 n (the ds row)."""
+    n, K = st.n, st.K
+    V = st.vec_len * 8
+    A = 80 * K * n + 24 * n
+    F = 4 * st.exact_factor_bytes if mode == "exact" else st.ilu_factor_bytes
+    P = F + 64 * K * n + 16 * n
+    N = log.iterations()
+    total = P + V
+    total += math.ceil(N / restart) * (A + P + 3 * V)
+    for k in range(N):
+        j = k % restart
+        total += 2 * A + P + (5 * j + 11) * V
+    return total
+
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
@@ -223,52 +258,55 @@ def run_ours(args):
     del hin, hout
     vec_bytes = st.vec_len * 8
 
-    # Krylov iterations/s on BASELINE config 1 (exact and ILU(4) preconditioners)
+    # Krylov iterations/s on BASELINE config 1 (exact, ILU(4) and ILU(21) preconditioners) and
+    # config 3 (exact), with the algorithmic HBM bytes of each solve against the peak
     krylov = {}
     if not args.skip_krylov:
-        q = c1_problem()
-        q.d_obs = fw.simulate(q)
-        s1 = fw.GnState(q, exact=True, ilu_level=4)
-        for mode in (fw.PrecondMode.exact, fw.PrecondMode.ilu):
+        def time_solve(state, mode, label, cfg):
+            o = fw.FsgnOptions(mode=mode, restart=30, tol=1e-3, maxit=60, ecg_stride=0)
             for _ in range(2):  # warm-up with the timed options (workspace, plans, clocks)
-                fw.fsgn_gmres_step(s1, fw.FsgnOptions(mode=mode, restart=30, tol=1e-3, maxit=60, ecg_stride=0))
+                fw.fsgn_gmres_step(state, o)
             runs = []
             for _ in range(5):
                 t0 = time.perf_counter()
-                ds, log = fw.fsgn_gmres_step(s1, fw.FsgnOptions(mode=mode, restart=30, tol=1e-3, maxit=60,
-                                                                ecg_stride=0))
+                ds, log = fw.fsgn_gmres_step(state, o)
                 runs.append((log.entries[-1].wall_time, time.perf_counter() - t0, log))
             runs.sort(key=lambda r: r[0])
             wt, tw, log = runs[2]
             it = log.iterations()
-            krylov[mode.name] = {"config": "C1 128x64, K=8, 5 Hz, eps=1e10, tol 1e-3, restart 30, maxit 60",
-                                 "iterations": it, "converged": log.converged,
-                                 "final_residual": log.final_residual(),
-                                 "iters_per_s": it / wt, "solve_wall_s": wt, "step_wall_s": tw,
-                                 "timing": "median of 5 solves after 2 warm-up solves, ConvergenceLog wall time"}
+            byt = krylov_alg_bytes(state, log, 30, "exact" if mode == fw.PrecondMode.exact else "ilu")
+            krylov[label] = {"config": cfg, "iterations": it, "converged": log.converged,
+                             "final_residual": log.final_residual(), "iters_per_s": it / wt,
+                             "ms_per_iter": wt / it * 1e3, "solve_wall_s": wt, "step_wall_s": tw,
+                             "alg_bytes_per_solve": byt, "achieved_gbs": byt / wt / 1e9,
+                             "hbm_frac": byt / wt / 1e9 / peak,
+                             "timing": "median of 5 solves after 2 warm-up solves, ConvergenceLog wall time; "
+                                       "bytes: SURVEY 8(d) per-iteration formula (krylov_alg_bytes)"}
+
+        q = c1_problem()
+        q.d_obs = fw.simulate(q)
+        c1cfg = "C1 128x64, K=8, 5 Hz, eps=1e10, tol 1e-3, restart 30, maxit 60"
+        s1 = fw.GnState(q, exact=True, ilu_level=4)
+        time_solve(s1, fw.PrecondMode.exact, "exact", c1cfg)
+        time_solve(s1, fw.PrecondMode.ilu, "ilu", c1cfg + ", ILU(4)")
         s1.close()
+        s21 = fw.GnState(q, exact=True, ilu_level=21)
+        time_solve(s21, fw.PrecondMode.ilu, "ilu21", c1cfg + ", ILU(21)")
+        s21.close()
         # config 3 (384x128, K=48, 3 Hz, exact preconditioner, eps = 1e-2 ||J^H J|| = 2.8e10)
         q3 = c3_problem(freq_hz=3.0)
         q3.d_obs = fw.simulate(q3)
         q3.epsilon = 2.8e10
         s3 = fw.GnState(q3, exact=True)
-        for _ in range(2):
-            fw.fsgn_gmres_step(s3, fw.FsgnOptions(restart=30, tol=1e-3, maxit=60, ecg_stride=0))
-        runs = []
-        for _ in range(5):
-            ds, log = fw.fsgn_gmres_step(s3, fw.FsgnOptions(restart=30, tol=1e-3, maxit=60, ecg_stride=0))
-            runs.append((log.entries[-1].wall_time, log))
-        runs.sort(key=lambda r: r[0])
-        wt, log = runs[2]
-        krylov["c3_exact"] = {"config": "C3 384x128, K=48, 3 Hz, eps=2.8e10, tol 1e-3, restart 30, maxit 60",
-                              "iterations": log.iterations(), "converged": log.converged,
-                              "final_residual": log.final_residual(), "iters_per_s": log.iterations() / wt,
-                              "solve_wall_s": wt, "timing": "median of 5 solves after 2 warm-up solves, ConvergenceLog wall time"}
+        time_solve(s3, fw.PrecondMode.exact, "c3_exact",
+                   "C3 384x128, K=48, 3 Hz, eps=2.8e10, tol 1e-3, restart 30, maxit 60")
         s3.close()
 
     cpu = None
     if rank == 0 and not args.skip_cpu:
         cpu = cpu_baseline_apply(p, sample_applies=None)
+        if not args.skip_krylov:
+            cpu["krylov"] = cpu_baseline_krylov()
 
     if rank == 0:
         tr = load_traffic().get("kkt_apply_c128_c2")
@@ -277,16 +315,12 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic (seeded; BASELINE config 2 shapes and distributions)",
-            "config": {"workload": "C2: isolated batched KKT apply, 512x256 grid, 20-cell PML, "
-                                   "K=64 sources, R=256 receivers, complex128",
-                       "nx": 512, "nz": 256, "K": K, "R": 256, "n": n,
-                       "l2": "inputs larger than L2 (2 alternating 270 MB input vectors + 134 MB u "
-                             "+ 2 outputs per step pair)",
-                       "parallelism": f"replicas x{ws}"},
+            "config": bench_config(ws, n),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,
                          "frac_of_datasheet_8000gbs": achieved / 8000.0,
                          "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                         "traffic_source": (f"{tr.get('source')}; not measured in this run") if tr else None,
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "kernel": kname},
             "c64": {"applies_per_s": ws / per32, "ms_per_apply": per32 * 1e3,
@@ -336,6 +370,32 @@ def cpu_baseline_apply(p, sample_applies=None):
                       f"{sec:.1f} s wall; {os.cpu_count()} host CPUs"}
 
 
+def cpu_baseline_krylov():
+    """The reference's fsgn_gmres_step (oracle/_ref, unmodified reference core; serial, so 1
+    core) on BASELINE config 1 with ecg_stride 0, same options as our krylov block."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    from paper_2204_06489_b200 import _abi
+    from paper_2204_06489_b200.problem import c1_problem
+    p = c1_problem()
+    p.d_obs = po.ref_simulate(p)
+    out = {}
+    for label, mode, level in (("exact", _abi.FWI_PRECOND_EXACT, 4), ("ilu", _abi.FWI_PRECOND_ILU, 4),
+                               ("ilu21", _abi.FWI_PRECOND_ILU, 21)):
+        ref = po.Ref(p, full=True, exact=True, ilu_level=level)
+        t0 = time.perf_counter()
+        _, log = ref.fsgn(mode, 30, 1e-3, 60, 0)
+        tw = time.perf_counter() - t0
+        it = log.iterations()
+        wt = log.entries[-1].wall_time
+        out[label] = {"iters_per_s": it / wt, "iterations": it, "converged": log.converged,
+                      "solve_wall_s": wt, "step_wall_s": tw, "cores": 1, "kind": "reference",
+                      "sample": "one reference fsgn_gmres_step (C1, tol 1e-3, restart 30, maxit 60, "
+                                f"ecg_stride 0{', ILU(%d)' % level if mode == _abi.FWI_PRECOND_ILU else ''}), "
+                                "ConvergenceLog wall time, same host, same run"}
+    return out
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -359,9 +419,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic (seeded; BASELINE config 2 shapes and distributions)",
-        "config": {"workload": "C2: isolated batched KKT apply, 512x256 grid, 20-cell PML, "
-                               "K=64 sources, R=256 receivers, complex128",
-                   "nx": 512, "nz": 256, "K": 64, "R": 256, "n": p.n},
+        "config": bench_config(ws, p.n),
         "cpu_baseline": {"value": value, "unit": "applies/s", "cores": th, "kind": "reference",
                          "sample": f"each step = {per_step} serial reference kkt_apply calls over {th} "
                                    f"host threads ({os.cpu_count()} CPUs)"},
@@ -373,7 +431,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--skip-cpu", action="store_true")
@@ -382,9 +440,6 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
-        if args.steps > 5:
-            args.steps = 5   # each reference step is a bounded multi-second CPU sample
-        args.warmup = min(args.warmup, 1)
         run_reference(args)
     else:
         run_ours(args)

@@ -119,6 +119,10 @@ typedef struct fwi_state_info {
     int has_exact, has_ilu;
     int64_t vec_doubles;      /* 4*K*n + n */
     int64_t device_bytes;     /* resident bytes held by the context */
+    int64_t exact_factor_bytes; /* exact block factorisation (0: none) */
+    int64_t ilu_factor_bytes;   /* ILU(p) factors incl. transposes and schedules (0: none) */
+    double exact_probe_residual; /* ||b - A A^{-1} b|| / ||b|| of the post-factorisation
+                                    probe (-1: not run) */
 } fwi_state_info;
 
 /* fwi::FsgnOptions (include/fwi/kkt.hpp:47-57). */
@@ -192,6 +196,8 @@ int fwi_dev_solve(fwi_dev_ctx* ctx, int mode, int adjoint, int nrhs, const doubl
 /* ---- KKT vectors -------------------------------------------------------- */
 int fwi_dev_vec_create(fwi_dev_ctx* ctx, int precision, fwi_dev_vec** out); /* zeros */
 int fwi_dev_vec_destroy(fwi_dev_vec* v);
+/* Precision the vector was created with (FWI_C128 / FWI_C64); -1 for NULL. */
+int fwi_dev_vec_precision(const fwi_dev_vec* v);
 int fwi_dev_vec_upload(fwi_dev_vec* v, const double* host_flat);   /* 4Kn+n doubles */
 int fwi_dev_vec_download(const fwi_dev_vec* v, double* host_flat);
 /* complex64 vectors: host side is 4Kn+n floats */

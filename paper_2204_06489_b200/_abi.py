@@ -50,7 +50,9 @@ class StateInfo(C.Structure):
     _fields_ = [("nx", C.c_int), ("nz", C.c_int), ("n", C.c_int), ("num_sources", C.c_int),
                 ("num_data", C.c_int), ("omega", C.c_double), ("epsilon", C.c_double),
                 ("drop_reg_term", C.c_int), ("has_exact", C.c_int), ("has_ilu", C.c_int),
-                ("vec_doubles", C.c_int64), ("device_bytes", C.c_int64)]
+                ("vec_doubles", C.c_int64), ("device_bytes", C.c_int64),
+                ("exact_factor_bytes", C.c_int64), ("ilu_factor_bytes", C.c_int64),
+                ("exact_probe_residual", C.c_double)]
 
 
 class FsgnOptions(C.Structure):

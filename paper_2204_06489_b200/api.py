@@ -119,6 +119,7 @@ def lib() -> C.CDLL:
                 "fwi_dev_solve": [_vp, C.c_int, C.c_int, C.c_int, _dp, _dp],
                 "fwi_dev_vec_create": [_vp, C.c_int, C.POINTER(_vp)],
                 "fwi_dev_vec_destroy": [_vp],
+                "fwi_dev_vec_precision": [_vp],
                 "fwi_dev_vec_upload": [_vp, _dp],
                 "fwi_dev_vec_download": [_vp, _dp],
                 "fwi_dev_vec_upload_f32": [_vp, _fp],
@@ -219,6 +220,8 @@ class GnState:
         self.vec_len = int(info.vec_doubles)
         self.device_bytes = int(info.device_bytes)
         self.has_exact, self.has_ilu = bool(info.has_exact), bool(info.has_ilu)
+        self.exact_factor_bytes, self.ilu_factor_bytes = int(info.exact_factor_bytes), int(info.ilu_factor_bytes)
+        self.exact_probe_residual = float(info.exact_probe_residual)
 
     def close(self):
         if getattr(self, "h", None):

@@ -118,7 +118,11 @@ int fwi_dev_ctx_info(const fwi_dev_ctx* ctx, fwi_state_info* o) {
         o->has_ilu = c.ilu != nullptr;
         o->vec_doubles = 4 * int64_t(c.K) * c.n + c.n;
         o->device_bytes = int64_t(c.diag.bytes() * 3 + c.u.bytes() + c.u32.bytes() + c.s.bytes() +
-                                  exact_bytes(c.exact) + c.work_a.bytes() + c.work_b.bytes() + c.work_c.bytes());
+                                  exact_bytes(c.exact) + ilu_bytes(c.ilu) + c.work_a.bytes() + c.work_b.bytes() +
+                                  c.work_c.bytes());
+        o->exact_factor_bytes = exact_bytes(c.exact);
+        o->ilu_factor_bytes = ilu_bytes(c.ilu);
+        o->exact_probe_residual = exact_probe_residual(c.exact);
     });
 }
 
@@ -255,6 +259,8 @@ int fwi_dev_vec_create(fwi_dev_ctx* ctx, int precision, fwi_dev_vec** out) {
 int fwi_dev_vec_destroy(fwi_dev_vec* v) {
     return guard([&] { delete v; });
 }
+
+int fwi_dev_vec_precision(const fwi_dev_vec* v) { return v ? v->v.prec : -1; }
 
 int fwi_dev_vec_upload(fwi_dev_vec* v, const double* h) {
     return guard([&] {

@@ -140,6 +140,7 @@ int reduce_blocks();
 void ilu_factor(Ctx& c, int level, double shift);
 void ilu_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int nrhs);
 void ilu_free(IluFactor*);
+int64_t ilu_bytes(const IluFactor*);
 
 // ---- exact.cu
 void exact_factor(Ctx& c);
@@ -147,6 +148,7 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
 void exact_free(ExactFactor*);
 void gmres_work_free(GmresWork*);
 int64_t exact_bytes(const ExactFactor*);
+double exact_probe_residual(const ExactFactor*);
 
 // ---- precond.cu
 void precond_apply(Ctx& c, int mode, const Vec& v, Vec& out);

@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(256) block_inverse_kernel(int b, const double2
         if (!(best > 0.0)) p = k;
         if (tid == 0) {
             piv[k] = p;
-            if (!(best > 0.0) && *status == 0) *status = status_base + k + 1;
+            if (!(best > 0.0)) atomicCAS(status, 0, status_base + k + 1);
         }
         // owners of rows p and k publish them (pre-swap); register index by unrolled select
         const int ip = p >> 2, ik = k >> 2;

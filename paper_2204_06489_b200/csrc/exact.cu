@@ -22,6 +22,7 @@
 // A^{-H} b = conj(A^{-1} conj(b)). Storage: L * nb^2 complex128
 // (C1: 8.4 MB, C3: 100 MB, C5: 34 GB), read twice per solve.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <string>
 #include <array>
@@ -48,6 +49,8 @@ struct ExactFactor {
     bool dense = false;     // long lines: GEMM line sweeps (dense.cu)
     bool dense_factor = false;  // whole-GPU block Gauss-Jordan per line (dense.cu)
     bool twisted = false;       // factored from both ends towards line `mid` (two sweep chains)
+    double probe_residual = -1; // ||b - A A^{-1} b|| / ||b|| of the post-factorisation probe
+    bool refactored = false;    // the probe forced whole-line pivoting
     int mid = 0;
     DenseWork dwork;
     DevBuf<double2> tbuf;   // dense sweep operand (nrhs x nb)
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(512) line_factor_kernel(
             for (int w = 0; w < (nt + 31) / 32; ++w)
                 if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < b)) { bv = red_v[w]; b = red_i[w]; }
             if (!(bv > 0.0)) {
-                if (*status == 0) *status = line * nb + k + 1;
+                atomicCAS(status, 0, line * nb + k + 1);
                 b = k;
             }
             s_p = b;
@@ -1246,7 +1249,10 @@ size_t sweep_smem(int nb) {
 
 }  // namespace
 
-void exact_factor(Ctx& c) {
+// line_pivot: factor every line with the one-CTA Gauss-Jordan, partial pivoting over the
+// whole line (the fallback when the residual probe rejects the block Gauss-Jordan, whose
+// pivot search is restricted to 64-wide diagonal blocks)
+static void exact_factor_once(Ctx& c, bool line_pivot) {
     const auto t_host0 = std::chrono::steady_clock::now();
     auto f = std::make_unique<ExactFactor>();
     f->col_lines = c.nz <= c.nx;  // short lines by default (least factor work and storage)
@@ -1285,14 +1291,16 @@ void exact_factor(Ctx& c) {
     const char* ef = std::getenv("FWI_EXACT_FACTOR");
     f->dense = nb > 512 || force_dense;
     f->dense_factor = f->dense || (nb > 112 && !(ef && std::string(ef) == "cta"));
-    if (!f->dense && std::getenv("FWI_EXACT_TWISTED") && std::string(std::getenv("FWI_EXACT_TWISTED")) == "1")
+    if (line_pivot && !f->dense) f->dense_factor = false;
+    if (!line_pivot && !f->dense && std::getenv("FWI_EXACT_TWISTED") &&
+        std::string(std::getenv("FWI_EXACT_TWISTED")) == "1")
         f->dense_factor = true;  // the twisted factorisation is built with the block Gauss-Jordan
     // Twisted factorisation: Schur recursions from both ends meet at the middle line,
     // so a solve is two concurrent sweep chains of ~L/2 lines each (then a dense
     // solve of the middle line) instead of one chain of L: a line step is latency-
     // bound, so this halves the sweep. Used when the step model says it pays.
     if (f->dense_factor && L >= 8) {
-        const char* et = std::getenv("FWI_EXACT_TWISTED");
+        const char* et = line_pivot ? nullptr : std::getenv("FWI_EXACT_TWISTED");
         if (et) {
             f->twisted = std::string(et) == "1";
         } else if (f->dense) {
@@ -1374,11 +1382,106 @@ void exact_factor(Ctx& c) {
         std::fprintf(stderr, "[fwi] exact factor nb=%d L=%d dense=%d twisted=%d: %.3f s\n", nb, L, int(f->dense),
                      int(f->twisted),
                      std::chrono::duration<double>(std::chrono::steady_clock::now() - t_host0).count());
-    if (st != 0)
+    if (st != 0) {
+        // status = line * nb + (position in the line) + 1. Reported as the grid node, the
+        // reference's elimination-column numbering (natural order, src/lu.cpp:113); which node
+        // of a singular operator meets the zero pivot first depends on the elimination order,
+        // and for a zero row (tests/test_lu.cpp:44-47) both name that row.
+        const int line = (st - 1) / nb, m = (st - 1) % nb;
+        const int node = f->col_lines ? m * c.nx + line : line * c.nx + m;
         throw FwiError(FWI_ERR_SINGULAR_PIVOT,
-                       "LU: singular pivot at elimination step " + std::to_string(st - 1), st - 1);
+                       "LU: singular pivot at node " + std::to_string(node) + " (exact block factorisation, line " +
+                           std::to_string(line) + ")",
+                       node);
+    }
     if (c.exact) exact_free(c.exact);
     c.exact = f.release();
+}
+
+namespace {
+// r = b - A x with the assembled 5-point planes (A(i,i-1) = east[i-1], A(i,i-nx) =
+// south[i-nx]: exact complex symmetry)
+__global__ void stencil_residual(int nx, int64_t n, const double2* __restrict__ diag,
+                                 const double2* __restrict__ east, const double2* __restrict__ south,
+                                 const double2* __restrict__ x, const double2* __restrict__ b,
+                                 double2* __restrict__ r) {
+    const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    double2 acc = fmul(diag[i], x[i]);
+    auto add = [&](double2 a, double2 v) {
+        const double2 t = fmul(a, v);
+        acc.x += t.x;
+        acc.y += t.y;
+    };
+    if (i + 1 < n) add(east[i], x[i + 1]);
+    if (i >= 1) add(east[i - 1], x[i - 1]);
+    if (i + nx < n) add(south[i], x[i + nx]);
+    if (i >= nx) add(south[i - nx], x[i - nx]);
+    r[i] = make_double2(b[i].x - acc.x, b[i].y - acc.y);
+}
+}  // namespace
+
+double exact_probe_residual(const ExactFactor* f) { return f ? f->probe_residual : -1.0; }
+
+// ||b - A A^{-1} b|| / ||b|| for one seeded random right-hand side
+double exact_residual_probe(Ctx& c) {
+    std::vector<double2> hb(size_t(c.n));
+    uint64_t z = 0x9e3779b97f4a7c15ull;
+    auto rnd = [&] {  // splitmix64 -> [-1, 1)
+        z += 0x9e3779b97f4a7c15ull;
+        uint64_t t = z;
+        t = (t ^ (t >> 30)) * 0xbf58476d1ce4e5b9ull;
+        t = (t ^ (t >> 27)) * 0x94d049bb133111ebull;
+        t ^= t >> 31;
+        return double(t >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+    };
+    for (auto& v : hb) v = make_double2(rnd(), rnd());
+    DevBuf<double2> b(c.n), x(c.n), r(c.n);
+    CK(cudaMemcpyAsync(b.p, hb.data(), b.bytes(), cudaMemcpyHostToDevice, c.stream));
+    const int64_t cnt = c.solve_count[FWI_PRECOND_EXACT];
+    exact_solve_batch(c, false, b.p, x.p, 1);
+    c.solve_count[FWI_PRECOND_EXACT] = cnt;  // not a caller's solve
+    stencil_residual<<<int((c.n + 255) / 256), 256, 0, c.stream>>>(c.nx, c.n, c.diag.p, c.east.p, c.south.p, x.p,
+                                                                   b.p, r.p);
+    CK_LAUNCH();
+    const double rr = dev_dot(&c, c.stream, reinterpret_cast<const double*>(r.p),
+                              reinterpret_cast<const double*>(r.p), 2 * int64_t(c.n));
+    const double bb = dev_dot(&c, c.stream, reinterpret_cast<const double*>(b.p),
+                              reinterpret_cast<const double*>(b.p), 2 * int64_t(c.n));
+    return std::sqrt(rr / bb);
+}
+
+// The exact factorisation with a residual guard. The block
+// factorisations pivot within a line, or within 64-wide diagonal blocks of a line (the
+// block Gauss-Jordan, nb > 112), never across lines as the reference's sparse LU does
+// (src/lu.cpp:56-133). One seeded right-hand side is solved after every factorisation;
+// above kProbeTol the lines are re-factored with partial pivoting over each whole line
+// (nb <= 512), and if that also fails, or for longer lines, SingularPivotError is raised
+// rather than returning an inaccurate factor. FWI_EXACT_PROBE=0 skips the probe.
+void exact_factor(Ctx& c) {
+    constexpr double kProbeTol = 1e-8;
+    exact_factor_once(c, false);
+    const char* ep = std::getenv("FWI_EXACT_PROBE");
+    if (ep && std::string(ep) == "0") return;
+    double res = exact_residual_probe(c);
+    c.exact->probe_residual = res;
+    if (!(res <= kProbeTol) && c.exact->nb <= 512 && c.exact->dense_factor) {
+        exact_factor_once(c, true);
+        res = exact_residual_probe(c);
+        c.exact->probe_residual = res;
+        c.exact->refactored = true;
+    }
+    if (std::getenv("FWI_EXACT_PLAN_LOG"))
+        std::fprintf(stderr, "[fwi] exact factor residual probe %.3e%s\n", res,
+                     c.exact->refactored ? " (after whole-line pivoting)" : "");
+    if (!(res <= kProbeTol)) {
+        char buf[160];
+        std::snprintf(buf, sizeof buf,
+                      "LU: exact block factorisation failed its residual probe (||b - A x|| / ||b|| = %.3e)", res);
+        exact_free(c.exact);
+        c.exact = nullptr;
+        throw FwiError(FWI_ERR_SINGULAR_PIVOT, buf, -1);
+    }
 }
 
 void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int nrhs) {

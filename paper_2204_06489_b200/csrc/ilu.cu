@@ -43,6 +43,7 @@ struct IluFactor {
 };
 
 void ilu_free(IluFactor* f) { delete f; }
+int64_t ilu_bytes(const IluFactor* f) { return f ? f->bytes : 0; }
 
 namespace {
 

@@ -1132,8 +1132,8 @@ bool launch_km(Ctx& c, KktKmPlan* p, const typename A::T* du, const typename A::
                                                                          tla[1], p->tm_u[1], a)),             \
      c.kkt_kernel[f32 ? 1 : 0] = MBc ? (f32 ? "kkt_km_kernel<F32, " #COLSc ", " #Sc ", bands> (source-major TMA K1, csrc/kkt_tma.cu)" \
                                            : "kkt_km_kernel<F64, " #COLSc ", " #Sc ", bands> (source-major TMA K1, csrc/kkt_tma.cu)") \
-                                     : (f32 ? "kkt_km_kernel<F32, " #COLSc ", " #Sc "> (source-major TMA K1, csrc/kkt_tma.cu)"     \
-                                           : "kkt_km_kernel<F64, " #COLSc ", " #Sc "> (source-major TMA K1, csrc/kkt_tma.cu)"))
+                                     : (f32 ? "kkt_km1_kernel<F32, " #COLSc ", " #Sc "> (source-major TMA K1, one band per CTA, csrc/kkt_tma.cu)" \
+                                           : "kkt_km1_kernel<F64, " #COLSc ", " #Sc "> (source-major TMA K1, one band per CTA, csrc/kkt_tma.cu)"))
     FWI_KM_DISPATCH(p->cols, p->stages, p->G < p->nbands ? 1 : 0, FWI_KM_LAUNCH);
 #undef FWI_KM_LAUNCH
     CK_LAUNCH();

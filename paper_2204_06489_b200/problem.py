@@ -408,3 +408,42 @@ def no_receiver_instance() -> Problem:
     sv = Survey.per_source([(5, 5), (7, 6)], [[], []])
     return Problem(grid=g, survey=sv, freq_hz=0.15, epsilon=1e-2, s=np.ones(g.n),
                    r=np.zeros(0, np.complex128), d_obs=np.zeros(0, np.complex128), name="norecv")
+
+
+def cancelling_slowness(freq_hz: float) -> float:
+    """Squared slowness whose stencil diagonal 4/h^2 - w^2 s X Z cancels exactly on an h = 1
+    grid without PML (X = Z = 1): fl(w^2 * s) == 4 (assemble_helmholtz, src/helmholtz.cpp:52-53)."""
+    w2 = omega_of(freq_hz) ** 2
+    s = 4.0 / w2
+    for _ in range(64):
+        if w2 * s == 4.0:
+            return s
+        s = math.nextafter(s, 0.0 if w2 * s > 4.0 else 10.0)
+    raise RuntimeError("no exactly cancelling slowness found")
+
+
+def zero_pivot_instance(freq_hz: float = 0.15) -> Problem:
+    """A Helmholtz instance with an exact zero ILU pivot (tests/test_ilu.cpp:107-120 on a real
+    operator): 7x6 grid, h = 1, no PML, node (1,1)'s diagonal cancels exactly; its earlier
+    neighbours are Dirichlet, so its ILU pivot is the bare diagonal -> ZeroPivotError(8).
+    The full operator is nonsingular (the exact LU pivots past it)."""
+    g = Grid(7, 6, 1.0, 0, sigma_max=0.0)
+    s = np.ones(g.n)
+    s[g.index(1, 1)] = cancelling_slowness(freq_hz)
+    sv = Survey.per_source([(3, 3)], [[(4, 3), (2, 4)]])
+    K = 1
+    u = np.linspace(0.1, 1.0, K * g.n) * (1.0 - 0.5j)
+    return Problem(grid=g, survey=sv, freq_hz=freq_hz, epsilon=1.0, s=s, u=u,
+                   r=np.array([0.5 - 0.25j, -0.125 + 1.0j]), name="zero_pivot")
+
+
+def singular_instance(freq_hz: float = 0.15) -> Problem:
+    """A singular Helmholtz operator with a zero row (tests/test_lu.cpp:44-47 on a real
+    operator): 3x3 grid, h = 1, no PML; the only interior node's couplings all go to
+    Dirichlet columns and its diagonal cancels -> SingularPivotError(4)."""
+    g = Grid(3, 3, 1.0, 0, sigma_max=0.0)
+    s = np.ones(g.n)
+    s[g.index(1, 1)] = cancelling_slowness(freq_hz)
+    sv = Survey.per_source([(1, 1)], [[(1, 1)]])
+    return Problem(grid=g, survey=sv, freq_hz=freq_hz, epsilon=1.0, s=s, u=np.ones(g.n, np.complex128),
+                   r=np.ones(1, np.complex128), name="singular")

@@ -77,12 +77,11 @@ def test_dense_precond_and_gmres_history_c1():
     want = ref.precond_apply(x, _abi.FWI_PRECOND_EXACT)
     got = fw.precond_apply(dev, fw.KktVector.from_host(dev, x), fw.PrecondMode.exact).to_host()
     assert rel(got, want) <= 1e-10
-    _, log_r = ref.fsgn(_abi.FWI_PRECOND_EXACT, 30, 0.0, 30, 0)
-    _, log_d = fw.fsgn_gmres_step(dev, fw.FsgnOptions(restart=30, tol=0.0, maxit=30, ecg_stride=0))
+    _, log_r = ref.fsgn(_abi.FWI_PRECOND_EXACT, 30, 0.0, 50, 0)
+    _, log_d = fw.fsgn_gmres_step(dev, fw.FsgnOptions(restart=30, tol=0.0, maxit=50, ecg_stride=0))
     rr, rd = np.array(log_r.residuals()), np.array(log_d.residuals())
     assert len(rr) == len(rd)
-    mask = rr >= 1e-6
-    assert (np.abs(rd - rr)[mask] / rr[mask]).max() <= 1e-8
+    assert (np.abs(rd - rr) / rr).max() <= 1e-8  # every entry, no floor
 
 
 def test_host_basis_gmres_history_matches_reference_c1():
@@ -102,8 +101,7 @@ def test_host_basis_gmres_history_matches_reference_c1():
         del os.environ["FWI_GMRES_HOST_BASIS"]
     rr, rd = np.array(log_r.residuals()), np.array(log_d.residuals())
     assert len(rr) == len(rd)
-    mask = rr >= 1e-6
-    assert (np.abs(rd - rr)[mask] / rr[mask]).max() <= 1e-8
+    assert (np.abs(rd - rr) / rr).max() <= 1e-8  # every entry, no floor
     assert log_d.stagnated == log_r.stagnated
 
 
@@ -158,8 +156,7 @@ def test_host_basis_small_restart_matches_reference(restart):
         del os.environ["FWI_GMRES_HOST_BASIS"]
     rr, rd = np.array(log_r.residuals()), np.array(log_d.residuals())
     assert len(rr) == len(rd) and log_d.stagnated == log_r.stagnated
-    mask = rr >= 1e-6
-    assert (np.abs(rd - rr)[mask] / rr[mask]).max() <= 1e-8
+    assert (np.abs(rd - rr) / rr).max() <= 1e-8  # every entry, no floor
 
 
 @pytest.mark.parametrize("mk", [lambda: small_problem(nx=40, nz=26, n_pml=4, K=3, R=5),

@@ -253,7 +253,7 @@ def test_forward_fields_match_reference(c1):
 def test_fsgn_residual_history_c1(c1, mode):
     """Residual histories agree to 1e-8 per iteration (north-star gate)."""
     p, ref, dev = c1
-    maxit = 50 if mode == fw.PrecondMode.ilu else 30
+    maxit = 50
     ds_r, log_r = ref.fsgn(int(mode), 30, 0.0, maxit, 0)
     ds_d, log_d = fw.fsgn_gmres_step(dev, fw.FsgnOptions(mode=mode, restart=30, tol=0.0, maxit=maxit,
                                                          ecg_stride=0))

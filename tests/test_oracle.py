@@ -9,7 +9,8 @@ import pytest
 import golden_io
 import pyoracle as po
 from paper_2204_06489_b200 import _abi
-from paper_2204_06489_b200.problem import no_receiver_instance, random_kkt, small_problem, standard_instance
+from paper_2204_06489_b200.problem import (no_receiver_instance, random_kkt, singular_instance, small_problem,
+                                           standard_instance, zero_pivot_instance)
 
 
 def eq(a, b):
@@ -161,8 +162,26 @@ def test_zero_rhs_returns_zero_in_zero_iterations():
 
 
 def test_zero_pivot_reported_like_reference():
-    """ZeroPivotError index (include/fwi/ilu.hpp:11-17) agrees with the reference."""
-    p = small_problem()
-    o = po.Orc(p, exact=False)
-    r = po.Ref(p, full=False, exact=False)
-    assert o.ilu_factor_status(2, 0.0) == r.ilu_factor_status(2, 0.0) == (0, -1)
+    """ZeroPivotError index (include/fwi/ilu.hpp:11-17; tests/test_ilu.cpp:107-120) agrees with
+    the reference on a Helmholtz operator whose pivot cancels exactly, and a shift rescues it."""
+    p = zero_pivot_instance()
+    o = po.Orc(p, exact=True)
+    r = po.Ref(p, full=False, exact=True)
+    for level in (0, 2, 5):
+        assert o.ilu_factor_status(level, 0.0) == r.ilu_factor_status(level, 0.0) == \
+            (_abi.FWI_ERR_ZERO_PIVOT, p.grid.index(1, 1))
+    assert o.ilu_factor_status(2, 0.5) == r.ilu_factor_status(2, 0.5) == (0, -1)
+    q = small_problem()
+    assert po.Orc(q, exact=False).ilu_factor_status(2, 0.0) == \
+        po.Ref(q, full=False, exact=False).ilu_factor_status(2, 0.0) == (0, -1)
+
+
+def test_singular_pivot_reported_like_reference():
+    """SingularPivotError index (include/fwi/lu.hpp:11-16; tests/test_lu.cpp:44-47): a zero row."""
+    p = singular_instance()
+    got = []
+    for mk in (lambda: po.Orc(p, exact=True), lambda: po.Ref(p, full=False, exact=True)):
+        with pytest.raises(po.CheckerError) as e:
+            mk()
+        got.append((e.value.code, e.value.index))
+    assert got[0] == got[1] == (_abi.FWI_ERR_SINGULAR_PIVOT, p.grid.index(1, 1))
