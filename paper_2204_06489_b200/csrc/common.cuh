@@ -10,6 +10,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -125,6 +126,18 @@ __device__ __forceinline__ double2 cdiv(double2 n, double2 dd) {
     return make_double2(x, y);
 }
 #endif
+
+// the divisor-only part of cdiv / host_cdiv: returns |c| < |d| with r and den as cdiv forms them
+inline bool host_cdiv_prep(double c, double d, double& r, double& den) {
+    if (std::fabs(c) < std::fabs(d)) {
+        r = c / d;
+        den = c * r + d;
+        return true;
+    }
+    r = d / c;
+    den = d * r + c;
+    return false;
+}
 
 // host twin of cdiv (used by the host-side ILU factorisation)
 inline void host_cdiv(double a, double b, double c, double d, double& x, double& y) {

@@ -441,3 +441,20 @@ def test_fused_mgs_bitwise_equals_stepwise(c1):
         del os.environ["FWI_GMRES_MGS_STEPS"]
     assert log_f.residuals() == log_s.residuals()
     assert np.array_equal(ds_f, ds_s)
+
+
+@pytest.mark.parametrize("level", [4, 21])
+def test_ilu_solves_bit_exact_config3_size(level):
+    """ILU(p) sweeps on the 384x128 config-3 grid (vector beyond shared memory: the
+    level-ordered ring sweep) are bit-identical to the reference's IluFactors::solve
+    (src/ilu.cpp:131-174), forward and adjoint, at the default level and the paper's."""
+    from paper_2204_06489_b200.problem import c3_problem
+    p = c3_problem(freq_hz=3.0)
+    rng = np.random.default_rng(31)
+    p.u = rng.standard_normal(p.K * p.n) + 1j * rng.standard_normal(p.K * p.n)
+    p.r = rng.standard_normal(p.survey.num_data) + 0j
+    ref = po.Ref(p, full=False, exact=False, ilu_level=level)
+    dev = fw.GnState(p, exact=False, ilu_level=level)
+    b = rng.standard_normal(p.n) + 1j * rng.standard_normal(p.n)
+    for adj in (False, True):
+        assert np.array_equal(dev.solve(b, fw.PrecondMode.ilu, adj), ref.solve(b, _abi.FWI_PRECOND_ILU, adj)), adj
