@@ -498,6 +498,26 @@ int ref_write_model(const char* path, int nx, int nz, double h, int n_pml, int k
     });
 }
 
+// the reference's model generators (src/model_io.cpp:437-487): kind 0 layered, 1 lens;
+// values out (nx*nz velocities)
+int ref_make_model(int kind, int nx, int nz, double h, int n_pml, const double* vel, int nvel, const int* ifc,
+                   int nifc, double bg, double amp, double cx, double cz, double rad, double* values) {
+    return guard([&] {
+        const Grid2D g = build_grid(nx, nz, h, n_pml);
+        const ModelFile m = kind == 0 ? make_layered_model(g, std::vector<double>(vel, vel + nvel),
+                                                           std::vector<int>(ifc, ifc + nifc))
+                                      : make_lens_model(g, bg, amp, cx, cz, rad);
+        std::memcpy(values, m.values.data(), m.values.size() * sizeof(double));
+    });
+}
+
+int ref_write_heatmap(const char* path, int nx, int nz, double h, int n_pml, const double* values) {
+    return guard([&] {
+        const Grid2D g = build_grid(nx, nz, h, n_pml);
+        write_heatmap(path, g, RealVector(values, values + std::size_t(nx) * nz));
+    });
+}
+
 // status: 0 ok, 1 ParseError, 2 IoError, 3 other; header out = nx, nz, n_pml, kind; h; values (cap doubles)
 int ref_read_model(const char* path, int* hdr, double* h, double* values, long cap) {
     try {

@@ -19,11 +19,12 @@
 // solve is validated by its residual ||A x - b|| in the tests and by parity with
 // the reference LU on small grids (FWI_EXACT_DENSE=1 forces this path).
 //
-// cgemm is a SIMT FP64 complex GEMM (B200 FP64: 64 DFMA/clk/SM, measured by
-// tools/fp64_probe.cu; the FP64 tensor path has the same peak, so DFMA with
-// register tiling is the right unit): 64x64 or 32x64 output tiles, 16-deep K
-// slabs staged through shared memory with register prefetch, 4 DFMA per
-// complex multiply-add.
+// cgemm runs on the FP64 tensor cores by default (zgemm_pipe_kernel: DMMA
+// m8n8k4, Gauss's three-product form, a 3-stage cp.async ring; FWI_CGEMM picks
+// the older variants): 32.2 TFLOP/s effective on 1024^3 against 26.5 for cuBLAS
+// ZGEMM. The SIMT DFMA kernel (cgemm_kernel, FWI_CGEMM=simt,
+// 64x64 or 32x64 tiles with register prefetch, 4 DFMA per complex
+// multiply-add) is kept as the reference point (12.5 TFLOP/s).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -451,12 +452,22 @@ constexpr int zgemm_pipe_smem() {
 
 // G3: Gauss's three-product form, S = (Ar+Ai)(Br+Bi): real = P - Q, imag = S - P - Q
 // (3 DMMA per complex k-step instead of 4; operand sums formed as the fragments load)
+// batch strides: blockIdx.z selects A + z sA, B + z sB, C0 + z sC0, C + z sC (cgemm_batched)
+struct GemmStrides {
+    int64_t a = 0, b = 0, c0 = 0, c = 0;
+};
+
 template <int BM, bool BT, bool G3>
 __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, double alpha,
                                                          const double2* __restrict__ A, int64_t lda,
                                                          const double2* __restrict__ B, int64_t ldb,
-                                                         const double2* C0, int64_t ldc0, double2* C, int64_t ldc) {
+                                                         const double2* C0, int64_t ldc0, double2* C, int64_t ldc,
+                                                         GemmStrides bs) {
     extern __shared__ __align__(16) double2 psm[];
+    A += blockIdx.z * bs.a;
+    B += blockIdx.z * bs.b;
+    if (C0) C0 += blockIdx.z * bs.c0;
+    C += blockIdx.z * bs.c;
     constexpr int ASZ = BM * kPPitchK, BSZ = BT ? kPBN * kPPitchK : kPBK * kPPitchN;
     constexpr int TM = BM / 16;  // m8 tiles per warp (warp tile (BM/2) x 16)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -563,15 +574,16 @@ __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, do
 
 template <int BM, bool BT, bool G3>
 void zgemm_pipe_launch(cudaStream_t st, int M, int N, int K, double alpha, const double2* A, int64_t lda,
-                       const double2* B, int64_t ldb, const double2* C0, int64_t ldc0, double2* C, int64_t ldc) {
+                       const double2* B, int64_t ldb, const double2* C0, int64_t ldc0, double2* C, int64_t ldc,
+                       GemmStrides bs = {}, int batch = 1) {
     constexpr int smem = zgemm_pipe_smem<BM, BT>();
     static bool attr = false;
     if (!attr) {
         CK(cudaFuncSetAttribute(zgemm_pipe_kernel<BM, BT, G3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
     }
-    zgemm_pipe_kernel<BM, BT, G3><<<dim3((N + kPBN - 1) / kPBN, (M + BM - 1) / BM), 256, smem, st>>>(
-        M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
+    zgemm_pipe_kernel<BM, BT, G3><<<dim3((N + kPBN - 1) / kPBN, (M + BM - 1) / BM, batch), 256, smem, st>>>(
+        M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs);
     CK_LAUNCH();
 }
 
@@ -629,6 +641,31 @@ void cgemm(cudaStream_t st, bool bt, int M, int N, int K, double alpha, const do
            const double2* B, int64_t ldb, const double2* C0, int64_t ldc0, double2* C, int64_t ldc) {
     if (bt) cgemm_launch<true>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
     else cgemm_launch<false>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
+}
+
+void cgemm_batched(cudaStream_t st, bool bt, int M, int N, int K, double alpha, const double2* A, int64_t lda,
+                   int64_t sA, const double2* B, int64_t ldb, int64_t sB, const double2* C0, int64_t ldc0,
+                   int64_t sC0, double2* C, int64_t ldc, int64_t sC, int batch) {
+    if (batch <= 0) return;
+    require(batch <= 65535, "cgemm_batched: batch above 65535");
+    GemmStrides bs;
+    bs.a = sA;
+    bs.b = sB;
+    bs.c0 = sC0;
+    bs.c = sC;
+    // 64-row tiles only when they still give every SM a tile (Gauss's 3-product form)
+    const int64_t tiles64 = int64_t((N + kPBN - 1) / kPBN) * ((M + 63) / 64) * batch;
+    if (bt) {
+        if (tiles64 >= sm_count() && M > 32)
+            zgemm_pipe_launch<64, true, true>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs, batch);
+        else
+            zgemm_pipe_launch<32, true, true>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs, batch);
+    } else {
+        if (tiles64 >= sm_count() && M > 32)
+            zgemm_pipe_launch<64, false, true>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs, batch);
+        else
+            zgemm_pipe_launch<32, false, true>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs, batch);
+    }
 }
 
 void DenseWork::ensure(int nb) {

@@ -11,6 +11,11 @@ constexpr int kDenseBlk = 64;  // Gauss-Jordan block width
 void cgemm(cudaStream_t st, bool bt, int M, int N, int K, double alpha, const double2* A, int64_t lda,
            const double2* B, int64_t ldb, const double2* C0, int64_t ldc0, double2* C, int64_t ldc);
 
+// strided-batched cgemm: for z < batch, C_z = C0_z + alpha A_z B_z with X_z = X + z sX
+void cgemm_batched(cudaStream_t st, bool bt, int M, int N, int K, double alpha, const double2* A, int64_t lda,
+                   int64_t sA, const double2* B, int64_t ldb, int64_t sB, const double2* C0, int64_t ldc0,
+                   int64_t sC0, double2* C, int64_t ldc, int64_t sC, int batch);
+
 struct DenseWork {
     DevBuf<double2> F, Ablk, R, Dinv;
     int nb_ = 0;

@@ -72,10 +72,14 @@ _INT_RE = re.compile(r"-?\d+")
 
 
 def parse_double(tok: str, what: str) -> float:
-    """std::from_chars(double) over the whole token (model_io.cpp:26-32)."""
+    """std::from_chars(double) over the whole token (model_io.cpp:26-32); a finite literal
+    that overflows ('1e400') is result_out_of_range there, a parse error here too."""
     if not _FLOAT_RE.fullmatch(tok):
         raise ParseError(f"bad numeric value for {what}: '{tok}'")
-    return float(tok)
+    v = float(tok)
+    if math.isinf(v) and "inf" not in tok.lower():
+        raise ParseError(f"bad numeric value for {what}: '{tok}'")
+    return v
 
 
 def parse_int(tok: str, what: str) -> int:
@@ -514,6 +518,10 @@ def load_inversion(model_path: str, survey_path: str, data_path: str, config_pat
     # PmlFlags::resolve (tools/fwi.cpp:28-38)
     power = pml_power if pml_power > 0.0 else cfg.pml_power
     c_ref = pml_c_ref if pml_c_ref > 0.0 else (cfg.pml_c_ref if cfg.pml_c_ref is not None else mf.mean_velocity())
+    if not c_ref > 0.0:  # make_pml_profile (src/grid.cpp:21-27)
+        raise ValueError("make_pml_profile: c_ref must be positive")
+    if not power > 0.0:
+        raise ValueError("make_pml_profile: power must be positive")
     grid = Grid(mf.grid.nx, mf.grid.nz, mf.grid.h, mf.grid.n_pml, _sigma_max_of(mf.grid, c_ref), power)
     if pml_sigma_max > 0.0:
         grid.sigma_max = pml_sigma_max
@@ -538,9 +546,21 @@ def _observed_at(inv: Inversion, f: float) -> np.ndarray:
     raise ValueError(f"no observed data at frequency {f}")
 
 
+class InversionAborted(RuntimeError):
+    """fwi_run's incomplete report (FwiReport::completed == false, src/driver.cpp:142-152):
+    raised by invert after the outputs of the completed steps are written (fwi invert exits 4)."""
+
+    def __init__(self, msg: str, steps: list):
+        super().__init__(msg)
+        self.steps = steps
+
+
 def invert(inv: Inversion, out_dir: str) -> list:
-    """fwi_run over the schedule on the device, then cmd_invert's outputs (tools/fwi.cpp:299-337):
-    model_XX.mod (velocity), convergence_XX.csv, misfit.csv, steps.csv, timing.csv."""
+    """fwi_run over the schedule on the device (src/driver.cpp:129-155: a failing step ends the
+    sweep, keeping the completed steps), then cmd_invert's outputs (tools/fwi.cpp:299-337) for
+    the completed steps: model_XX.mod (velocity), heatmap_XX.ppm + .txt, convergence_XX.csv,
+    misfit.csv, steps.csv, timing.csv. Raises InversionAborted after writing them if a step
+    failed."""
     from dataclasses import replace
 
     from . import api
@@ -549,10 +569,14 @@ def invert(inv: Inversion, out_dir: str) -> list:
                          gmres_restart=c.gmres_restart, ilu_level=c.ilu_level, ilu_diag_shift=c.ilu_diag_shift,
                          v_min=c.v_min, v_max=c.v_max, ecg_stride=c.ecg_stride, ecg_stop_tol=c.ecg_stop_tol)
     os.makedirs(out_dir, exist_ok=True)
-    steps, s = [], inv.s0
+    steps, s, error = [], inv.s0, None
     for f in inv.frequencies:
-        q = replace(inv.problem, d_obs=_observed_at(inv, f))
-        r = api.gn_step(q, s, f, inv.epsilons[f], gcfg)
+        try:
+            q = replace(inv.problem, d_obs=_observed_at(inv, f))
+            r = api.gn_step(q, s, f, inv.epsilons[f], gcfg)
+        except Exception as e:  # noqa: BLE001 — fwi_run catches std::exception
+            error = f"step at {f:.6f} Hz failed: {e}"
+            break
         steps.append(r)
         s = r.s
     misfit = ["frequency_hz,resid_norm_ini,resid_norm_fin\n"]
@@ -564,15 +588,120 @@ def invert(inv: Inversion, out_dir: str) -> list:
                     f"{format_double(st.update_relnorm)},{format_double(st.log.final_residual())}\n")
         timing.append(f"{format_double(st.freq_hz)},{st.wall_seconds:.3f}\n")
         tag = f"{i:02d}"
-        write_model(os.path.join(out_dir, f"model_{tag}.mod"),
-                    ModelFile(inv.problem.grid, VELOCITY_MPS, 1.0 / np.sqrt(st.s)))
-        conv = ["iteration,normal_resid,solver_resid,precond_resid\n"]
-        for e in st.log.entries:
-            nr = format_double(e.normal_residual) if e.normal_residual is not None else ""
-            pr = format_double(e.precond_residual) if e.precond_residual is not None else ""
-            conv.append(f"{e.iteration},{nr},{format_double(e.residual_norm)},{pr}\n")
-        atomic_write(os.path.join(out_dir, f"convergence_{tag}.csv"), "".join(conv).encode())
+        vel = 1.0 / np.sqrt(st.s)
+        write_model(os.path.join(out_dir, f"model_{tag}.mod"), ModelFile(inv.problem.grid, VELOCITY_MPS, vel))
+        write_heatmap(os.path.join(out_dir, f"heatmap_{tag}.ppm"), inv.problem.grid, vel)
+        write_convergence_csv(os.path.join(out_dir, f"convergence_{tag}.csv"), st.log)
     atomic_write(os.path.join(out_dir, "misfit.csv"), "".join(misfit).encode())
     atomic_write(os.path.join(out_dir, "steps.csv"), "".join(rows).encode())
     atomic_write(os.path.join(out_dir, "timing.csv"), "".join(timing).encode())
+    if error is not None:
+        raise InversionAborted(error, steps)
     return steps
+
+
+def write_convergence_csv(path: str, log) -> None:
+    """write_convergence_csv (tools/fwi.cpp:45-53)."""
+    conv = ["iteration,normal_resid,solver_resid,precond_resid\n"]
+    for e in log.entries:
+        nr = format_double(e.normal_residual) if e.normal_residual is not None else ""
+        pr = format_double(e.precond_residual) if e.precond_residual is not None else ""
+        conv.append(f"{e.iteration},{nr},{format_double(e.residual_norm)},{pr}\n")
+    atomic_write(path, "".join(conv).encode())
+
+
+def write_timing_csv(path: str, log) -> None:
+    """write_timing_csv (tools/fwi.cpp:55-63)."""
+    out = ["iteration,wall_seconds\n"] + [f"{e.iteration},{e.wall_time:.3f}\n" for e in log.entries]
+    atomic_write(path, "".join(out).encode())
+
+
+# --------------------------------------------------------------------------
+# heatmap and model generators (src/model_io.cpp:383-513)
+# --------------------------------------------------------------------------
+
+_STOPS = ((0, 0, 96), (32, 96, 255), (245, 245, 245), (255, 128, 32), (128, 16, 16))
+
+
+def _colormap(t: float):
+    """The fixed diverging colormap (model_io.cpp:389-401)."""
+    t = min(max(t, 0.0), 1.0)
+    pos = t * 4.0
+    i = min(3, int(pos))
+    f = pos - i
+    a, b = _STOPS[i], _STOPS[i + 1]
+    return tuple(a[c] + f * (b[c] - a[c]) for c in range(3))
+
+
+def write_heatmap(path: str, grid: Grid, node_values) -> None:
+    """write_heatmap (model_io.cpp:405-435): binary PPM of the core, min/max .txt sidecar."""
+    v = np.asarray(node_values, np.float64)
+    if v.size != grid.n:
+        raise ValueError("write_heatmap: value count does not match grid")
+    p = grid.n_pml
+    core = v.reshape(grid.nz, grid.nx)[p:grid.nz - p, p:grid.nx - p]
+    lo, hi = float(core.min()), float(core.max())
+    span = hi - lo if hi > lo else 1.0
+    px = bytearray()
+    for val in core.ravel().tolist():
+        r, g, b = _colormap((val - lo) / span)
+        px += bytes((int(r + 0.5) & 255, int(g + 0.5) & 255, int(b + 0.5) & 255))
+    atomic_write(path, f"P6\n{core.shape[1]} {core.shape[0]}\n255\n".encode() + bytes(px))
+    atomic_write(os.path.splitext(path)[0] + ".txt", f"min {format_double(lo)}\nmax {format_double(hi)}\n".encode())
+
+
+def make_layered_model(grid: Grid, velocities: list, interfaces: list) -> ModelFile:
+    """make_layered_model (model_io.cpp:437-463)."""
+    if not velocities:
+        raise ValueError("make_layered_model: need at least one layer")
+    if len(interfaces) + 1 != len(velocities):
+        raise ValueError("make_layered_model: need one interface fewer than layers")
+    for i, z in enumerate(interfaces):
+        if z <= 0 or z >= grid.nz:
+            raise ValueError("make_layered_model: interface outside the grid")
+        if i > 0 and z <= interfaces[i - 1]:
+            raise ValueError("make_layered_model: interfaces must ascend")
+    if any(not v > 0.0 for v in velocities):
+        raise ValueError("make_layered_model: velocities must be positive")
+    vals = np.empty(grid.n)
+    for iz in range(grid.nz):
+        layer = 0
+        while layer < len(interfaces) and iz >= interfaces[layer]:
+            layer += 1
+        vals[iz * grid.nx:(iz + 1) * grid.nx] = velocities[layer]
+    return ModelFile(grid, VELOCITY_MPS, vals)
+
+
+def make_lens_model(grid: Grid, background: float, amplitude: float, cx: float, cz: float,
+                    radius: float) -> ModelFile:
+    """make_lens_model (model_io.cpp:465-487), the same operations per node."""
+    if not background > 0.0:
+        raise ValueError("make_lens_model: background must be positive")
+    if not radius > 0.0:
+        raise ValueError("make_lens_model: radius must be positive")
+    two_r2 = 2.0 * radius * radius
+    vals = np.empty(grid.n)
+    for iz in range(grid.nz):
+        for ix in range(grid.nx):
+            dx, dz = ix - cx, iz - cz
+            v = background + amplitude * math.exp(-(dx * dx + dz * dz) / two_r2)
+            if not v > 0.0:
+                raise ValueError("make_lens_model: non-positive velocity produced")
+            vals[iz * grid.nx + ix] = v
+    return ModelFile(grid, VELOCITY_MPS, vals)
+
+
+def import_raw_model(grid: Grid, raw_path: str, out_kind: int) -> ModelFile:
+    """import_raw_model (model_io.cpp:489-513): headerless float32 velocities."""
+    try:
+        with open(raw_path, "rb") as f:
+            raw = f.read()
+    except OSError as e:
+        raise IoError(f"cannot open raw model {raw_path}") from e
+    expected = grid.n * 4
+    if len(raw) != expected:
+        raise ParseError(f"raw model: expected {expected} bytes ({grid.n} float32 values), found {len(raw)}")
+    v = np.frombuffer(raw, dtype="<f4").astype(np.float64)
+    if not np.all(np.isfinite(v)) or not np.all(v > 0.0):
+        raise ParseError("raw model: velocities must be finite and positive")
+    return ModelFile(grid, out_kind, v if out_kind == VELOCITY_MPS else 1.0 / (v * v))
