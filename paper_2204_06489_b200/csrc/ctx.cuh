@@ -150,6 +150,14 @@ void gmres_work_free(GmresWork*);
 int64_t exact_bytes(const ExactFactor*);
 double exact_probe_residual(const ExactFactor*);
 
+// ---- bcr.cu (block cyclic reduction, used by exact.cu)
+struct BcrFactor;
+constexpr int kBcrMinLines = 256;  // lines from which cyclic reduction replaces the Schur sweeps
+BcrFactor* bcr_factor(Ctx& c, bool col_lines, int nb, int L, const double2* coup, int* status);
+void bcr_solve(Ctx& c, BcrFactor& f, const double2* coup, double2* W, int nrhs);
+void bcr_free(BcrFactor*);
+int64_t bcr_bytes(const BcrFactor*);
+
 // ---- precond.cu
 void precond_apply(Ctx& c, int mode, const Vec& v, Vec& out);
 void precond_apply_raw(Ctx& c, int mode, const double* v, double* out);

@@ -643,11 +643,179 @@ void cgemm(cudaStream_t st, bool bt, int M, int N, int K, double alpha, const do
     else cgemm_launch<false>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc);
 }
 
+namespace {
+// Split-K strided-batched complex GEMM for a few narrow products (the upper levels of the
+// cyclic reduction: M = nrhs, N = K = nb, batch 1..50, where the tiled kernel leaves most
+// SMs idle and each CTA runs its whole K at one SM's DMMA rate): one warp per 8x8 output
+// tile and K chunk of kc, operands straight from L2 into DMMA fragments (Gauss's three-
+// product form), partial tiles to part[(z S + s)][M][N]; zgemm_splitk_reduce sums them in
+// chunk order (deterministic) and applies alpha and C0.
+template <bool BT>
+__global__ void __launch_bounds__(128) zgemm_splitk_kernel(int M, int N, int K, int kc, int S,
+                                                          const double2* __restrict__ A, int64_t lda, int64_t sA,
+                                                          const double2* __restrict__ B, int64_t ldb, int64_t sB,
+                                                          double2* __restrict__ part) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int n0 = (blockIdx.x * 4 + w) * 8, m0 = blockIdx.y * 8;
+    const int z = blockIdx.z / S, s = blockIdx.z % S;
+    if (n0 >= N) return;
+    A += z * sA;
+    B += z * sB;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int k0 = s * kc, k1 = min(K, k0 + kc);
+    const int m = m0 + g, n = n0 + g;
+    const bool mok = m < M, nok = n < N;
+    double P[2] = {0.0, 0.0}, Q[2] = {0.0, 0.0}, I[2] = {0.0, 0.0};
+#pragma unroll 8
+    for (int k = k0; k < k1; k += 4) {
+        const int kk = k + t4;
+        const bool kok = kk < k1;
+        const double2 a = (mok && kok) ? __ldg(A + int64_t(m) * lda + kk) : make_double2(0.0, 0.0);
+        const double2 b = (nok && kok) ? __ldg(BT ? B + int64_t(n) * ldb + kk : B + int64_t(kk) * ldb + n)
+                                       : make_double2(0.0, 0.0);
+        dmma(P, a.x, b.x);
+        dmma(Q, a.y, b.y);
+        dmma(I, a.x + a.y, b.x + b.y);
+    }
+    double2* out = part + int64_t(blockIdx.z) * M * N;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int mm = m0 + g, nn = n0 + 2 * t4 + e;
+        if (mm < M && nn < N) out[int64_t(mm) * N + nn] = make_double2(P[e] - Q[e], I[e] - P[e] - Q[e]);
+    }
+}
+
+// Up to two products in one launch, for the cyclic-reduction solve levels:
+//   C_z = C0_z + sum_t alpha_t A_{t,z} B_{t,z}    (term t present for z in [lo_t, hi_t))
+// one warp per 8x8 output tile over the whole K (M = nrhs, N = K = nb), operands from L2
+// into DMMA fragments (Gauss's three-product form), C0 read in the epilogue. Fewer launches
+// than one tiled GEMM per product plus reductions, and every SM busy on narrow batches.
+struct Gemm2Term {
+    const double2* A;
+    int64_t lda, sA;
+    const double2* B;
+    int64_t ldb, sB;
+    double alpha;
+    int bt, lo, hi;
+};
+
+__global__ void __launch_bounds__(128) zgemm2_warp_kernel(int M, int N, int K, Gemm2Term t0, Gemm2Term t1,
+                                                         int nterms, const double2* C0, int64_t ldc0, int64_t sC0,
+                                                         double2* C, int64_t ldc, int64_t sC) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int n0 = (blockIdx.x * 4 + w) * 8, m0 = blockIdx.y * 8, z = blockIdx.z;
+    if (n0 >= N) return;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int m = m0 + g, n = n0 + g;
+    const bool mok = m < M, nok = n < N;
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // (re, im) x 2 columns
+    for (int tt = 0; tt < nterms; ++tt) {
+        const Gemm2Term& T = tt == 0 ? t0 : t1;
+        if (z < T.lo || z >= T.hi) continue;
+        const double2* A = T.A + (z - T.lo) * T.sA;
+        const double2* B = T.B + (z - T.lo) * T.sB;
+        double P[2] = {0.0, 0.0}, Q[2] = {0.0, 0.0}, I[2] = {0.0, 0.0};
+        // chunks of 8 k4-steps: the next chunk's 16 loads are issued before this chunk's DMMAs
+        constexpr int CH = 8;
+        double2 ca[CH], cb[CH], na[CH], nb_[CH];
+        auto load = [&](int k0, double2 (&ra)[CH], double2 (&rb)[CH]) {
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                const int kk = k0 + 4 * q + t4;
+                const bool kok = kk < K;
+                ra[q] = (mok && kok) ? __ldg(A + int64_t(m) * T.lda + kk) : make_double2(0.0, 0.0);
+                rb[q] = (nok && kok) ? __ldg(T.bt ? B + int64_t(n) * T.ldb + kk : B + int64_t(kk) * T.ldb + n)
+                                     : make_double2(0.0, 0.0);
+            }
+        };
+        load(0, ca, cb);
+        for (int k0 = 0; k0 < K; k0 += 4 * CH) {
+            if (k0 + 4 * CH < K) load(k0 + 4 * CH, na, nb_);
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                dmma(P, ca[q].x, cb[q].x);
+                dmma(Q, ca[q].y, cb[q].y);
+                dmma(I, ca[q].x + ca[q].y, cb[q].x + cb[q].y);
+            }
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                ca[q] = na[q];
+                cb[q] = nb_[q];
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            acc[e][0] += T.alpha * (P[e] - Q[e]);
+            acc[e][1] += T.alpha * (I[e] - P[e] - Q[e]);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int mm = m0 + g, nn = n0 + 2 * t4 + e;
+        if (mm >= M || nn >= N) continue;
+        double2 v = make_double2(acc[e][0], acc[e][1]);
+        if (C0) {
+            const double2 c = C0[z * sC0 + int64_t(mm) * ldc0 + nn];
+            v.x += c.x;
+            v.y += c.y;
+        }
+        C[z * sC + int64_t(mm) * ldc + nn] = v;
+    }
+}
+
+__global__ void zgemm_splitk_reduce(int M, int N, int S, double alpha, const double2* __restrict__ part,
+                                    const double2* C0, int64_t ldc0, int64_t sC0, double2* C, int64_t ldc,
+                                    int64_t sC) {
+    const int z = blockIdx.y;
+    const int64_t mn = int64_t(M) * N;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < mn; t += int64_t(gridDim.x) * blockDim.x) {
+        const int m = int(t / N), n = int(t % N);
+        double2 acc = make_double2(0.0, 0.0);
+        for (int s = 0; s < S; ++s) {
+            const double2 p = part[(int64_t(z) * S + s) * mn + t];
+            acc.x += p.x;
+            acc.y += p.y;
+        }
+        double2 v = make_double2(alpha * acc.x, alpha * acc.y);
+        if (C0) {
+            const double2 c = C0[z * sC0 + int64_t(m) * ldc0 + n];
+            v.x += c.x;
+            v.y += c.y;
+        }
+        C[z * sC + int64_t(m) * ldc + n] = v;
+    }
+}
+}  // namespace
+
 void cgemm_batched(cudaStream_t st, bool bt, int M, int N, int K, double alpha, const double2* A, int64_t lda,
                    int64_t sA, const double2* B, int64_t ldb, int64_t sB, const double2* C0, int64_t ldc0,
-                   int64_t sC0, double2* C, int64_t ldc, int64_t sC, int batch) {
+                   int64_t sC0, double2* C, int64_t ldc, int64_t sC, int batch, double2* scratch,
+                   size_t scratch_count) {
     if (batch <= 0) return;
     require(batch <= 65535, "cgemm_batched: batch above 65535");
+    // few tiles: split K over warps (see zgemm_splitk_kernel); FWI_CGEMM_SPLITK_CTAS moves the
+    // switch point (tiled CTAs below which the split-K form runs)
+    static const int64_t split_below = std::getenv("FWI_CGEMM_SPLITK_CTAS")
+                                           ? std::atoll(std::getenv("FWI_CGEMM_SPLITK_CTAS"))
+                                           : 2 * int64_t(sm_count());
+    const int64_t ctas32 = int64_t((N + kPBN - 1) / kPBN) * ((M + 31) / 32) * batch;
+    if (scratch && ctas32 < split_below) {
+        const int kc = 32, S = (K + kc - 1) / kc;
+        const size_t need = size_t(batch) * S * size_t(M) * N;
+        if (need <= scratch_count && int64_t(batch) * S <= 65535) {
+            const dim3 g((N + 31) / 32, (M + 7) / 8, unsigned(batch * S));
+            if (bt)
+                zgemm_splitk_kernel<true><<<g, 128, 0, st>>>(M, N, K, kc, S, A, lda, sA, B, ldb, sB, scratch);
+            else
+                zgemm_splitk_kernel<false><<<g, 128, 0, st>>>(M, N, K, kc, S, A, lda, sA, B, ldb, sB, scratch);
+            CK_LAUNCH();
+            const int64_t mn = int64_t(M) * N;
+            zgemm_splitk_reduce<<<dim3(unsigned(std::min<int64_t>((mn + 255) / 256, 64)), unsigned(batch)), 256, 0,
+                                  st>>>(M, N, S, alpha, scratch, C0, ldc0, sC0, C, ldc, sC);
+            CK_LAUNCH();
+            return;
+        }
+    }
     GemmStrides bs;
     bs.a = sA;
     bs.b = sB;
@@ -666,6 +834,30 @@ void cgemm_batched(cudaStream_t st, bool bt, int M, int N, int K, double alpha, 
         else
             zgemm_pipe_launch<32, false, true>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs, batch);
     }
+}
+
+void cgemm2(cudaStream_t st, int M, int N, int K, const CgemmTerm& a, const CgemmTerm* b, const double2* C0,
+            int64_t ldc0, int64_t sC0, double2* C, int64_t ldc, int64_t sC, int batch) {
+    if (batch <= 0) return;
+    require(batch <= 65535, "cgemm2: batch above 65535");
+    auto conv = [](const CgemmTerm& t) {
+        Gemm2Term g;
+        g.A = t.A;
+        g.lda = t.lda;
+        g.sA = t.sA;
+        g.B = t.B;
+        g.ldb = t.ldb;
+        g.sB = t.sB;
+        g.alpha = t.alpha;
+        g.bt = t.bt ? 1 : 0;
+        g.lo = t.lo;
+        g.hi = t.hi;
+        return g;
+    };
+    const Gemm2Term t0 = conv(a), t1 = b ? conv(*b) : t0;
+    const dim3 g((N + 31) / 32, (M + 7) / 8, unsigned(batch));
+    zgemm2_warp_kernel<<<g, 128, 0, st>>>(M, N, K, t0, t1, b ? 2 : 1, C0, ldc0, sC0, C, ldc, sC);
+    CK_LAUNCH();
 }
 
 void DenseWork::ensure(int nb) {

@@ -11,10 +11,28 @@ constexpr int kDenseBlk = 64;  // Gauss-Jordan block width
 void cgemm(cudaStream_t st, bool bt, int M, int N, int K, double alpha, const double2* A, int64_t lda,
            const double2* B, int64_t ldb, const double2* C0, int64_t ldc0, double2* C, int64_t ldc);
 
-// strided-batched cgemm: for z < batch, C_z = C0_z + alpha A_z B_z with X_z = X + z sX
+// strided-batched cgemm: for z < batch, C_z = C0_z + alpha A_z B_z with X_z = X + z sX.
+// scratch (scratch_count complex): partial tiles of the split-K form used for few tiles;
+// without it the tiled kernel always runs.
 void cgemm_batched(cudaStream_t st, bool bt, int M, int N, int K, double alpha, const double2* A, int64_t lda,
                    int64_t sA, const double2* B, int64_t ldb, int64_t sB, const double2* C0, int64_t ldc0,
-                   int64_t sC0, double2* C, int64_t ldc, int64_t sC, int batch);
+                   int64_t sC0, double2* C, int64_t ldc, int64_t sC, int batch, double2* scratch = nullptr,
+                   size_t scratch_count = 0);
+
+// One term of cgemm2: alpha A_z B_z (B transposed when bt) for batch entries z in [lo, hi),
+// the operands at A + (z - lo) sA, B + (z - lo) sB.
+struct CgemmTerm {
+    const double2* A;
+    int64_t lda, sA;
+    const double2* B;
+    int64_t ldb, sB;
+    double alpha;
+    bool bt;
+    int lo, hi;
+};
+// C_z = C0_z + term a (+ term b), z < batch: up to two products in one launch (warp tiles)
+void cgemm2(cudaStream_t st, int M, int N, int K, const CgemmTerm& a, const CgemmTerm* b, const double2* C0,
+            int64_t ldc0, int64_t sC0, double2* C, int64_t ldc, int64_t sC, int batch);
 
 struct DenseWork {
     DevBuf<double2> F, Ablk, R, Dinv;

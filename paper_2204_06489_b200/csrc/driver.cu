@@ -52,6 +52,9 @@ void gn_step(const fwi_state_desc& d0, const fwi_gn_options& o, double* s_out, f
     d.u = nullptr;  // linearisation: fields from the device's own forward solves
     d.r = nullptr;
     d.exact_factor = 1;
+    // make_gn_state builds the ILU factors only for the ILU solver (src/driver.cpp:78-83), and
+    // IluFactors::factor rejects a negative fill level (src/ilu.cpp:9-10)
+    require(o.solver != FWI_SOLVER_FSGN_ILU || o.ilu_level >= 0, "IluFactors::factor: fill level must be >= 0");
     d.ilu_level = o.solver == FWI_SOLVER_FSGN_ILU ? o.ilu_level : -1;
     d.ilu_diag_shift = o.ilu_diag_shift;
     std::unique_ptr<Ctx> c(ctx_create(d));

@@ -59,6 +59,7 @@ struct ExactFactor {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     DenseWork dwork2;
     DevBuf<double2> tbuf2;
+    BcrFactor* bcr = nullptr;  // block cyclic reduction (bcr.cu) instead of the Schur sweeps
     void ensure_side() {
         if (s2) return;
         CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
@@ -66,6 +67,7 @@ struct ExactFactor {
         CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     }
     ~ExactFactor() {
+        if (bcr) bcr_free(bcr);
         if (s2) {
             cudaStreamSynchronize(s2);
             cudaStreamDestroy(s2);
@@ -76,7 +78,9 @@ struct ExactFactor {
 };
 
 void exact_free(ExactFactor* f) { delete f; }
-int64_t exact_bytes(const ExactFactor* f) { return f ? int64_t(f->G.bytes() + f->coup.bytes()) : 0; }
+int64_t exact_bytes(const ExactFactor* f) {
+    return f ? int64_t(f->G.bytes() + f->coup.bytes()) + bcr_bytes(f->bcr) : 0;
+}
 
 namespace {
 
@@ -1249,6 +1253,12 @@ size_t sweep_smem(int nb) {
 
 }  // namespace
 
+// cyclic reduction for nb-node lines, L of them (FWI_EXACT_BCR=1|0 forces it on or off)
+static bool bcr_wanted(bool line_pivot, int nb, int L) {
+    const char* eb = std::getenv("FWI_EXACT_BCR");
+    return !line_pivot && nb <= 512 && L >= 2 && (eb ? std::string(eb) == "1" : (L >= kBcrMinLines && nb >= 32));
+}
+
 // line_pivot: factor every line with the one-CTA Gauss-Jordan, partial pivoting over the
 // whole line (the fallback when the residual probe rejects the block Gauss-Jordan, whose
 // pivot search is restricted to 64-wide diagonal blocks)
@@ -1266,8 +1276,9 @@ static void exact_factor_once(Ctx& c, bool line_pivot) {
         WarpPlan ps, pl;
         if (o == "long" && nbl <= 512) {
             f->col_lines = !f->col_lines;
-        } else if (o.empty() && nbl <= 512 && nbs != nbl && warp_plan(nbs, nbl, nbs + 1, c.K, ps) &&
-                   warp_plan(nbl, nbs, nbl + 1, c.K, pl) && pl.est < 0.9 * ps.est) {
+        } else if (o.empty() && nbl <= 512 && nbs != nbl && !bcr_wanted(line_pivot, nbs, nbl) &&
+                   warp_plan(nbs, nbl, nbs + 1, c.K, ps) && warp_plan(nbl, nbs, nbl + 1, c.K, pl) &&
+                   pl.est < 0.9 * ps.est) {
             f->col_lines = !f->col_lines;
         }
     }
@@ -1276,13 +1287,20 @@ static void exact_factor_once(Ctx& c, bool line_pivot) {
     const int nb = f->nb, L = f->L;
     require(nb <= 2048, "exact block factorisation: line length above 2048 is not supported");
     f->gp = nb + 1;
-    f->G.alloc(size_t(L) * nb * f->gp);
     f->coup.alloc(size_t(L) * nb);
     f->status.alloc(1);
     CK(cudaMemsetAsync(f->status.p, 0, sizeof(int), c.stream));
     extract_lines<<<grid_blocks(int64_t(L) * nb, 256, 1 << 20), 256, 0, c.stream>>>(
         f->col_lines, c.nx, L, nb, c.east.p, c.south.p, f->coup.p);
     CK_LAUNCH();
+    // Block cyclic reduction (bcr.cu) when the line chain is long: a Schur sweep is 2L
+    // latency-bound line steps, cyclic reduction log2 L levels of batched tensor-core GEMMs.
+    // FWI_EXACT_BCR=1|0 forces it on or off (diagnostics).
+    {
+        if (bcr_wanted(line_pivot, nb, L)) f->bcr = bcr_factor(c, f->col_lines, nb, L, f->coup.p, f->status.p);
+    }
+    if (!f->bcr) {
+    f->G.alloc(size_t(L) * nb * f->gp);
     // Sweeps: GEMM per line beyond the cluster kernel's reach (nb > 512). Factor: the
     // whole-GPU block Gauss-Jordan whenever a line does not fit one CTA's shared memory
     // (nb > 112; ~8x faster than the one-CTA global-memory Gauss-Jordan at nb = 128).
@@ -1375,12 +1393,13 @@ static void exact_factor_once(Ctx& c, bool line_pivot) {
         CK_LAUNCH();
     }
     }
+    }  // !f->bcr
     int st = 0;
     CK(cudaMemcpyAsync(&st, f->status.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
     if (std::getenv("FWI_EXACT_PLAN_LOG"))
-        std::fprintf(stderr, "[fwi] exact factor nb=%d L=%d dense=%d twisted=%d: %.3f s\n", nb, L, int(f->dense),
-                     int(f->twisted),
+        std::fprintf(stderr, "[fwi] exact factor nb=%d L=%d dense=%d twisted=%d bcr=%d: %.3f s\n", nb, L,
+                     int(f->dense), int(f->twisted), int(f->bcr != nullptr),
                      std::chrono::duration<double>(std::chrono::steady_clock::now() - t_host0).count());
     if (st != 0) {
         // status = line * nb + (position in the line) + 1. Reported as the grid node, the
@@ -1507,7 +1526,11 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
     gather_lines<<<tg, tb, 0, c.stream>>>(f.col_lines, c.nx, c.nz, f.L, f.nb, nrhs, adjoint, b, W);
     CK_LAUNCH();
     bool done = false;
-    if (f.dense) {
+    if (f.bcr) {
+        bcr_solve(c, *f.bcr, f.coup.p, W, nrhs);
+        done = true;
+    }
+    if (!done && f.dense) {
         ExactFactor& fm = const_cast<ExactFactor&>(f);
         if (fm.tbuf.count < size_t(nrhs) * f.nb) fm.tbuf.alloc(size_t(nrhs) * f.nb);
         if (f.twisted) {
@@ -1520,6 +1543,7 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
         done = true;
     }
     const char* sw = std::getenv("FWI_EXACT_SWEEP");  // "warp" (default) | "cta" | "legacy"
+    if (done) sw = "none";
     const std::string sweep = sw ? sw : "warp";
     if (!done && sweep == "warp") {
         // plans are cached per (nb, L, nrhs) (the model queries cluster occupancy);
@@ -1608,7 +1632,7 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
             }
         }
     }
-    if (!done && sweep != "legacy") {
+    if (!done && sweep != "legacy" && sweep != "none") {
         ClusterPlan cp;
         if (cluster_plan(f.nb, f.L, f.gp, nrhs, cp)) {
             cp.a.G = f.G.p;
@@ -1627,7 +1651,7 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
             }
         }
     }
-    if (!done) {
+    if (!done && sweep != "none") {
         sweep_kernel<kSweepKG><<<(nrhs + kSweepKG - 1) / kSweepKG, 256, sweep_smem(f.nb), c.stream>>>(
             f.L, f.nb, nrhs, f.G.p, f.gp, f.coup.p, W);
         CK_LAUNCH();

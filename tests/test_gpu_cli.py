@@ -43,9 +43,15 @@ def test_simulate_compare_invert_from_files(tmp_path):
         want = po.ref_simulate(p, p.s)
         assert np.linalg.norm(b - want) <= 1e-10 * np.linalg.norm(want)
     out = d / "cmp"
+    # compare-solvers takes epsilon_for(0, 1): an epsilon_list must hold one value (as the
+    # reference's cmd_compare, which rejects the two-value list with exit code 3)
     assert cli.main(["compare-solvers", "--initial", str(d / "init.mod"), "--survey", str(d / "s.svy"),
                      "--data", str(d / "obs.csv"), "--freq", "2", "--out", str(out), "--ilu-levels", "0,3",
-                     "--config", str(d / "c.cfg")]) == 0
+                     "--config", str(d / "c.cfg")]) == 3
+    (d / "c1.cfg").write_text("epsilon_start = 1e-3\nepsilon_end = 1e-3\nmax_inner = 20\ninner_tol = 1e-6\n")
+    assert cli.main(["compare-solvers", "--initial", str(d / "init.mod"), "--survey", str(d / "s.svy"),
+                     "--data", str(d / "obs.csv"), "--freq", "2", "--out", str(out), "--ilu-levels", "0,3",
+                     "--config", str(d / "c1.cfg")]) == 0
     for tag in ("cg", "gmres_full", "gmres_ilu_p0", "gmres_ilu_p3"):
         assert (out / f"convergence_{tag}.csv").exists() and (out / f"update_{tag}.f64").exists()
     assert (out / "summary.csv").read_text().startswith('metric,"CG","GMRes-full"')

@@ -211,3 +211,41 @@ def test_host_basis_returns_the_device_mode_solution(mode, restart, maxit):
     assert log_h.residuals() == log_dev.residuals() and log_h.stagnated == log_dev.stagnated
     assert log_h.stagnated == log_r.stagnated
     assert np.linalg.norm(np.asarray(ds_h) - np.asarray(ds_r)) <= 1e-6 * np.linalg.norm(np.asarray(ds_r))
+
+
+@pytest.mark.parametrize("mk", [lambda: small_problem(nx=40, nz=26, n_pml=4, K=3, R=5),
+                                lambda: small_problem(nx=22, nz=37, n_pml=3, K=2, R=4, seed=5),
+                                lambda: small_problem(nx=31, nz=23, n_pml=4, K=9, R=7, seed=3),
+                                lambda: small_problem(nx=150, nz=130, n_pml=8, K=3, R=6)])
+def test_cyclic_reduction_matches_reference(mk, monkeypatch):
+    """Block cyclic reduction (csrc/bcr.cu; forced with FWI_EXACT_BCR=1: odd and even line
+    counts, both orientations, nb > 112) against the reference LU (src/lu.cpp:168-209)."""
+    monkeypatch.setenv("FWI_EXACT_BCR", "1")
+    p = mk()
+    ref = po.Ref(p, full=False, exact=True)
+    dev = fw.GnState(p, exact=True)
+    assert dev.exact_probe_residual <= 1e-11
+    rng = np.random.default_rng(17)
+    b = rng.standard_normal(p.n) + 1j * rng.standard_normal(p.n)
+    for adj in (False, True):
+        want = ref.solve(b, _abi.FWI_PRECOND_EXACT, adj)
+        got = dev.solve(b, fw.PrecondMode.exact, adj)
+        assert rel(got, want) <= 1e-10, (adj, rel(got, want))
+
+
+def test_cyclic_reduction_gmres_history_c1(monkeypatch):
+    """The history gate (50 iterations, restart crossed, every entry) with the exact
+    preconditioner's block solves by cyclic reduction."""
+    monkeypatch.setenv("FWI_EXACT_BCR", "1")
+    p = c1_problem()
+    p.d_obs = po.ref_simulate(p)
+    ref = po.Ref(p, full=True, exact=True)
+    q = c1_problem()
+    q.d_obs, q.u, q.r = p.d_obs, ref.u(), ref.residual()
+    dev = fw.GnState(q, exact=True)
+    _, log_r = ref.fsgn(_abi.FWI_PRECOND_EXACT, 30, 0.0, 50, 0)
+    _, log_d = fw.fsgn_gmres_step(dev, fw.FsgnOptions(restart=30, tol=0.0, maxit=50, ecg_stride=0))
+    rr, rd = np.array(log_r.residuals()), np.array(log_d.residuals())
+    assert len(rr) == len(rd) == 51
+    print("cyclic reduction history deviation", (np.abs(rd - rr) / rr).max())
+    assert (np.abs(rd - rr) / rr).max() <= 1e-8
