@@ -260,6 +260,10 @@ typedef struct fwi_gn_options {
 
 typedef struct fwi_gn_result {
     double misfit_ini, misfit_fin, update_relnorm, wall_seconds;
+    /* split of wall_seconds: linearisation (assembly, exact factorisation, forward solves,
+     * ILU(p)), of which the host ILU(p) factorisation; the Krylov solve; the re-solve at the
+     * updated model */
+    double setup_seconds, ilu_factor_seconds, krylov_seconds, final_seconds;
 } fwi_gn_result;
 
 int fwi_dev_gn_step(const fwi_state_desc* desc, const fwi_gn_options* opt, double* s_out,

@@ -73,7 +73,8 @@ class GnOptions(C.Structure):
 
 class GnResult(C.Structure):
     _fields_ = [("misfit_ini", C.c_double), ("misfit_fin", C.c_double), ("update_relnorm", C.c_double),
-                ("wall_seconds", C.c_double)]
+                ("wall_seconds", C.c_double), ("setup_seconds", C.c_double), ("ilu_factor_seconds", C.c_double),
+                ("krylov_seconds", C.c_double), ("final_seconds", C.c_double)]
 
 
 class LogEntry(C.Structure):

@@ -529,6 +529,10 @@ class GnStepResult:
     misfit_fin: float
     update_relnorm: float
     wall_seconds: float
+    setup_seconds: float = 0.0       # linearisation (incl. the host ILU(p) factorisation)
+    ilu_factor_seconds: float = 0.0
+    krylov_seconds: float = 0.0
+    final_seconds: float = 0.0       # re-solve at the updated model
 
 
 def gn_step(problem: Problem, s: np.ndarray, freq_hz: float, epsilon: float, config: FwiConfig = FwiConfig()):
@@ -549,7 +553,8 @@ def gn_step(problem: Problem, s: np.ndarray, freq_hz: float, epsilon: float, con
     lb = _abi.LogBuffer(config.max_inner + 2)
     _check(lib().fwi_dev_gn_step(C.byref(d), C.byref(o), _p(s_out), C.byref(res), C.byref(lb.c)))
     return GnStepResult(freq_hz, epsilon, s_out, lb.to_log(), res.misfit_ini, res.misfit_fin,
-                        res.update_relnorm, res.wall_seconds)
+                        res.update_relnorm, res.wall_seconds, res.setup_seconds, res.ilu_factor_seconds,
+                        res.krylov_seconds, res.final_seconds)
 
 
 def fwi_run(problem: Problem, observed: dict, s0: np.ndarray, epsilons: dict, config: FwiConfig = FwiConfig(),

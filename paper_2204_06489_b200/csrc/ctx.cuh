@@ -59,6 +59,7 @@ struct Ctx {
     IluFactor* ilu = nullptr;      // owned (ilu_free)
     GmresWork* gmres_work = nullptr;  // owned (gmres_work_free): Krylov buffers reused across solves
     int64_t solve_count[2] = {0, 0};
+    double t_ilu_factor = 0.0;  // host ILU(p) factorisation time of the current factors, s
     KktPlan* kplan[2] = {nullptr, nullptr};      // tile-TMA apply plans (c128, c64), built lazily
     KktKmPlan* kmplan[2] = {nullptr, nullptr};   // source-major TMA apply plans (c128, c64), built lazily
     // 0: source-major TMA kernel (falling back to the tile-TMA kernel, then the plain kernel),

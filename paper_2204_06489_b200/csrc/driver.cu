@@ -58,6 +58,9 @@ void gn_step(const fwi_state_desc& d0, const fwi_gn_options& o, double* s_out, f
     d.ilu_level = o.solver == FWI_SOLVER_FSGN_ILU ? o.ilu_level : -1;
     d.ilu_diag_shift = o.ilu_diag_shift;
     std::unique_ptr<Ctx> c(ctx_create(d));
+    const auto t1 = std::chrono::steady_clock::now();
+    res->setup_seconds = std::chrono::duration<double>(t1 - t0).count();
+    res->ilu_factor_seconds = c->t_ilu_factor;
     const int nd = c->ndata, n = c->n;
     const auto* obs = reinterpret_cast<const std::complex<double>*>(d0.d_obs);
     res->misfit_ini = relative_misfit(dpred_of(*c), obs, nd);
@@ -75,6 +78,8 @@ void gn_step(const fwi_state_desc& d0, const fwi_gn_options& o, double* s_out, f
     else
         fsgn_gmres_step(*c, fo, ds.data(), log);
     c.reset();
+    const auto t2 = std::chrono::steady_clock::now();
+    res->krylov_seconds = std::chrono::duration<double>(t2 - t1).count();
 
     // clamp (src/driver.cpp:108-113)
     const double s_lo = 1.0 / (o.v_max * o.v_max), s_hi = 1.0 / (o.v_min * o.v_min);
@@ -94,7 +99,9 @@ void gn_step(const fwi_state_desc& d0, const fwi_gn_options& o, double* s_out, f
     d2.ilu_level = -1;
     std::unique_ptr<Ctx> c2(ctx_create(d2));
     res->misfit_fin = relative_misfit(dpred_of(*c2), obs, nd);
-    res->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    const auto t3 = std::chrono::steady_clock::now();
+    res->final_seconds = std::chrono::duration<double>(t3 - t2).count();
+    res->wall_seconds = std::chrono::duration<double>(t3 - t0).count();
 }
 
 }  // namespace fwi_b200

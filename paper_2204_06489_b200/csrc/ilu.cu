@@ -18,6 +18,7 @@
 // memory (config 1), or in a ring indexed by level-ordered position when it
 // is too large (config 3/4: operands lie < 700 positions behind their rows).
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <complex>
 #include <cstdio>
@@ -690,6 +691,7 @@ void run_sweep(const Sweep& s, int64_t n, int nrhs, double2* x, cudaStream_t st,
 
 void ilu_factor(Ctx& c, int level, double shift) {
     require(level >= 0, "IluFactors::factor: fill level must be >= 0");
+    const auto t_start = std::chrono::steady_clock::now();
     std::vector<int> arp, aci;
     std::vector<cplx> ava;
     host_csr(c, arp, aci, ava);
@@ -792,6 +794,7 @@ void ilu_factor(Ctx& c, int level, double shift) {
     CK(cudaMemsetAsync(f->zslot.p, 0, sizeof(double2), c.stream));
     if (c.ilu) ilu_free(c.ilu);
     c.ilu = f.release();
+    c.t_ilu_factor = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
 }
 
 // x = M^{-1} b (or M^{-H} b) for nrhs source-major right-hand sides.

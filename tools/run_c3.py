@@ -60,6 +60,8 @@ for r in rep:
     rows.append({"freq_hz": r.freq_hz, "outer_iterations": r.log.iterations(), "converged": r.log.converged,
                  "final_residual": r.log.final_residual(), "misfit_ini": r.misfit_ini, "misfit_fin": r.misfit_fin,
                  "update_relnorm": r.update_relnorm, "newton_step_s": r.wall_seconds,
+                 "setup_s": r.setup_seconds, "host_ilu_factor_s": r.ilu_factor_seconds,
+                 "krylov_s": r.krylov_seconds, "final_resolve_s": r.final_seconds,
                  "model_err_rel": float(np.linalg.norm(v - vt) / np.linalg.norm(vt)),
                  "inner_iterations": 0})
 v0 = 1.0 / np.sqrt(p.s)
