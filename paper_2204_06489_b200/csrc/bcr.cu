@@ -55,6 +55,11 @@ struct BcrFactor {
 };
 
 void bcr_free(BcrFactor* f) { delete f; }
+
+// one-product levels of at least this many blocks use the tiled DMMA kernel (shared-memory
+// operand reuse), narrower ones the warp-tile kernel (every SM busy)
+constexpr int kBcrTiledBatch = 64;
+constexpr int kBcrTiledBatch2 = 64;  // the same for the two-product levels (two tiled launches)
 int64_t bcr_bytes(const BcrFactor* f) {
     return f ? int64_t(f->store.bytes() + f->t.bytes() + f->r.bytes() + f->part.bytes()) : 0;
 }
@@ -420,27 +425,30 @@ void bcr_solve(Ctx& c, BcrFactor& f, const double2* coup, double2* W, int nrhs) 
         f.part.alloc(size_t(std::min(f.lv[0].ne, 2 * sm_count())) * size_t((nb + 31) / 32) * size_t(blk));
         f.nrhs_cap = nrhs;
     }
+
     const cudaStream_t st = c.stream;
     double2* T = f.t.p;
     auto Wl = [&](const BcrLevel& v, int j) { return W + int64_t(v.line0 + j * v.step) * blk; };
     // FWI_BCR_GEMM=tiled: the tiled DMMA kernel for the t = M b products (diagnostics)
     static const bool tiled = std::getenv("FWI_BCR_GEMM") && std::string(std::getenv("FWI_BCR_GEMM")) == "tiled";
+    static const bool warp_only = std::getenv("FWI_BCR_GEMM") && std::string(std::getenv("FWI_BCR_GEMM")) == "warp";
     auto term = [](const double2* A, int64_t sA, const double2* B, int64_t sB, double alpha, bool bt, int lo, int hi,
                    int nb_) {
         return CgemmTerm{A, nb_, sA, B, nb_, sB, alpha, bt, lo, hi};
     };
+    auto emit = [&](const CgemmTerm& ta, const CgemmTerm* tb, const double2* C0, int64_t sC0, double2* C, int64_t sC,
+                    int batch) { cgemm2(st, nrhs, nb, nb, ta, tb, C0, nb, sC0, C, nb, sC, batch); };
     // down
     for (size_t l = 0; l < f.lv.size(); ++l) {
         const BcrLevel& v = f.lv[l];
         double2* Tl = T + v.t_off * blk;
         const int64_t sw = 2 * int64_t(v.step) * blk;  // W stride between same-parity blocks
         // t_b = M_b b_{2b} (rows k of b times M^T)
-        if (tiled)
+        if (tiled || (v.ne >= kBcrTiledBatch && !warp_only))
             cgemm_batched(st, true, nrhs, nb, nb, 1.0, Wl(v, 0), nb, sw, v.M, nb, nn, nullptr, 0, 0, Tl, nb, blk, v.ne,
                           f.part.p, f.part.count);
         else
-            cgemm2(st, nrhs, nb, nb, term(Wl(v, 0), sw, v.M, nn, 1.0, true, 0, v.ne, nb), nullptr, nullptr, 0, 0, Tl,
-                   nb, blk, v.ne);
+            emit(term(Wl(v, 0), sw, v.M, nn, 1.0, true, 0, v.ne, nb), nullptr, nullptr, 0, Tl, blk, v.ne);
         if (v.no == 0) break;
         if (l == 0) {
             l0_down<<<ew_grid(blk, v.no), 256, 0, st>>>(nb, v.m, blk, coup, Tl, W);
@@ -448,9 +456,17 @@ void bcr_solve(Ctx& c, BcrFactor& f, const double2* coup, double2* W, int nrhs) 
         } else {
             // b_{2b+1} -= U_{2b}^T t_b (rows: t_b U_{2b}) + U_{2b+1} t_{b+1} (rows: t_{b+1} U_{2b+1}^T)
             const int np = std::min(v.no, v.ne - 1);
-            const CgemmTerm ta = term(Tl, blk, v.U, 2 * nn, -1.0, false, 0, v.no, nb);
-            const CgemmTerm tb = term(Tl + blk, blk, v.U + nn, 2 * nn, -1.0, true, 0, np, nb);
-            cgemm2(st, nrhs, nb, nb, ta, np > 0 ? &tb : nullptr, Wl(v, 1), nb, sw, Wl(v, 1), nb, sw, v.no);
+            if (v.no >= kBcrTiledBatch2 && !warp_only) {
+                cgemm_batched(st, false, nrhs, nb, nb, -1.0, Tl, nb, blk, v.U, nb, 2 * nn, Wl(v, 1), nb, sw, Wl(v, 1),
+                              nb, sw, v.no, f.part.p, f.part.count);
+                if (np > 0)
+                    cgemm_batched(st, true, nrhs, nb, nb, -1.0, Tl + blk, nb, blk, v.U + nn, nb, 2 * nn, Wl(v, 1), nb,
+                                  sw, Wl(v, 1), nb, sw, np, f.part.p, f.part.count);
+            } else {
+                const CgemmTerm ta = term(Tl, blk, v.U, 2 * nn, -1.0, false, 0, v.no, nb);
+                const CgemmTerm tb = term(Tl + blk, blk, v.U + nn, 2 * nn, -1.0, true, 0, np, nb);
+                emit(ta, np > 0 ? &tb : nullptr, Wl(v, 1), sw, Wl(v, 1), sw, v.no);
+            }
         }
     }
     // up
@@ -466,19 +482,32 @@ void bcr_solve(Ctx& c, BcrFactor& f, const double2* coup, double2* W, int nrhs) 
                 CK(cudaMemsetAsync(f.r.p, 0, size_t(blk) * sizeof(double2), st));
             }
             // x_{2b} = t_b - R_b M_b^T
-            cgemm2(st, nrhs, nb, nb, term(f.r.p, blk, v.M, nn, -1.0, true, 0, v.ne, nb), nullptr, Tl, nb, blk, Wl(v, 0),
-                   nb, sw, v.ne);
+            if (v.ne >= kBcrTiledBatch && !warp_only)
+                cgemm_batched(st, true, nrhs, nb, nb, -1.0, f.r.p, nb, blk, v.M, nb, nn, Tl, nb, blk, Wl(v, 0), nb, sw,
+                              v.ne, f.part.p, f.part.count);
+            else
+                cgemm2(st, nrhs, nb, nb, term(f.r.p, blk, v.M, nn, -1.0, true, 0, v.ne, nb), nullptr, Tl, nb, blk,
+                       Wl(v, 0), nb, sw, v.ne);
         } else {
             // x_{2b} = t_b - x_{2b-1} P_b^T (b >= 1) - x_{2b+1} Q_b^T (2b+1 < m)
             const int nq = v.m / 2;
+            if (v.ne >= kBcrTiledBatch2 && !warp_only) {  // copy t, then both products in place
+                copy_blocks<<<ew_grid(blk, v.ne), 256, 0, st>>>(blk, v.ne, Tl, blk, Wl(v, 0), sw);
+                CK_LAUNCH();
+                if (v.ne > 1)
+                    cgemm_batched(st, true, nrhs, nb, nb, -1.0, Wl(v, 1), nb, sw, v.P + nn, nb, nn, Wl(v, 2), nb, sw,
+                                  Wl(v, 2), nb, sw, v.ne - 1, f.part.p, f.part.count);
+                if (nq > 0)
+                    cgemm_batched(st, true, nrhs, nb, nb, -1.0, Wl(v, 1), nb, sw, v.Q, nb, nn, Wl(v, 0), nb, sw, Wl(v, 0),
+                                  nb, sw, nq, f.part.p, f.part.count);
+                continue;
+            }
             const CgemmTerm tp = term(Wl(v, 1), sw, v.P + nn, nn, -1.0, true, 1, v.ne, nb);
             const CgemmTerm tq = term(Wl(v, 1), sw, v.Q, nn, -1.0, true, 0, nq, nb);
             if (v.ne > 1)
-                cgemm2(st, nrhs, nb, nb, tp, nq > 0 ? &tq : nullptr, Tl, nb, blk, Wl(v, 0), nb, sw, v.ne);
-            else if (nq > 0)
-                cgemm2(st, nrhs, nb, nb, tq, nullptr, Tl, nb, blk, Wl(v, 0), nb, sw, v.ne);
+                emit(tp, nq > 0 ? &tq : nullptr, Tl, blk, Wl(v, 0), sw, v.ne);
             else
-                cgemm2(st, nrhs, nb, nb, tq, nullptr, Tl, nb, blk, Wl(v, 0), nb, sw, v.ne);  // tq empty: x = t
+                emit(tq, nullptr, Tl, blk, Wl(v, 0), sw, v.ne);  // (tq empty when nq = 0: x = t)
         }
     }
 }

@@ -699,12 +699,10 @@ struct Gemm2Term {
     int bt, lo, hi;
 };
 
-__global__ void __launch_bounds__(128) zgemm2_warp_kernel(int M, int N, int K, Gemm2Term t0, Gemm2Term t1,
-                                                         int nterms, const double2* C0, int64_t ldc0, int64_t sC0,
-                                                         double2* C, int64_t ldc, int64_t sC) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int n0 = (blockIdx.x * 4 + w) * 8, m0 = blockIdx.y * 8, z = blockIdx.z;
-    if (n0 >= N) return;
+// one 8x8 output tile (rows m0.., columns n0.., batch entry z) of C_z = C0_z + sum_t alpha_t A B
+__device__ __forceinline__ void zgemm2_tile(int M, int N, int K, const Gemm2Term& t0, const Gemm2Term& t1, int nterms,
+                                            const double2* C0, int64_t ldc0, int64_t sC0, double2* C, int64_t ldc,
+                                            int64_t sC, int m0, int n0, int z, int lane) {
     const int g = lane >> 2, t4 = lane & 3;
     const int m = m0 + g, n = n0 + g;
     const bool mok = m < M, nok = n < N;
@@ -761,6 +759,15 @@ __global__ void __launch_bounds__(128) zgemm2_warp_kernel(int M, int N, int K, G
         }
         C[z * sC + int64_t(mm) * ldc + nn] = v;
     }
+}
+
+__global__ void __launch_bounds__(128) zgemm2_warp_kernel(int M, int N, int K, Gemm2Term t0, Gemm2Term t1,
+                                                         int nterms, const double2* C0, int64_t ldc0, int64_t sC0,
+                                                         double2* C, int64_t ldc, int64_t sC) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int n0 = (blockIdx.x * 4 + w) * 8, m0 = blockIdx.y * 8, z = blockIdx.z;
+    if (n0 >= N) return;
+    zgemm2_tile(M, N, K, t0, t1, nterms, C0, ldc0, sC0, C, ldc, sC, m0, n0, z, lane);
 }
 
 __global__ void zgemm_splitk_reduce(int M, int N, int S, double alpha, const double2* __restrict__ part,
@@ -821,7 +828,15 @@ void cgemm_batched(cudaStream_t st, bool bt, int M, int N, int K, double alpha, 
     bs.b = sB;
     bs.c0 = sC0;
     bs.c = sC;
+    // 48-row tiles for 48 rows (config 3's 48 right-hand sides: no padded rows); otherwise
     // 64-row tiles only when they still give every SM a tile (Gauss's 3-product form)
+    if (M == 48) {
+        if (bt)
+            zgemm_pipe_launch<48, true, true>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs, batch);
+        else
+            zgemm_pipe_launch<48, false, true>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs, batch);
+        return;
+    }
     const int64_t tiles64 = int64_t((N + kPBN - 1) / kPBN) * ((M + 63) / 64) * batch;
     if (bt) {
         if (tiles64 >= sm_count() && M > 32)

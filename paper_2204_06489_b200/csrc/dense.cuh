@@ -1,6 +1,8 @@
 // dense.cuh — whole-GPU dense kernels of the long-line exact solver (dense.cu).
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace fwi_b200 {
