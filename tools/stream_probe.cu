@@ -35,21 +35,24 @@ int main() {
     cudaMalloc(&o1, m * 16); cudaMalloc(&o2, m * 16);
     cudaMemset(a, 0, m * 16); cudaMemset(b, 0, m * 16); cudaMemset(c, 0, m * 16);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    int grids[] = {148 * 4, 148 * 8, 148 * 16, 148 * 32};
-    for (int g : grids) {
-        for (int rep = 0; rep < 3; ++rep) mix<<<g, 256>>>(a, b, c, o1, o2, m);
+    // (grid, block): one 512-thread CTA per SM is the source-major K1's shape
+    int grids[][2] = {{148, 512}, {144, 512}, {296, 512}, {148, 1024}, {148 * 4, 256}, {148 * 8, 256},
+                      {148 * 16, 256}, {148 * 32, 256}};
+    for (auto& gb : grids) {
+        const int g = gb[0], bs = gb[1];
+        for (int rep = 0; rep < 3; ++rep) mix<<<g, bs>>>(a, b, c, o1, o2, m);
         cudaEventRecord(e0);
-        for (int rep = 0; rep < 20; ++rep) mix<<<g, 256>>>(a, b, c, o1, o2, m);
+        for (int rep = 0; rep < 20; ++rep) mix<<<g, bs>>>(a, b, c, o1, o2, m);
         cudaEventRecord(e1); cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 20;
-        printf("mix3r2w grid %5d: %.4f ms  %.0f GB/s\n", g, ms, 5.0 * m * 16 / ms / 1e6);
+        printf("mix3r2w grid %5d x %4d: %.4f ms  %.0f GB/s\n", g, bs, ms, 5.0 * m * 16 / ms / 1e6);
         cudaEventRecord(e0);
-        for (int rep = 0; rep < 20; ++rep) rd<<<g, 256>>>(a, b, c, o1, m);
+        for (int rep = 0; rep < 20; ++rep) rd<<<g, bs>>>(a, b, c, o1, m);
         cudaEventRecord(e1); cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1); ms /= 20;
         printf("read3     grid %5d: %.4f ms  %.0f GB/s\n", g, ms, 3.0 * m * 16 / ms / 1e6);
         cudaEventRecord(e0);
-        for (int rep = 0; rep < 20; ++rep) wr<<<g, 256>>>(o1, o2, m);
+        for (int rep = 0; rep < 20; ++rep) wr<<<g, bs>>>(o1, o2, m);
         cudaEventRecord(e1); cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1); ms /= 20;
         printf("write2    grid %5d: %.4f ms  %.0f GB/s\n", g, ms, 2.0 * m * 16 / ms / 1e6);
