@@ -1,27 +1,37 @@
-// ilu.cu — ILU(p) block solver: host factorisation + batched, level-scheduled
-// triangular sweeps on the device (K2/K4, inexact mode).
+// ilu.cu — ILU(p) block solver: factorisation + batched, level-scheduled triangular sweeps on
+// the device (K2/K4, inexact mode).
 //
-// Reference: IluFactors::factor (src/ilu.cpp:8-106), build_transposes
-// (:108-129), solve (:131-174).
+// Reference: IluFactors::factor (src/ilu.cpp:8-106), build_transposes (:108-129), solve
+// (:131-174).
 //
-// The factorisation is per-Newton-step setup. It runs on the host in the
-// same operation order as the reference (level-of-fill symbolic phase, IKJ
-// numeric phase with the `lij == 0` skip, libgcc complex division), so the
-// factors are bit-identical to the reference's and the inexact
-// preconditioner reproduces the reference's output exactly. The four
-// triangular sweeps (L, U forward; U^H, L^H adjoint) run on the device for
-// all sources at once, one CTA per source (ilu_sweep_tma): rows grouped into
-// dependency levels, each level in two phases — every thread forms products
-// (lane per entry), then each row's owner subtracts them in the reference's
-// entry order (bit-faithful) — with the level data streamed into shared
-// memory by TMA bulk copies several levels ahead. The vector lives in shared
-// memory (config 1), or in a ring indexed by level-ordered position when it
-// is too large (config 3/4: operands lie < 700 positions behind their rows).
+// The factorisation is per-Newton-step setup; the factors must be bit-identical to the
+// reference's for the inexact preconditioner to reproduce its output exactly.
+//  * symbolic phase (level-of-fill patterns, host, the reference's rules) and everything that
+//    depends only on the pattern — level schedules, the level-ordered sweep layouts, the
+//    numeric phase's update lists — are built once per (grid, fill level) and cached across
+//    contexts (a Newton sweep re-factors the same pattern every step);
+//  * numeric phase on the device (ilu_numeric), the reference's IKJ order exactly: rows in
+//    dependency levels, one warp per row; for each j of row i's L pattern in ascending
+//    order, w_j /= U_jj (libgcc complex division), skipped if zero, then the row's entries
+//    k in U_j's pattern updated in parallel (each k once per j, so the order of the updates
+//    to every w_k is the reference's); zero pivots raise ZeroPivotError(row) with the
+//    smallest failing row, the one the reference reports;
+//  * the four sweeps' value arrays (L, U forward; U^H, L^H adjoint) gathered from the factor
+//    in their level-ordered layouts, and U's divisors prepared (ilu_sweep_vals).
+// The sweeps run for all sources at once, one CTA per source (ilu_sweep_tma): rows grouped
+// into dependency levels, each level in two phases — every thread forms products (lane per
+// entry), then each row's owner subtracts them in the reference's entry order (bit-faithful)
+// — with the level data streamed into shared memory by TMA bulk copies several levels ahead.
+// The vector lives in shared memory (config 1), or in a ring indexed by level-ordered
+// position when it is too large (config 3/4: operands lie < 700 positions behind their rows).
 #include <algorithm>
 #include <chrono>
-#include <cstdlib>
+#include <climits>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
+#include <memory>
+#include <mutex>
 #include <queue>
 #include <string>
 
@@ -31,7 +41,7 @@ namespace fwi_b200 {
 
 using cplx = std::complex<double>;
 
-constexpr int kIluBatch = 8;  // entries per batch of the sweep kernels (row padding unit)
+constexpr int kIluBatch = 8;      // entries per batch of the sweep kernels (row padding unit)
 constexpr int kIluThreads = 256;  // sweep kernel block
 constexpr int kIluEpl = 2;        // entries per thread and level (a level holds <= kIluThreads * kIluEpl)
 constexpr int kIluRows = 128;     // rows per (sub-)level
@@ -39,35 +49,48 @@ constexpr int kIluRing = 4;       // TMA stage ring
 constexpr int kIluAhead = 3;      // levels staged ahead
 constexpr int kIluRingW = 2048;   // operand ring (positions) of the ring sweep, a power of two
 
-struct Sweep {          // one triangular sweep in CSR form + its level schedule
-    DevBuf<int> ptr, idx, lvl_ptr, lvl_rows;
-    DevBuf<double2> val;
-    // the same entries regrouped in level order: row lvl_rows[r] owns
-    // entries [rstart[r], rstart[r+1]) of (lidx, lval), in the row's own order
-    // (entries padded per row to a multiple of kIluBatch; diagonals of U / U^T in ldiag;
-    // levels wider than the kernel are cut into consecutive sub-levels)
-    DevBuf<int> rstart, lidx;
-    DevBuf<int4> recs;      // per level-ordered row: {row, first entry, end entry (level-relative), position}
-    DevBuf<int> lpos;       // operand level-ordered positions (ring sweep), -1 for padding
+// One triangular sweep's pattern-only data: the entries regrouped in level order (row
+// lvl_rows[r] owns entries [rstart[r], rstart[r+1]) in the row's own order, padded to a
+// multiple of kIluBatch; the diagonals of U / U^T apart; levels wider than the kernel cut into
+// consecutive sub-levels) and where each entry's value comes from in the factor.
+struct Sweep {
+    DevBuf<int> lvl_rows, lidx, lpos;  // rows in level order; operand node / level position (-1: padding)
+    DevBuf<int4> recs;                 // per level-ordered row: {row, first entry, end entry, position}
+    DevBuf<int4> lmeta;                // per (sub-)level: first row, end row, first entry, end entry
+    DevBuf<int> vmap;                  // per entry: index of its value in the factor (-1: padding)
+    DevBuf<int> dmap;                  // per level-ordered row: index of its divisor (sweeps with one)
+    bool has_diag = false, conj_diag = false;
     bool ring_ok = false;
-    DevBuf<double2> lval;
-    DevBuf<double4> ldiag;  // per level-ordered row: divisor {ratio, denominator, |c| < |d|, 0}
-    DevBuf<int4> lmeta;  // per level: first row, end row, first entry, end entry
-    int nlev = 0;            // (sub-)levels of the two-phase kernel
-    int nlev0 = 0;           // dependency levels (lvl_ptr)
-    int ecap = 0, rcap = 0;  // max entries / rows of one (sub-)level
+    int nlev = 0, nent = 0;
+    int maxrow = 0;
+};
+
+// Everything that depends only on the pattern of one (grid, fill level).
+struct IluPattern {
+    int nx = 0, nz = 0, n = 0, level = 0;
+    int64_t nfv = 0;                                   // factor values: row i at [rowoff[i], rowoff[i+1]): L then U
+    int maxcnt = 0, maxnl = 0, maxupd = 0;             // longest factor row, L row, row update list
+    DevBuf<int> rowoff, nl, arp, aslot, lp, jdiag, updptr, frows;
+    DevBuf<int2> upd;                                  // (slot in row i, factor index of U_jk)
+    std::vector<int> flvl;                             // numeric phase levels (host) over frows
+    Sweep L, U, Ut, Lt;
+    int64_t bytes = 0;
 };
 
 struct IluFactor {
     int level = 0;
-    Sweep L, U, Ut, Lt;  // Ut/Lt: transposes for the adjoint
+    std::shared_ptr<IluPattern> pat;
+    DevBuf<double2> fv;                                // L | U per row
+    DevBuf<double2> lval[4];                           // per sweep (L, U, Ut, Lt)
+    DevBuf<double4> ldiag[4];                          // per sweep with a divisor (U, Ut)
     int64_t bytes = 0;
     DevBuf<double2> zslot;  // the padding entries' operand (+0) when the vector is in global memory
     DevBuf<double2> blo;    // right-hand sides in level order (ring sweep scratch, nrhs x n)
+    DevBuf<int> status;
 };
 
 void ilu_free(IluFactor* f) { delete f; }
-int64_t ilu_bytes(const IluFactor* f) { return f ? f->bytes : 0; }
+int64_t ilu_bytes(const IluFactor* f) { return f ? f->bytes + (f->pat ? f->pat->bytes : 0) : 0; }
 
 namespace {
 
@@ -129,294 +152,331 @@ void build_levels(int n, const std::vector<int>& ptr, const std::vector<int>& id
     for (int i = 0; i < n; ++i) rows[pos[lv[i]]++] = i;
 }
 
-void upload_sweep(Sweep& s, int n, const std::vector<int>& ptr, const std::vector<int>& idx,
-                  const std::vector<cplx>& val, bool forward, bool has_diag, cudaStream_t st, int64_t& bytes) {
-    std::vector<int> lp, rows;
-    build_levels(n, ptr, idx, forward, lp, rows, s.nlev);
-    s.nlev0 = s.nlev;
-    auto up = [&](auto& buf, const auto& v) {
-        using T = typename std::remove_reference_t<decltype(buf)>;
-        (void)sizeof(T);
-        buf.alloc(std::max<size_t>(v.size(), 1));
-        if (!v.empty())
-            CK(cudaMemcpyAsync(buf.p, v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice, st));
-        bytes += int64_t(v.size() * sizeof(v[0]));
-    };
-    up(s.ptr, ptr);
-    up(s.idx, idx);
-    up(s.lvl_ptr, lp);
-    up(s.lvl_rows, rows);
-    {
-        // level order; per row the off-diagonal entries in the row's own order, padded to a
-        // multiple of kIluBatch with (n, 0) entries; the diagonal (U: first, U^T: last) apart
-        std::vector<int> rst(n + 1, 0), li;
-        std::vector<cplx> lv, dg(n, cplx(1.0, 0.0));
-        li.reserve(idx.size() + size_t(n) * kIluBatch);
-        lv.reserve(val.size() + size_t(n) * kIluBatch);
-        for (int r = 0; r < n; ++r) {
-            const int i = rows[r];
-            for (int q = ptr[i]; q < ptr[i + 1]; ++q) {
-                if (idx[q] == i && has_diag) {
-                    dg[r] = val[q];
-                    continue;
-                }
-                li.push_back(idx[q]);
-                lv.push_back(val[q]);
-            }
-            while (li.size() % kIluBatch) {
-                li.push_back(n);
-                lv.push_back(cplx(0.0, 0.0));
-            }
-            rst[r + 1] = int(li.size());
-        }
-        up(s.rstart, rst);
-        // sub-levels: at most kIluThreads rows and kIluThreads * kIluEpl entries each
-        std::vector<int> sp{0};
-        for (int l = 0; l < s.nlev; ++l) {
-            int r = lp[l];
-            while (r < lp[l + 1]) {
-                const int r0 = r;
-                while (r < lp[l + 1] && r - r0 < kIluRows && rst[r + 1] - rst[r0] <= kIluThreads * kIluEpl) ++r;
-                if (r == r0)
-                    throw FwiError(FWI_ERR_NOT_SUPPORTED, "ILU sweep: a factor row holds more than " +
-                                                             std::to_string(kIluThreads * kIluEpl) + " entries");
-                sp.push_back(r);
-            }
-        }
-        lp.swap(sp);
-        s.nlev = int(lp.size()) - 1;
-        s.ecap = s.rcap = 1;
-        std::vector<int4> rec(n);
-        for (int l = 0; l < s.nlev; ++l) {
-            s.rcap = std::max(s.rcap, lp[l + 1] - lp[l]);
-            s.ecap = std::max(s.ecap, rst[lp[l + 1]] - rst[lp[l]]);
-            for (int r = lp[l]; r < lp[l + 1]; ++r)
-                rec[r] = make_int4(rows[r], rst[r] - rst[lp[l]], rst[r + 1] - rst[lp[l]], r);
-        }
-        s.ecap = (s.ecap + kIluBatch - 1) / kIluBatch * kIluBatch;
-        up(s.recs, rec);
-        std::vector<int4> meta(s.nlev);
-        for (int l = 0; l < s.nlev; ++l) meta[l] = make_int4(lp[l], lp[l + 1], rst[lp[l]], rst[lp[l + 1]]);
-        up(s.lmeta, meta);
-        up(s.lidx, li);
-        // operand positions for the ring sweep (padding: -1) and whether the ring holds them
-        {
-            std::vector<int> pos(n + 1, -1), lpos(li.size());
-            for (int r = 0; r < n; ++r) pos[rows[r]] = r;
-            int maxd = 0;
-            for (int r = 0; r < n; ++r)
-                for (int q = rst[r]; q < rst[r + 1]; ++q) {
-                    lpos[q] = pos[li[q]];
-                    if (li[q] < n) maxd = std::max(maxd, r - pos[li[q]]);
-                }
-            s.ring_ok = maxd + kIluRows < kIluRingW;
-            up(s.lpos, lpos);
-        }
-        s.lval.alloc(std::max<size_t>(lv.size(), 1));
-        if (!lv.empty())
-            CK(cudaMemcpyAsync(s.lval.p, lv.data(), lv.size() * sizeof(cplx), cudaMemcpyHostToDevice, st));
-        bytes += int64_t(lv.size() * sizeof(cplx));
-        if (has_diag) {
-            // divisor of each row: U(i,i) (forward U sweep) or conj(U(i,i)) (the U^H sweep)
-            std::vector<double4> q(n);
-            for (int r = 0; r < n; ++r) {
-                const double c = dg[r].real(), d = forward ? -dg[r].imag() : dg[r].imag();
-                double rr, den;
-                const bool small_c = host_cdiv_prep(c, d, rr, den);
-                q[r] = make_double4(rr, den, small_c ? 1.0 : 0.0, 0.0);
-            }
-            s.ldiag.alloc(size_t(n));
-            CK(cudaMemcpyAsync(s.ldiag.p, q.data(), size_t(n) * sizeof(double4), cudaMemcpyHostToDevice, st));
-            CK(cudaStreamSynchronize(st));
-            bytes += int64_t(n) * int64_t(sizeof(double4));
-        }
-    }
-    s.val.alloc(std::max<size_t>(val.size(), 1));
-    if (!val.empty())
-        CK(cudaMemcpyAsync(s.val.p, val.data(), val.size() * sizeof(cplx), cudaMemcpyHostToDevice, st));
-    bytes += int64_t(val.size() * sizeof(cplx));
-    CK(cudaStreamSynchronize(st));
+template <class T>
+void upload(DevBuf<T>& buf, const std::vector<T>& v, cudaStream_t st, int64_t& bytes) {
+    buf.alloc(std::max<size_t>(v.size(), 1));
+    if (!v.empty()) CK(cudaMemcpyAsync(buf.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    bytes += int64_t(v.size() * sizeof(T));
 }
 
-void transpose_csr(int n, const std::vector<int>& ptr, const std::vector<int>& idx,
-                   const std::vector<cplx>& val, std::vector<int>& tp, std::vector<int>& ti,
-                   std::vector<cplx>& tv) {
+// The sweep layout of one triangular factor given in CSR (ptr, idx) with src[p] = index of
+// entry p's value in the factor; has_diag: the row's diagonal is its divisor (kept apart).
+void build_sweep(Sweep& s, int n, const std::vector<int>& ptr, const std::vector<int>& idx,
+                 const std::vector<int>& src, bool forward, bool has_diag, bool conj_diag, cudaStream_t st,
+                 int64_t& bytes) {
+    std::vector<int> lp, rows;
+    int nlev0 = 0;
+    build_levels(n, ptr, idx, forward, lp, rows, nlev0);
+    s.has_diag = has_diag;
+    s.conj_diag = conj_diag;
+    upload(s.lvl_rows, rows, st, bytes);
+    // level order; per row the off-diagonal entries in the row's own order, padded to a
+    // multiple of kIluBatch with (n, -1) entries; the diagonal (U: first, U^T: last) apart
+    std::vector<int> rst(n + 1, 0), li, vm, dm(n, -1);
+    li.reserve(idx.size() + size_t(n) * kIluBatch);
+    vm.reserve(idx.size() + size_t(n) * kIluBatch);
+    for (int r = 0; r < n; ++r) {
+        const int i = rows[r];
+        for (int q = ptr[i]; q < ptr[i + 1]; ++q) {
+            if (idx[q] == i && has_diag) {
+                dm[r] = src[q];
+                continue;
+            }
+            li.push_back(idx[q]);
+            vm.push_back(src[q]);
+        }
+        while (li.size() % kIluBatch) {
+            li.push_back(n);
+            vm.push_back(-1);
+        }
+        rst[r + 1] = int(li.size());
+        s.maxrow = std::max(s.maxrow, rst[r + 1] - rst[r]);
+    }
+    // sub-levels: at most kIluRows rows and kIluThreads * kIluEpl entries each
+    std::vector<int> sp{0};
+    for (int l = 0; l < nlev0; ++l) {
+        int r = lp[l];
+        while (r < lp[l + 1]) {
+            const int r0 = r;
+            while (r < lp[l + 1] && r - r0 < kIluRows && rst[r + 1] - rst[r0] <= kIluThreads * kIluEpl) ++r;
+            if (r == r0)
+                throw FwiError(FWI_ERR_NOT_SUPPORTED, "ILU sweep: a factor row holds more than " +
+                                                         std::to_string(kIluThreads * kIluEpl) + " entries");
+            sp.push_back(r);
+        }
+    }
+    lp.swap(sp);
+    s.nlev = int(lp.size()) - 1;
+    s.nent = int(li.size());
+    std::vector<int4> rec(n);
+    for (int l = 0; l < s.nlev; ++l)
+        for (int r = lp[l]; r < lp[l + 1]; ++r)
+            rec[r] = make_int4(rows[r], rst[r] - rst[lp[l]], rst[r + 1] - rst[lp[l]], r);
+    upload(s.recs, rec, st, bytes);
+    std::vector<int4> meta(s.nlev);
+    for (int l = 0; l < s.nlev; ++l) meta[l] = make_int4(lp[l], lp[l + 1], rst[lp[l]], rst[lp[l + 1]]);
+    upload(s.lmeta, meta, st, bytes);
+    upload(s.lidx, li, st, bytes);
+    upload(s.vmap, vm, st, bytes);
+    if (has_diag) upload(s.dmap, dm, st, bytes);
+    // operand positions for the ring sweep (padding: -1) and whether the ring holds them
+    std::vector<int> pos(n + 1, -1), lpos(li.size());
+    for (int r = 0; r < n; ++r) pos[rows[r]] = r;
+    int maxd = 0;
+    for (int r = 0; r < n; ++r)
+        for (int q = rst[r]; q < rst[r + 1]; ++q) {
+            lpos[q] = pos[li[q]];
+            if (li[q] < n) maxd = std::max(maxd, r - pos[li[q]]);
+        }
+    s.ring_ok = maxd + kIluRows < kIluRingW;
+    upload(s.lpos, lpos, st, bytes);
+}
+
+// transpose of a CSR pattern; tsrc[q] = source entry index of transposed entry q
+void transpose_pattern(int n, const std::vector<int>& ptr, const std::vector<int>& idx, std::vector<int>& tp,
+                       std::vector<int>& ti, std::vector<int>& tsrc) {
     tp.assign(n + 1, 0);
     for (int c : idx) tp[c + 1]++;
     for (int j = 0; j < n; ++j) tp[j + 1] += tp[j];
     ti.resize(idx.size());
-    tv.resize(idx.size());
+    tsrc.resize(idx.size());
     std::vector<int> nx(tp.begin(), tp.end() - 1);
     for (int i = 0; i < n; ++i)  // rows ascending -> ascending order within each transposed row
         for (int p = ptr[i]; p < ptr[i + 1]; ++p) {
             const int q = nx[idx[p]]++;
             ti[q] = i;
-            tv[q] = val[p];
+            tsrc[q] = p;
         }
+}
+
+// The pattern of ILU(level) on the operand's pattern (rp, ci) and all pattern-only data.
+std::shared_ptr<IluPattern> build_pattern(const Ctx& c, int level, const std::vector<int>& arp,
+                                          const std::vector<int>& aci) {
+    auto P = std::make_shared<IluPattern>();
+    P->nx = c.nx;
+    P->nz = c.nz;
+    P->level = level;
+    const int n = c.n;
+    P->n = n;
+    const cudaStream_t st = c.stream;
+    // ---- symbolic phase: levels of fill (src/ilu.cpp:19-50). Row i starts from A's pattern
+    // at level 0; pivot rows j < i are visited in ascending order (a min-heap, since fill
+    // created through j only lands at k > j), and fill (i,k) via j gets lev(i,j) + lev(j,k) + 1
+    // if <= level.
+    std::vector<std::vector<int>> lpat(n), upat(n);
+    std::vector<std::vector<std::pair<int, int>>> ulev(n);
+    std::vector<int> lev(n, 0), stamp(n, -1), cols;
+    for (int i = 0; i < n; ++i) {
+        cols.clear();
+        std::priority_queue<int, std::vector<int>, std::greater<int>> todo;
+        bool has_diag = false;
+        for (int p = arp[i]; p < arp[i + 1]; ++p) {
+            const int j = aci[p];
+            stamp[j] = i;
+            lev[j] = 0;
+            cols.push_back(j);
+            if (j < i) todo.push(j);
+            has_diag |= (j == i);
+        }
+        if (!has_diag)
+            throw FwiError(FWI_ERR_INVALID_ARGUMENT,
+                           "IluFactors::factor: missing diagonal at row " + std::to_string(i));
+        while (!todo.empty()) {
+            const int j = todo.top();
+            todo.pop();
+            const int lj = lev[j];
+            for (const auto& [k, lu] : ulev[j]) {
+                const int nl = lj + lu + 1;
+                if (nl > level) continue;
+                if (stamp[k] != i) {
+                    stamp[k] = i;
+                    lev[k] = nl;
+                    cols.push_back(k);
+                    if (k < i) todo.push(k);
+                } else if (nl < lev[k]) {
+                    lev[k] = nl;
+                }
+            }
+        }
+        std::sort(cols.begin(), cols.end());
+        for (int cc : cols) {
+            if (cc < i)
+                lpat[i].push_back(cc);
+            else
+                upat[i].push_back(cc);
+            if (cc > i) ulev[i].emplace_back(cc, lev[cc]);
+        }
+    }
+    // ---- factor layout: row i = [L entries | U entries (diagonal first)]
+    std::vector<int> lp(n + 1, 0), up(n + 1, 0), rowoff(n + 1, 0), nl(n);
+    for (int i = 0; i < n; ++i) {
+        lp[i + 1] = lp[i] + int(lpat[i].size());
+        up[i + 1] = up[i] + int(upat[i].size());
+        nl[i] = int(lpat[i].size());
+        rowoff[i + 1] = rowoff[i] + int(lpat[i].size() + upat[i].size());
+    }
+    P->nfv = rowoff[n];
+    for (int i = 0; i < n; ++i) {
+        P->maxcnt = std::max(P->maxcnt, rowoff[i + 1] - rowoff[i]);
+        P->maxnl = std::max(P->maxnl, nl[i]);
+    }
+    std::vector<int> li(lp[n]), ui(up[n]);
+    for (int i = 0; i < n; ++i) {
+        std::copy(lpat[i].begin(), lpat[i].end(), li.begin() + lp[i]);
+        std::copy(upat[i].begin(), upat[i].end(), ui.begin() + up[i]);
+    }
+    auto lsrc = [&](int i, int p) { return rowoff[i] + (p - lp[i]); };
+    auto usrc = [&](int i, int p) { return rowoff[i] + nl[i] + (p - up[i]); };
+    // ---- numeric phase data (src/ilu.cpp:52-104): A's entries scattered into row slots; per
+    // L entry (i, j): the index of U_jj and the updates w_k -= l_ij u_jk for k in U_j's pattern
+    // that row i holds (the stamp test)
+    std::vector<int> aslot(arp[n]), jdiag(lp[n]), updptr(lp[n] + 1, 0);
+    std::vector<int2> upd;
+    std::vector<int> slot(n, -1);
+    for (int i = 0; i < n; ++i) {
+        int q = 0;
+        for (int cc : lpat[i]) slot[cc] = q++;
+        for (int cc : upat[i]) slot[cc] = q++;
+        for (int p = arp[i]; p < arp[i + 1]; ++p) aslot[p] = slot[aci[p]];
+        for (int t = 0; t < nl[i]; ++t) {
+            const int j = lpat[i][t], pl = lp[i] + t;
+            jdiag[pl] = usrc(j, up[j]);
+            for (int p = up[j] + 1; p < up[j + 1]; ++p) {
+                const int k = ui[p];
+                if (slot[k] >= 0) upd.push_back(make_int2(slot[k], usrc(j, p)));
+            }
+            updptr[pl + 1] = int(upd.size());
+        }
+        for (int cc : lpat[i]) slot[cc] = -1;
+        for (int cc : upat[i]) slot[cc] = -1;
+    }
+    for (int i = 0; i < n; ++i) P->maxupd = std::max(P->maxupd, updptr[lp[i + 1]] - updptr[lp[i]]);
+    std::vector<int> flp, frows;
+    int fnlev = 0;
+    build_levels(n, lp, li, true, flp, frows, fnlev);
+    P->flvl = flp;
+    upload(P->rowoff, rowoff, st, P->bytes);
+    upload(P->nl, nl, st, P->bytes);
+    upload(P->arp, arp, st, P->bytes);
+    upload(P->aslot, aslot, st, P->bytes);
+    upload(P->lp, lp, st, P->bytes);
+    upload(P->jdiag, jdiag, st, P->bytes);
+    upload(P->updptr, updptr, st, P->bytes);
+    upload(P->upd, upd, st, P->bytes);
+    upload(P->frows, frows, st, P->bytes);
+    // ---- the four sweeps (build_transposes, src/ilu.cpp:108-129)
+    std::vector<int> ls(lp[n]), us(up[n]);
+    for (int i = 0; i < n; ++i) {
+        for (int p = lp[i]; p < lp[i + 1]; ++p) ls[p] = lsrc(i, p);
+        for (int p = up[i]; p < up[i + 1]; ++p) us[p] = usrc(i, p);
+    }
+    std::vector<int> tp, ti, tsrc, ts;
+    build_sweep(P->L, n, lp, li, ls, true, false, false, st, P->bytes);
+    build_sweep(P->U, n, up, ui, us, false, true, false, st, P->bytes);
+    transpose_pattern(n, up, ui, tp, ti, tsrc);
+    ts.resize(tsrc.size());
+    for (size_t q = 0; q < tsrc.size(); ++q) ts[q] = us[tsrc[q]];
+    build_sweep(P->Ut, n, tp, ti, ts, true, true, true, st, P->bytes);
+    transpose_pattern(n, lp, li, tp, ti, tsrc);
+    ts.resize(tsrc.size());
+    for (size_t q = 0; q < tsrc.size(); ++q) ts[q] = ls[tsrc[q]];
+    build_sweep(P->Lt, n, tp, ti, ts, false, false, false, st, P->bytes);
+    CK(cudaStreamSynchronize(st));
+    return P;
+}
+
+// ---- numeric phase kernels --------------------------------------------------
+
+// One warp per row of one level: the reference's IKJ loop (src/ilu.cpp:66-103) on row i,
+// everything the row reads staged in shared memory first — w, U_jj of every j, and every
+// update entry (slot, u_jk) of the row, loaded together in one coalesced pass (they come
+// from earlier, final rows) — so the j loop runs from shared memory: lane 0 forms
+// l_ij = w_j / U_jj (libgcc division), then the lanes apply j's updates (distinct slots).
+struct NumericSmem {  // per-warp layout (double2 units, then ints)
+    int maxcnt, maxnl, maxupd;
+    __host__ __device__ size_t d2() const { return size_t(maxcnt) + maxnl + maxupd; }
+    __host__ __device__ size_t ints() const { return size_t(maxupd) + maxnl + 1; }
+    __host__ __device__ size_t bytes() const { return d2() * 16 + (ints() * 4 + 15) / 16 * 16; }
+};
+
+__global__ void __launch_bounds__(128) ilu_numeric(int r0, int r1, const int* __restrict__ frows,
+                                                   const int* __restrict__ rowoff, const int* __restrict__ nl,
+                                                   const int* __restrict__ arp, const int* __restrict__ aslot,
+                                                   const double2* __restrict__ ava, double shift,
+                                                   const int* __restrict__ lp, const int* __restrict__ jdiag,
+                                                   const int* __restrict__ updptr, const int2* __restrict__ upd,
+                                                   double2* fv, int* status, NumericSmem L) {
+    extern __shared__ __align__(16) unsigned char nraw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double2* w = reinterpret_cast<double2*>(nraw + size_t(wid) * L.bytes());
+    double2* ujj = w + L.maxcnt;
+    double2* uval = ujj + L.maxnl;
+    int* uslot = reinterpret_cast<int*>(uval + L.maxupd);
+    int* uptr = uslot + L.maxupd;
+    const int r = r0 + int(blockIdx.x) * (blockDim.x >> 5) + wid;
+    if (r >= r1) return;
+    const int i = frows[r];
+    const int base = rowoff[i], cnt = rowoff[i + 1] - base, nli = nl[i], l0 = lp[i];
+    const int e0 = updptr[l0], ne = updptr[l0 + nli] - e0;
+    for (int t = lane; t < cnt; t += 32) w[t] = make_double2(0.0, 0.0);
+    for (int q = lane; q < nli; q += 32) ujj[q] = fv[jdiag[l0 + q]];  // U_jj of every j (final rows)
+    for (int q = lane; q <= nli; q += 32) uptr[q] = updptr[l0 + q] - e0;
+    for (int e = lane; e < ne; e += 32) {
+        const int2 u = upd[e0 + e];
+        uslot[e] = u.x;
+        uval[e] = fv[u.y];
+    }
+    __syncwarp();
+    for (int p = arp[i] + lane; p < arp[i + 1]; p += 32) w[aslot[p]] = cadd(w[aslot[p]], ava[p]);  // w[col] += a
+    __syncwarp();
+    if (lane == 0) w[nli].x = __dadd_rn(w[nli].x, shift);  // w[i] += shift
+    __syncwarp();
+    for (int q = 0; q < nli; ++q) {
+        double2 lij = make_double2(0.0, 0.0);
+        if (lane == 0) {
+            lij = cdiv(w[q], ujj[q]);  // w[j] /= uv[ud]
+            w[q] = lij;
+        }
+        lij.x = __shfl_sync(0xffffffffu, lij.x, 0);
+        lij.y = __shfl_sync(0xffffffffu, lij.y, 0);
+        if (lij.x == 0.0 && lij.y == 0.0) continue;  // if (lij == 0.0) continue;
+        for (int e = uptr[q] + lane; e < uptr[q + 1]; e += 32)
+            w[uslot[e]] = csub(w[uslot[e]], cmul(lij, uval[e]));  // w[k] -= lij * uv[p]
+        __syncwarp();
+    }
+    __syncwarp();
+    if (lane == 0 && w[nli].x == 0.0 && w[nli].y == 0.0) atomicMin(status, i);
+    for (int t = lane; t < cnt; t += 32) fv[base + t] = w[t];
+}
+
+// sweep values from the factor: lval[e] = fv[vmap[e]] (padding: +0); divisors (U / U^H):
+// cdiv's ratio and denominator (host_cdiv_prep) of U_ii or conj(U_ii)
+__global__ void ilu_sweep_vals(int nent, const int* __restrict__ vmap, const double2* __restrict__ fv,
+                               double2* __restrict__ lval, int n, const int* __restrict__ dmap, bool conj_diag,
+                               double4* __restrict__ ldiag) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < nent) {
+        const int v = vmap[t];
+        lval[t] = v >= 0 ? fv[v] : make_double2(0.0, 0.0);
+    }
+    if (ldiag && t < n) {
+        const double2 d = fv[dmap[t]];
+        const double cc = d.x, dd = conj_diag ? -d.y : d.y;
+        double r, den, small;
+        if (fabs(cc) < fabs(dd)) {
+            r = __ddiv_rn(cc, dd);
+            den = __dadd_rn(__dmul_rn(cc, r), dd);
+            small = 1.0;
+        } else {
+            r = __ddiv_rn(dd, cc);
+            den = __dadd_rn(__dmul_rn(dd, r), cc);
+            small = 0.0;
+        }
+        ldiag[t] = make_double4(r, den, small, 0.0);
+    }
 }
 
 enum SweepKind { kLfwd = 0, kUbwd = 1, kUtfwd = 2, kLtbwd = 3 };
-
-// One CTA per group of `kg` right-hand sides; levels in order with a barrier
-// between them; each (row, rhs) item follows the reference's entry order.
-template <int KIND>
-__global__ void __launch_bounds__(256) ilu_sweep_kernel(int64_t n, int nrhs, int kg, int nlev,
-                                                       const int* __restrict__ lvl_ptr,
-                                                       const int* __restrict__ lvl_rows,
-                                                       const int* __restrict__ ptr,
-                                                       const int* __restrict__ idx,
-                                                       const double2* __restrict__ val, double2* x) {
-    const int k0 = blockIdx.x * kg;
-    const int kc = min(kg, nrhs - k0);
-    if (kc <= 0) return;
-    for (int l = 0; l < nlev; ++l) {
-        const int r0 = lvl_ptr[l], r1 = lvl_ptr[l + 1];
-        const int items = (r1 - r0) * kc;
-        for (int it = threadIdx.x; it < items; it += blockDim.x) {
-            const int i = lvl_rows[r0 + it / kc];
-            double2* xk = x + int64_t(k0 + it % kc) * n;
-            double2 s = xk[i];
-            const int p0 = ptr[i], p1 = ptr[i + 1];
-            if (KIND == kLfwd || KIND == kLtbwd) {
-                for (int p = p0; p < p1; ++p) {
-                    const double2 a = val[p];
-                    const double2 xv = xk[idx[p]];
-                    s = csub(s, KIND == kLfwd ? cmul(a, xv) : cmulc(a, xv));
-                }
-                xk[i] = s;
-            } else if (KIND == kUbwd) {  // diagonal first
-                for (int p = p0 + 1; p < p1; ++p) s = csub(s, cmul(val[p], xk[idx[p]]));
-                xk[i] = cdiv(s, val[p0]);
-            } else {  // kUtfwd: row i of U^T, diagonal last
-                double2 dg = make_double2(0.0, 0.0);
-                for (int p = p0; p < p1; ++p) {
-                    const int k = idx[p];
-                    if (k == i)
-                        dg = val[p];
-                    else
-                        s = csub(s, cmulc(val[p], xk[k]));
-                }
-                xk[i] = cdiv(s, make_double2(dg.x, -dg.y));
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// Two-phase level sweep (the default). One CTA per right-hand side, kIluThreads threads, one
-// barrier pair per level:
-//   phase A  every thread forms the products a_e * x[k_e] of up to kIluEpl of the level's
-//            entries (lane per entry: the level's ~240 products of config 1's ILU(21) take one
-//            product's latency instead of a 40-long per-row sequence) into shared memory;
-//   phase B  thread t owns the level's row t and subtracts its products from b_i in the
-//            reference's entry order (a chain of dependent subtractions: the irreducible
-//            part), divides by the diagonal of U / U^T, and stores x_i.
-// The level's entry indices / values and row records are loaded into registers one level
-// ahead (they do not depend on x), so the only memory reads on the critical path are the x
-// operands (shared memory, or L1/L2 for vectors beyond shared memory) and the products.
-// Entries are the padded rows of the level-ordered arrays (padding: operand +0 at slot n,
-// value 0 -> product +0, which leaves the running sum bit-for-bit unchanged).
-template <int KIND, bool XS>
-__global__ void __launch_bounds__(kIluThreads) ilu_sweep_2p(int n, int nlev, const int4* __restrict__ lmeta,
-                                                           const int4* __restrict__ recs,
-                                                           const int* __restrict__ idx,
-                                                           const double2* __restrict__ val,
-                                                           const double4* __restrict__ ldiag, double2* x,
-                                                           const double2* __restrict__ zslot, long long* trace) {
-    extern __shared__ __align__(16) double2 dyn[];
-    constexpr bool kHasDiag = KIND == kUbwd || KIND == kUtfwd;
-    constexpr int T = kIluThreads, E = kIluEpl;
-    double2* xk = x + int64_t(blockIdx.x) * n;
-    double2* xs = XS ? dyn : xk;
-    double2* prod = dyn + (XS ? n + 1 : 0);  // [T * E] products of the current level
-    const double2* zero = XS ? xs + n : zslot;
-    const int tid = threadIdx.x;
-    if (XS) {
-        for (int i = tid; i < n; i += T) xs[i] = xk[i];
-        if (tid == 0) xs[n] = make_double2(0.0, 0.0);
-    }
-    // level l's operands in registers (loaded during level l-1)
-    int kc[E];
-    double2 ac[E];
-    int4 rc = make_int4(-1, 0, 0, 0);
-    double4 dc = make_double4(0, 0, 0, 0);
-    int4 m = nlev > 0 ? __ldg(lmeta) : make_int4(0, 0, 0, 0);
-    auto load_level = [&](const int4 mm, int (&kk)[E], double2 (&aa)[E], int4& rr, double4& dd) {
-#pragma unroll
-        for (int j = 0; j < E; ++j) {
-            const int e = mm.z + tid + j * T;
-            kk[j] = e < mm.w ? __ldg(idx + e) : -1;
-            aa[j] = e < mm.w ? __ldg(val + e) : make_double2(0.0, 0.0);
-        }
-        const int r = mm.x + tid;
-        rr = r < mm.y ? __ldg(recs + r) : make_int4(-1, 0, 0, 0);
-        if (kHasDiag && r < mm.y) {
-            const double2 d0 = __ldg(reinterpret_cast<const double2*>(ldiag + r));
-            const double2 d1 = __ldg(reinterpret_cast<const double2*>(ldiag + r) + 1);
-            dd = make_double4(d0.x, d0.y, d1.x, d1.y);
-        }
-    };
-    // one level: prefetch level l+1 into (kn, an, rn, dn), phase A and phase B of level l
-    // from (kc, ac, rc, dc). The loop is unrolled by two with the register sets in turn, so
-    // the prefetched loads are first consumed a whole level later.
-    int4 mnext = nlev > 1 ? __ldg(lmeta + 1) : make_int4(0, 0, 0, 0);  // level l+1's bounds, loaded during l-1
-    auto step = [&](int l, int (&kc)[E], double2 (&ac)[E], int4& rc, double4& dc, int (&kn)[E], double2 (&an)[E],
-                    int4& rn, double4& dn) {
-        const bool tr = trace && blockIdx.x == 0 && tid == 0;  // diagnostics (FWI_ILU_TRACE)
-        if (tr) trace[5 * l] = clock64();
-        const int4 mn = l + 1 < nlev ? mnext : make_int4(0, 0, 0, 0);
-        mnext = l + 2 < nlev ? __ldg(lmeta + l + 2) : make_int4(0, 0, 0, 0);
-        load_level(mn, kn, an, rn, dn);
-        // phase A: products of level l
-#pragma unroll
-        for (int j = 0; j < E; ++j) {
-            if (kc[j] >= 0) {
-                const double2 xv = XS ? xs[kc[j]] : *(kc[j] < n ? xk + kc[j] : zero);
-                const int e = tid + j * T;  // level-relative entry; one skew slot per 8 (bank spread)
-                prod[e + (e >> 3)] = (KIND == kLfwd || KIND == kUbwd) ? cmul(ac[j], xv) : cmulc(ac[j], xv);
-            }
-        }
-        if (tr) trace[5 * l + 1] = clock64();
-        __syncthreads();
-        if (tr) trace[5 * l + 2] = clock64();
-        // phase B: the rows of level l, entries in the reference's order
-        if (rc.x >= 0) {
-            const int i = rc.x;
-            double2 s = XS ? xs[i] : xk[i];
-            for (int p = rc.y; p < rc.z; p += kIluBatch) {
-                double2 t[kIluBatch];
-#pragma unroll
-                for (int u = 0; u < kIluBatch; ++u) t[u] = prod[p + (p >> 3) + u];
-#pragma unroll
-                for (int u = 0; u < kIluBatch; ++u) s = csub(s, t[u]);
-            }
-            if (kHasDiag)  // libgcc __divdc3 with the divisor's ratio and denominator precomputed
-                s = dc.z != 0.0 ? make_double2(__ddiv_rn(__dadd_rn(__dmul_rn(s.x, dc.x), s.y), dc.y),
-                                               __ddiv_rn(__dsub_rn(__dmul_rn(s.y, dc.x), s.x), dc.y))
-                                : make_double2(__ddiv_rn(__dadd_rn(__dmul_rn(s.y, dc.x), s.x), dc.y),
-                                               __ddiv_rn(__dsub_rn(s.y, __dmul_rn(s.x, dc.x)), dc.y));
-            if (XS)
-                xs[i] = s;
-            else
-                xk[i] = s;
-        }
-        if (tr) trace[5 * l + 3] = clock64();
-        __syncthreads();
-        if (tr) trace[5 * l + 4] = clock64();
-    };
-    int kb[E];
-    double2 ab[E];
-    int4 rb = make_int4(-1, 0, 0, 0);
-    double4 db = make_double4(0, 0, 0, 0);
-    load_level(m, kc, ac, rc, dc);
-    __syncthreads();
-    for (int l = 0; l < nlev; l += 2) {
-        step(l, kc, ac, rc, dc, kb, ab, rb, db);
-        if (l + 1 < nlev) step(l + 1, kb, ab, rb, db, kc, ac, rc, dc);
-    }
-    if (XS)
-        for (int i = tid; i < n; i += T) xk[i] = xs[i];
-}
 
 // Two-phase level sweep (the default). One CTA per right-hand side, kIluThreads threads, one
 // barrier pair per level:
@@ -427,9 +487,10 @@ __global__ void __launch_bounds__(kIluThreads) ilu_sweep_2p(int n, int nlev, con
 //            reference's entry order (the chain of dependent subtractions, the irreducible
 //            part), divides by the diagonal of U / U^T, and stores x_i.
 // A level's entry indices and values, row records and divisors are contiguous in the
-// level-ordered arrays; thread 0 streams them into a ring of kIluStages shared-memory stages
-// with TMA bulk copies (cp.async.bulk + mbarrier) kIluStages levels ahead, so no global load
-// is waited on inside the level loop except the x operands of vectors beyond shared memory.
+// level-ordered arrays; a thread without a row streams them into a ring of kIluRing shared-
+// memory stages with TMA bulk copies (cp.async.bulk + mbarrier) kIluAhead levels ahead, so no
+// global load is waited on inside the level loop except the x operands of vectors beyond
+// shared memory.
 // Entries are the padded rows of the level-ordered arrays (padding: operand +0 at slot n,
 // value 0 -> product +0, which leaves the running sum bit-for-bit unchanged).
 __device__ __forceinline__ uint32_t ilu_smem_addr(const void* p) {
@@ -623,72 +684,43 @@ __global__ void ilu_gather(int n, const int* __restrict__ rows, const double2* _
     blo[o + r] = x[o + __ldg(rows + r)];
 }
 
+
 template <int KIND>
-void run_sweep(const Sweep& s, int64_t n, int nrhs, double2* x, cudaStream_t st, const double2* zslot,
-               double2* blo) {
-    const size_t prod = size_t(kIluThreads) * kIluEpl * 9 / 8 * sizeof(double2);
-    const size_t smem = size_t(n + 1) * sizeof(double2) + prod;
-    const char* mode = std::getenv("FWI_ILU_GLOBAL");  // diagnostics: "1" = the unstaged one-row-per-thread kernel
-    static const bool no_tma = std::getenv("FWI_ILU_NOTMA") != nullptr;  // diagnostics: register-prefetch kernel
-    {
-        const size_t base = size_t(kIluRing) * IluStageLayout::bytes + 16 * kIluRing +
-                            size_t(kIluThreads) * kIluEpl * 9 / 8 * sizeof(double2);
-        const size_t with_x = base + size_t(n + 1) * sizeof(double2);
-        const size_t with_ring = base + size_t(kIluRingW + 1) * sizeof(double2);
-        static const bool no_ring = std::getenv("FWI_ILU_NORING") != nullptr;  // diagnostics
-        if (!mode && !no_tma && base <= 220 * 1024) {
-            const int md = with_x <= 220 * 1024 ? 1 : (s.ring_ok && !no_ring && blo) ? 2 : 0;
-            const size_t sm = md == 1 ? with_x : md == 2 ? with_ring : base;
-            static size_t set[3] = {0, 0, 0};  // per (KIND, MODE): the attribute only ever grows
-            auto launch = [&](auto kern, const int* ix) {
-                if (sm > set[md]) {
-                    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-                    set[md] = sm;
-                }
-                kern<<<nrhs, kIluThreads, sm, st>>>(int(n), s.nlev, s.lmeta.p, s.recs.p, ix, s.lval.p, s.ldiag.p, x,
-                                                    zslot, blo, g_ilu_trace);
-            };
-            if (md == 1) {
-                launch(ilu_sweep_tma<KIND, 1>, s.lidx.p);
-            } else if (md == 2) {
-                // the right-hand sides gathered into the sweep's level order
-                ilu_gather<<<dim3((unsigned(n) + 255) / 256, unsigned(nrhs)), 256, 0, st>>>(int(n), s.lvl_rows.p, x,
-                                                                                            blo);
-                CK_LAUNCH();
-                launch(ilu_sweep_tma<KIND, 2>, s.lpos.p);
-            } else {
-                launch(ilu_sweep_tma<KIND, 0>, s.lidx.p);
-            }
-            CK_LAUNCH();
-            return;
+void run_sweep(const Sweep& s, const double2* lval, const double4* ldiag, int64_t n, int nrhs, double2* x,
+               cudaStream_t st, const double2* zslot, double2* blo) {
+    const size_t base = size_t(kIluRing) * IluStageLayout::bytes + 16 * kIluRing +
+                        size_t(kIluThreads) * kIluEpl * 9 / 8 * sizeof(double2);
+    const size_t with_x = base + size_t(n + 1) * sizeof(double2);
+    const size_t with_ring = base + size_t(kIluRingW + 1) * sizeof(double2);
+    static const bool no_ring = std::getenv("FWI_ILU_NORING") != nullptr;  // diagnostics
+    const int md = with_x <= 220 * 1024 ? 1 : (s.ring_ok && !no_ring && blo) ? 2 : 0;
+    const size_t sm = md == 1 ? with_x : md == 2 ? with_ring : base;
+    static size_t set[3] = {0, 0, 0};  // per (KIND, MODE): the attribute only ever grows
+    auto launch = [&](auto kern, const int* ix) {
+        if (sm > set[md]) {
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+            set[md] = sm;
         }
-    }
-    if (!mode) {
-        if (smem <= 220 * 1024) {
-            static size_t set = 0;
-            if (smem > set) {
-                CK(cudaFuncSetAttribute(ilu_sweep_2p<KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(smem)));
-                set = smem;
-            }
-            ilu_sweep_2p<KIND, true><<<nrhs, kIluThreads, smem, st>>>(int(n), s.nlev, s.lmeta.p, s.recs.p, s.lidx.p,
-                                                                     s.lval.p, s.ldiag.p, x, zslot, g_ilu_trace);
-        } else {
-            ilu_sweep_2p<KIND, false><<<nrhs, kIluThreads, prod, st>>>(int(n), s.nlev, s.lmeta.p, s.recs.p, s.lidx.p,
-                                                                      s.lval.p, s.ldiag.p, x, zslot, g_ilu_trace);
-        }
+        kern<<<nrhs, kIluThreads, sm, st>>>(int(n), s.nlev, s.lmeta.p, s.recs.p, ix, lval, ldiag, x, zslot, blo,
+                                            g_ilu_trace);
+    };
+    if (md == 1) {
+        launch(ilu_sweep_tma<KIND, 1>, s.lidx.p);
+    } else if (md == 2) {
+        // the right-hand sides gathered into the sweep's level order
+        ilu_gather<<<dim3((unsigned(n) + 255) / 256, unsigned(nrhs)), 256, 0, st>>>(int(n), s.lvl_rows.p, x, blo);
         CK_LAUNCH();
-        return;
+        launch(ilu_sweep_tma<KIND, 2>, s.lpos.p);
+    } else {
+        launch(ilu_sweep_tma<KIND, 0>, s.lidx.p);
     }
-    const int kg = 1;
-    ilu_sweep_kernel<KIND><<<(nrhs + kg - 1) / kg, 256, 0, st>>>(n, nrhs, kg, s.nlev0, s.lvl_ptr.p,
-                                                                s.lvl_rows.p, s.ptr.p, s.idx.p,
-                                                                s.val.p, x);
     CK_LAUNCH();
 }
 
 }  // namespace
 
+// ILU(level) of the context's operator with diagonal shift `shift` (IluFactors::factor,
+// src/ilu.cpp:8-106): the pattern from the cache (or built), the numeric phase on the device.
 void ilu_factor(Ctx& c, int level, double shift) {
     require(level >= 0, "IluFactors::factor: fill level must be >= 0");
     const auto t_start = std::chrono::steady_clock::now();
@@ -696,105 +728,85 @@ void ilu_factor(Ctx& c, int level, double shift) {
     std::vector<cplx> ava;
     host_csr(c, arp, aci, ava);
     const int n = c.n;
-
-    // ---- symbolic phase: levels of fill (src/ilu.cpp:19-50). Row i starts
-    // from A's pattern at level 0; pivot rows j < i are visited in ascending
-    // order (a min-heap, since fill created through j only lands at k > j),
-    // and fill (i,k) via j gets lev(i,j) + lev(j,k) + 1 if <= level.
-    std::vector<std::vector<int>> lpat(n), upat(n);
-    std::vector<std::vector<std::pair<int, int>>> ulev(n);
-    std::vector<int> lev(n, 0), stamp(n, -1), cols;
-    for (int i = 0; i < n; ++i) {
-        cols.clear();
-        std::priority_queue<int, std::vector<int>, std::greater<int>> todo;
-        bool has_diag = false;
-        for (int p = arp[i]; p < arp[i + 1]; ++p) {
-            const int j = aci[p];
-            stamp[j] = i;
-            lev[j] = 0;
-            cols.push_back(j);
-            if (j < i) todo.push(j);
-            has_diag |= (j == i);
-        }
-        if (!has_diag)
-            throw FwiError(FWI_ERR_INVALID_ARGUMENT,
-                           "IluFactors::factor: missing diagonal at row " + std::to_string(i));
-        while (!todo.empty()) {
-            const int j = todo.top();
-            todo.pop();
-            const int lj = lev[j];
-            for (const auto& [k, lu] : ulev[j]) {
-                const int nl = lj + lu + 1;
-                if (nl > level) continue;
-                if (stamp[k] != i) {
-                    stamp[k] = i;
-                    lev[k] = nl;
-                    cols.push_back(k);
-                    if (k < i) todo.push(k);
-                } else if (nl < lev[k]) {
-                    lev[k] = nl;
-                }
-            }
-        }
-        std::sort(cols.begin(), cols.end());
-        for (int cc : cols) {
-            if (cc < i)
-                lpat[i].push_back(cc);
-            else
-                upat[i].push_back(cc);
-            if (cc > i) ulev[i].emplace_back(cc, lev[cc]);
-        }
+    // pattern cache: the operator's pattern depends on the grid only (Dirichlet ring), so a
+    // Newton sweep re-factors one pattern per fill level
+    static std::mutex mu;
+    static std::vector<std::shared_ptr<IluPattern>> cache;
+    std::shared_ptr<IluPattern> P;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto& e : cache)
+            if (e->nx == c.nx && e->nz == c.nz && e->level == level) P = e;
     }
-
-    // ---- numeric phase (src/ilu.cpp:52-104), IKJ on the fixed pattern
-    std::vector<int> lp(n + 1, 0), up(n + 1, 0);
-    for (int i = 0; i < n; ++i) {
-        lp[i + 1] = lp[i] + int(lpat[i].size());
-        up[i + 1] = up[i] + int(upat[i].size());
+    const auto t_pat0 = std::chrono::steady_clock::now();
+    if (!P) {
+        P = build_pattern(c, level, arp, aci);
+        std::lock_guard<std::mutex> lk(mu);
+        cache.push_back(P);
+        if (cache.size() > 4) cache.erase(cache.begin());
     }
-    std::vector<int> li(lp[n]), ui(up[n]);
-    std::vector<cplx> lv(lp[n]), uv(up[n]);
-    std::vector<cplx> w(n, 0.0);
-    std::fill(stamp.begin(), stamp.end(), -1);
-    for (int i = 0; i < n; ++i) {
-        for (int cc : lpat[i]) { stamp[cc] = i; w[cc] = 0.0; }
-        for (int cc : upat[i]) { stamp[cc] = i; w[cc] = 0.0; }
-        for (int p = arp[i]; p < arp[i + 1]; ++p) w[aci[p]] += ava[p];
-        w[i] += shift;
-        for (int j : lpat[i]) {
-            const int ud = up[j];
-            w[j] /= uv[ud];
-            const cplx lij = w[j];
-            if (lij == 0.0) continue;
-            for (int p = ud + 1; p < up[j + 1]; ++p) {
-                const int k = ui[p];
-                if (stamp[k] == i) w[k] -= lij * uv[p];
-            }
-        }
-        if (w[i] == 0.0) throw FwiError(FWI_ERR_ZERO_PIVOT,
-                                        "ILU: zero pivot at row " + std::to_string(i) +
-                                            " (consider a diagonal shift)", i);
-        int p = lp[i];
-        for (int cc : lpat[i]) { li[p] = cc; lv[p] = w[cc]; ++p; }
-        p = up[i];
-        for (int cc : upat[i]) { ui[p] = cc; uv[p] = w[cc]; ++p; }
-    }
-
+    const auto t_pat1 = std::chrono::steady_clock::now();
     auto f = std::make_unique<IluFactor>();
     f->level = level;
-    std::vector<int> ltp, lti, utp, uti;
-    std::vector<cplx> ltv, utv;
-    transpose_csr(n, lp, li, lv, ltp, lti, ltv);
-    transpose_csr(n, up, ui, uv, utp, uti, utv);
-    upload_sweep(f->L, n, lp, li, lv, true, false, c.stream, f->bytes);
-    upload_sweep(f->U, n, up, ui, uv, false, true, c.stream, f->bytes);
-    upload_sweep(f->Ut, n, utp, uti, utv, true, true, c.stream, f->bytes);
-    upload_sweep(f->Lt, n, ltp, lti, ltv, false, false, c.stream, f->bytes);
+    f->pat = P;
+    f->fv.alloc(size_t(std::max<int64_t>(P->nfv, 1)));
+    f->status.alloc(1);
+    DevBuf<double2> a(ava.size());
+    CK(cudaMemcpyAsync(a.p, ava.data(), ava.size() * sizeof(cplx), cudaMemcpyHostToDevice, c.stream));
+    const int big = INT_MAX;
+    CK(cudaMemcpyAsync(f->status.p, &big, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    // numeric phase, level by level (a row's L pattern are its dependencies)
+    const NumericSmem ns{std::max(P->maxcnt, 1), std::max(P->maxnl, 1), std::max(P->maxupd, 1)};
+    const size_t nsm = size_t(4) * ns.bytes();
+    require(nsm <= 220 * 1024, "ILU: factor rows too long for the device numeric phase");
+    static size_t nsm_set = 0;
+    if (nsm > 48 * 1024 && nsm > nsm_set) {
+        CK(cudaFuncSetAttribute(ilu_numeric, cudaFuncAttributeMaxDynamicSharedMemorySize, int(nsm)));
+        nsm_set = nsm;
+    }
+    for (size_t l = 0; l + 1 < P->flvl.size(); ++l) {
+        const int r0 = P->flvl[l], r1 = P->flvl[l + 1];
+        const int warps = 4;
+        ilu_numeric<<<(r1 - r0 + warps - 1) / warps, 32 * warps, nsm, c.stream>>>(
+            r0, r1, P->frows.p, P->rowoff.p, P->nl.p, P->arp.p, P->aslot.p, a.p, shift, P->lp.p, P->jdiag.p,
+            P->updptr.p, P->upd.p, f->fv.p, f->status.p, ns);
+        CK_LAUNCH();
+    }
+    int st = big;
+    CK(cudaMemcpyAsync(&st, f->status.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    if (st != big)
+        throw FwiError(FWI_ERR_ZERO_PIVOT, "ILU: zero pivot at row " + std::to_string(st) + " (consider a diagonal shift)",
+                       st);
+    const auto t_num = std::chrono::steady_clock::now();
+    const Sweep* sw[4] = {&P->L, &P->U, &P->Ut, &P->Lt};
+    for (int k = 0; k < 4; ++k) {
+        const Sweep& s = *sw[k];
+        f->lval[k].alloc(size_t(std::max(s.nent, 1)));
+        if (s.has_diag) f->ldiag[k].alloc(size_t(n));
+        f->bytes += int64_t(f->lval[k].bytes() + f->ldiag[k].bytes());
+        const int work = std::max(s.nent, n);
+        ilu_sweep_vals<<<(work + 255) / 256, 256, 0, c.stream>>>(s.nent, s.vmap.p, f->fv.p, f->lval[k].p, n,
+                                                                s.has_diag ? s.dmap.p : nullptr, s.conj_diag,
+                                                                s.has_diag ? f->ldiag[k].p : nullptr);
+        CK_LAUNCH();
+    }
     f->zslot.alloc(1);
     CK(cudaMemsetAsync(f->zslot.p, 0, sizeof(double2), c.stream));
+    f->bytes += f->fv.bytes();
+    CK(cudaStreamSynchronize(c.stream));
     if (c.ilu) ilu_free(c.ilu);
     c.ilu = f.release();
-    c.t_ilu_factor = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    const auto t_end = std::chrono::steady_clock::now();
+    c.t_ilu_factor = std::chrono::duration<double>(t_end - t_start).count();
+    if (std::getenv("FWI_ILU_TIMING"))
+        std::fprintf(stderr, "[fwi] ILU(%d) factor: operator %.3f s, pattern %.3f s%s, numeric (device) %.3f s, "
+                             "sweep values %.3f s\n",
+                     level, std::chrono::duration<double>(t_pat0 - t_start).count(),
+                     std::chrono::duration<double>(t_pat1 - t_pat0).count(),
+                     t_pat1 - t_pat0 > std::chrono::milliseconds(1) ? " (built)" : " (cached)",
+                     std::chrono::duration<double>(t_num - t_pat1).count(),
+                     std::chrono::duration<double>(t_end - t_num).count());
 }
 
 // x = M^{-1} b (or M^{-H} b) for nrhs source-major right-hand sides.
@@ -804,27 +816,28 @@ void ilu_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int nrh
     if (x != b)
         CK(cudaMemcpyAsync(x, b, size_t(nrhs) * n * sizeof(double2), cudaMemcpyDeviceToDevice, c.stream));
     IluFactor& f = *c.ilu;
+    const IluPattern& P = *f.pat;
     // level-ordered right-hand sides of the ring sweep (vectors beyond shared memory)
     double2* blo = nullptr;
     if (size_t(n + 1) * sizeof(double2) > 100 * 1024) {
         if (f.blo.count < size_t(nrhs) * size_t(n)) f.blo.alloc(size_t(nrhs) * size_t(n));
         blo = f.blo.p;
     }
-    const char* tpath = std::getenv("FWI_ILU_TRACE");
+    const char* tpath = std::getenv("FWI_ILU_TRACE");  // diagnostics: clock64 trace of the first sweep
     DevBuf<long long> tb;
     if (tpath) {
-        tb.alloc(size_t(5) * (adjoint ? f.Ut : f.L).nlev);
+        tb.alloc(size_t(5) * (adjoint ? P.Ut : P.L).nlev);
         CK(cudaMemsetAsync(tb.p, 0, tb.bytes(), c.stream));
         g_ilu_trace = tb.p;
     }
     if (!adjoint) {
-        run_sweep<kLfwd>(f.L, n, nrhs, x, c.stream, f.zslot.p, blo);
+        run_sweep<kLfwd>(P.L, f.lval[0].p, nullptr, n, nrhs, x, c.stream, f.zslot.p, blo);
         g_ilu_trace = nullptr;
-        run_sweep<kUbwd>(f.U, n, nrhs, x, c.stream, f.zslot.p, blo);
+        run_sweep<kUbwd>(P.U, f.lval[1].p, f.ldiag[1].p, n, nrhs, x, c.stream, f.zslot.p, blo);
     } else {
-        run_sweep<kUtfwd>(f.Ut, n, nrhs, x, c.stream, f.zslot.p, blo);
+        run_sweep<kUtfwd>(P.Ut, f.lval[2].p, f.ldiag[2].p, n, nrhs, x, c.stream, f.zslot.p, blo);
         g_ilu_trace = nullptr;
-        run_sweep<kLtbwd>(f.Lt, n, nrhs, x, c.stream, f.zslot.p, blo);
+        run_sweep<kLtbwd>(P.Lt, f.lval[3].p, nullptr, n, nrhs, x, c.stream, f.zslot.p, blo);
     }
     if (tpath) {
         std::vector<long long> h(tb.count);
