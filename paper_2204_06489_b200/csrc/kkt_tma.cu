@@ -443,14 +443,14 @@ CUtensorMapL2promotion l2promo() {
 // element is 8 bytes: a double (complex128: 4 per pair) or a whole complex64
 // (2 per pair; the copy engine does not interpret the payload).
 bool encode(CUtensorMap* tm, bool f32, const void* base, int nx, int nz, int K, int gr, int box_pairs,
-            int box_rows) {
+            int box_rows, int box_sources = 1) {
     auto fn = encode_fn();
     if (!fn) return false;
     const cuuint64_t e = cuuint64_t(gr) * (f32 ? 1 : 2);  // 8-byte elements per group
     const cuuint64_t cb = f32 ? 8 : 16;  // bytes per complex
     cuuint64_t dims[4] = {e, cuuint64_t(nx / gr), cuuint64_t(nz), cuuint64_t(K)};
     cuuint64_t strides[3] = {cuuint64_t(gr) * cb, cuuint64_t(nx) * cb, cuuint64_t(nx) * nz * cb};
-    cuuint32_t box[4] = {cuuint32_t(e), cuuint32_t(box_pairs), cuuint32_t(box_rows), 1};
+    cuuint32_t box[4] = {cuuint32_t(e), cuuint32_t(box_pairs), cuuint32_t(box_rows), cuuint32_t(box_sources)};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     const CUresult r = fn(tm, f32 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
                           const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -643,6 +643,7 @@ struct KmArgs {
     R* ods;
     int hlo;                          // rectangle heights are hlo or hlo + 1
     uint32_t hb[2], ub[2], tx[2];     // halo box bytes (128-aligned), u box bytes, stage fill (h = hlo, hlo+1)
+    uint32_t pb[2];                   // bytes of one source plane of a halo box (km1, KS planes per box)
     uint32_t stage_bytes;
     const T* u;                       // u through registers instead of a TMA box (ul = 1)
     int ul;
@@ -690,8 +691,14 @@ __device__ __forceinline__ float2 ldg_na<float2>(const float2* p) {
 }
 
 // One band per CTA (config 2): the single-band form of kkt_km_kernel below, kept separate because
-// the band loop costs it ~2.5 % (127.5 against 124.5 us on config 2)
-template <class A, int COLS, int S>
+// the band loop costs it ~2.5 % (127.5 against 124.5 us on config 2).
+// WS = 0: one block barrier per step, then thread 0 refills the drained stage.
+// WS = 2: per-stage "empty" mbarriers (one arrival per warp) instead of the block barrier: the
+//   last warp to finish a stage refills it (a shared counter per stage elects it), so no warp
+//   waits for the others — warps run up to S - 1 steps apart within the ring.
+// KS: sources per stage (one TMA box KS planes deep, K % KS == 0): complex64 moves half the
+//   bytes of complex128 per source, so KS = 2 gives its steps the same size.
+template <class A, int COLS, int S, int WS, int KS>
 __global__ void __launch_bounds__(512, 1)
     kkt_km1_kernel(const __grid_constant__ CUtensorMap tdu0, const __grid_constant__ CUtensorMap tla0,
                   const __grid_constant__ CUtensorMap tu0, const __grid_constant__ CUtensorMap tdu1,
@@ -702,6 +709,7 @@ __global__ void __launch_bounds__(512, 1)
     constexpr int kSl = 512 / COLS;  // row slots; a thread owns rows slot and slot + kSl
     extern __shared__ __align__(1024) unsigned char sm[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + size_t(S) * P.stage_bytes);
+    unsigned* done = reinterpret_cast<unsigned*>(bar + S);  // WS = 2: warps finished with stage s
     const int tid = threadIdx.x, lx = tid % COLS, zs = tid / COLS;
     const int nx = P.nx, nz = P.nz, K = P.K, RP = P.RP;
     const int64_t n = P.n;
@@ -713,19 +721,23 @@ __global__ void __launch_bounds__(512, 1)
     const CUtensorMap* tdu = hi ? &tdu1 : &tdu0;
     const CUtensorMap* tla = hi ? &tla1 : &tla0;
     const CUtensorMap* tu = hi ? &tu1 : &tu0;
-    const uint32_t hb = P.hb[hi], tx = P.tx[hi];
-    auto issue = [&](int k) {
-        const int s = k % S;
+    const uint32_t hb = P.hb[hi], tx = P.tx[hi], pb = P.pb[hi];
+    const int steps = K / KS;
+    auto issue = [&](int g) {  // step g: sources [g KS, g KS + KS)
+        const int s = g % S;
         unsigned char* st = sm + size_t(s) * P.stage_bytes;
         mbar_expect_tx(&bar[s], tx);
-        tma_load_4d(st, tdu, 0, x0 / P.gr - 1, z0 - 1, k, &bar[s]);
-        tma_load_4d(st + hb, tla, 0, x0 / P.gr - 1, z0 - 1, k, &bar[s]);
-        if (!P.ul) tma_load_4d(st + 2 * hb, tu, 0, x0 / P.gr, z0, k, &bar[s]);
+        tma_load_4d(st, tdu, 0, x0 / P.gr - 1, z0 - 1, g * KS, &bar[s]);
+        tma_load_4d(st + hb, tla, 0, x0 / P.gr - 1, z0 - 1, g * KS, &bar[s]);
+        if (!P.ul) tma_load_4d(st + 2 * hb, tu, 0, x0 / P.gr, z0, g * KS, &bar[s]);
     };
     if (tid == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&bar[s], 1);
+            if (WS == 2) done[s] = 0u;
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int k = 0; k < S && k < K; ++k) issue(k);
+        for (int g = 0; g < S && g < steps; ++g) issue(g);
     }
     bool act[2], hN[2], hW[2], hE[2], hS[2];
     T cD[2], cN[2], cW[2], cE[2], cS[2];
@@ -759,59 +771,83 @@ __global__ void __launch_bounds__(512, 1)
     const bool warp_full = __all_sync(0xffffffffu, full);
     const int UP = P.W;  // u box row pitch (complex)
     const int lxs = min(lx, P.W - 1);  // lanes beyond the strip read (and drop) its last column
-    T un[2] = {A::zero(), A::zero()};  // ul: u_k of the next step, loaded one step ahead
-    if (P.ul)
+    T un[KS][2];  // ul: u of the next step's sources, loaded one step ahead
 #pragma unroll
-        for (int r = 0; r < 2; ++r)
-            if (act[r]) un[r] = ldg_na(P.u + cnode[r]);
+    for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) un[kk][r] = (P.ul && act[r]) ? ldg_na(P.u + int64_t(kk) * n + cnode[r]) : A::zero();
     __syncthreads();
-    for (int k = 0; k < K; ++k) {
-        T ucur[2] = {un[0], un[1]};
-        if (P.ul && k + 1 < K)
+    for (int g = 0; g < steps; ++g) {
+        T ucur[KS][2];
 #pragma unroll
-            for (int r = 0; r < 2; ++r)
-                if (act[r]) un[r] = ldg_na(P.u + int64_t(k + 1) * n + cnode[r]);
-        const int s = k % S;
-        mbar_wait(&bar[s], (k / S) & 1);
-        const unsigned char* st = sm + size_t(s) * P.stage_bytes;
-        const T* dus = reinterpret_cast<const T*>(st) + P.gr + lxs;
-        const T* las = reinterpret_cast<const T*>(st + hb) + P.gr + lxs;
-        const T* us = reinterpret_cast<const T*>(st + 2 * hb) + lxs;
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int row = zs + kSl * r;
-            if (row >= h) continue;  // CTA-uniform per slot: the rectangle's last rows
-            T s_, t_;
-            const T* dr = dus + (row + 1) * RP;
-            const T* lr = las + (row + 1) * RP;
-            if (warp_full)
-                node_step<A, true>(dr, lr, RP, true, true, true, true, cD[r], cN[r], cW[r], cE[r], cS[r], s_, t_);
-            else
-                node_step<A, false>(dr, lr, RP, hN[r], hW[r], hE[r], hS[r], cD[r], cN[r], cW[r], cE[r], cS[r], s_,
-                                    t_);
-            const T duc = dr[0], lac = lr[0], uc = P.ul ? ucur[r] : us[row * UP];
-            pl[r] = A::radd(pl[r], A::re_pconj(P.w2, uc, lac));
-            if (!act[r]) continue;
-            const int64_t o = int64_t(k) * n + cnode[r];
-            st_mode(P.ola + o, A::sub(s_, A::pmul(P.w2, uc, dsv[r])), P.stmode);
-            if (qr[r] < qe[r] && P.nrec_k[qr[r]] == k) {
-                T f = A::zero();
-                while (qr[r] < qe[r] && P.nrec_k[qr[r]] == k) {
-                    f = A::add(f, A::rm(R(P.nrec_w2[qr[r]]), duc));
-                    ++qr[r];
-                }
-                t_ = A::add(f, t_);
-            }
-            st_mode(P.odu + o, t_, P.stmode);
+        for (int kk = 0; kk < KS; ++kk) {
+            ucur[kk][0] = un[kk][0];
+            ucur[kk][1] = un[kk][1];
         }
-        __syncthreads();  // every thread is done with stage s
-        if (tid == 0 && k + S < K) issue(k + S);
+        if (P.ul && g + 1 < steps)
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+                    if (act[r]) un[kk][r] = ldg_na(P.u + int64_t((g + 1) * KS + kk) * n + cnode[r]);
+        const int s = g % S;
+        mbar_wait(&bar[s], (g / S) & 1);
+        const unsigned char* st = sm + size_t(s) * P.stage_bytes;
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+            const int k = g * KS + kk;
+            const T* dus = reinterpret_cast<const T*>(st + kk * pb) + P.gr + lxs;
+            const T* las = reinterpret_cast<const T*>(st + hb + kk * pb) + P.gr + lxs;
+            const T* us = reinterpret_cast<const T*>(st + 2 * hb) + kk * UP * h + lxs;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int row = zs + kSl * r;
+                if (row >= h) continue;  // CTA-uniform per slot: the rectangle's last rows
+                T s_, t_;
+                const T* dr = dus + (row + 1) * RP;
+                const T* lr = las + (row + 1) * RP;
+                if (warp_full)
+                    node_step<A, true>(dr, lr, RP, true, true, true, true, cD[r], cN[r], cW[r], cE[r], cS[r], s_, t_);
+                else
+                    node_step<A, false>(dr, lr, RP, hN[r], hW[r], hE[r], hS[r], cD[r], cN[r], cW[r], cE[r], cS[r],
+                                        s_, t_);
+                const T duc = dr[0], lac = lr[0], uc = P.ul ? ucur[kk][r] : us[row * UP];
+                pl[r] = A::radd(pl[r], A::re_pconj(P.w2, uc, lac));
+                if (!act[r]) continue;
+                const int64_t o = int64_t(k) * n + cnode[r];
+                st_mode(P.ola + o, A::sub(s_, A::pmul(P.w2, uc, dsv[r])), P.stmode);
+                if (qr[r] < qe[r] && P.nrec_k[qr[r]] == k) {
+                    T f = A::zero();
+                    while (qr[r] < qe[r] && P.nrec_k[qr[r]] == k) {
+                        f = A::add(f, A::rm(R(P.nrec_w2[qr[r]]), duc));
+                        ++qr[r];
+                    }
+                    t_ = A::add(f, t_);
+                }
+                st_mode(P.odu + o, t_, P.stmode);
+            }
+        }
+        if constexpr (WS == 2) {
+            // this warp is done with stage s; the last of the 16 refills it with step g + S
+            __syncwarp();
+            if ((tid & 31) == 0) {
+                unsigned old;
+                asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                             : "=r"(old) : "r"(smem_u32(&done[s])) : "memory");
+                if (old % 16u == 15u && g + S < steps) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    issue(g + S);
+                }
+            }
+        } else {
+            __syncthreads();  // every thread is done with stage s
+            if (tid == 0 && g + S < steps) issue(g + S);
+        }
     }
 #pragma unroll
     for (int r = 0; r < 2; ++r)
         if (act[r]) P.ods[cnode[r]] = A::rsub(A::rmulr(P.eps, dsv[r]), pl[r]);
 }
-
 template <class A, int COLS, int S, bool MB>
 __global__ void __launch_bounds__(512, 1)
     kkt_km_kernel(const __grid_constant__ CUtensorMap tdu0, const __grid_constant__ CUtensorMap tla0,
@@ -967,7 +1003,8 @@ __global__ void __launch_bounds__(512, 1)
 struct KktKmPlan {
     bool ok = false;
     int cols = 128, stages = 0, G = 0, per_strip = 0, W = 0, gr = 8, RP = 0, hlo = 0, ul = 1, nbands = 0;
-    uint32_t hb[2] = {0, 0}, ub[2] = {0, 0}, tx[2] = {0, 0}, stage_bytes = 0;
+    int ws = 0, ks = 1;  // one-band kernel: ring discipline, sources per stage
+    uint32_t hb[2] = {0, 0}, ub[2] = {0, 0}, tx[2] = {0, 0}, pb[2] = {0, 0}, stage_bytes = 0;
     size_t smem = 0;
     CUtensorMap tm_u[2];
 };
@@ -976,18 +1013,28 @@ void kkt_km_plan_free(KktKmPlan* p) { delete p; }
 
 namespace {
 
-// (COLS, S, MB) instantiations; MB: several bands per CTA
-#define FWI_KM_DISPATCH(COLSv, Sv, MBv, CALL)                \
-    switch ((COLSv * 16 + Sv) * 2 + (MBv)) {                 \
-        case (128 * 16 + 2) * 2: CALL(128, 2, false); break; \
-        case (128 * 16 + 3) * 2: CALL(128, 3, false); break; \
-        case (64 * 16 + 3) * 2: CALL(64, 3, false); break;   \
-        case (64 * 16 + 4) * 2: CALL(64, 4, false); break;   \
-        case (32 * 16 + 2) * 2: CALL(32, 2, false); break;   \
-        case (32 * 16 + 3) * 2: CALL(32, 3, false); break;   \
-        case (64 * 16 + 2) * 2 + 1: CALL(64, 2, true); break; \
-        case (64 * 16 + 3) * 2 + 1: CALL(64, 3, true); break; \
-        default: CALL(64, 2, false); break;                  \
+// instantiations: (COLS, S, MB, WS, KS); MB: several bands per CTA (kkt_km_kernel), else the
+// one-band kkt_km1_kernel with its ring discipline WS and sources per stage KS
+#define FWI_KM_KEY(COLSv, Sv, MBv, WSv, KSv) (((((COLSv) * 16 + (Sv)) * 2 + (MBv)) * 4 + (WSv)) * 4 + (KSv))
+#define FWI_KM_DISPATCH(COLSv, Sv, MBv, WSv, KSv, CALL)                              \
+    switch (FWI_KM_KEY(COLSv, Sv, MBv, WSv, KSv)) {                                  \
+        case FWI_KM_KEY(128, 2, 0, 0, 1): CALL(128, 2, false, 0, 1); break;          \
+        case FWI_KM_KEY(128, 3, 0, 0, 1): CALL(128, 3, false, 0, 1); break;          \
+        case FWI_KM_KEY(64, 3, 0, 0, 1): CALL(64, 3, false, 0, 1); break;            \
+        case FWI_KM_KEY(64, 4, 0, 0, 1): CALL(64, 4, false, 0, 1); break;            \
+        case FWI_KM_KEY(32, 2, 0, 0, 1): CALL(32, 2, false, 0, 1); break;            \
+        case FWI_KM_KEY(32, 3, 0, 0, 1): CALL(32, 3, false, 0, 1); break;            \
+        case FWI_KM_KEY(64, 2, 0, 2, 1): CALL(64, 2, false, 2, 1); break;            \
+        case FWI_KM_KEY(64, 3, 0, 2, 1): CALL(64, 3, false, 2, 1); break;            \
+        case FWI_KM_KEY(64, 4, 0, 2, 1): CALL(64, 4, false, 2, 1); break;            \
+        case FWI_KM_KEY(64, 2, 0, 0, 2): CALL(64, 2, false, 0, 2); break;            \
+        case FWI_KM_KEY(64, 3, 0, 0, 2): CALL(64, 3, false, 0, 2); break;            \
+        case FWI_KM_KEY(64, 2, 0, 2, 2): CALL(64, 2, false, 2, 2); break;            \
+        case FWI_KM_KEY(64, 3, 0, 2, 2): CALL(64, 3, false, 2, 2); break;            \
+        case FWI_KM_KEY(64, 4, 0, 2, 2): CALL(64, 4, false, 2, 2); break;            \
+        case FWI_KM_KEY(64, 2, 1, 0, 1): CALL(64, 2, true, 0, 1); break;             \
+        case FWI_KM_KEY(64, 3, 1, 0, 1): CALL(64, 3, true, 0, 1); break;             \
+        default: CALL(64, 2, false, 0, 1); break;                                    \
     }
 
 template <class A>
@@ -1035,22 +1082,38 @@ KktKmPlan* build_km_plan(Ctx& c, bool f32) {
     // shared memory alone slows the C2 apply: +30 KB 128 -> 140 us, +60 KB 154 us)
     p->ul = 1;
     if (const char* e = std::getenv("FWI_KKT_KM_ULDG")) p->ul = std::atoi(e) != 0;
+    const bool mb = p->G < p->nbands;
+    // one-band kernel: ring discipline (FWI_KKT_KM_WS) and sources per stage (FWI_KKT_KM_KS)
+    if (!mb) {
+        // complex64: two sources per stage, so a step moves the bytes of a complex128 step
+        // (C2: 91.6 -> 82.9 us with non-allocating stores, tools/exp_km_c64.sh); the per-stage
+        // empty barriers (WS = 2) measured within noise of the block barrier (124.6 vs 125.2 us
+        // at 3 stages for complex128, slower for complex64), so the block barrier stays
+        p->ks = f32 ? 2 : 1;
+        if (const char* e = std::getenv("FWI_KKT_KM_WS")) p->ws = std::atoi(e) == 2 ? 2 : 0;
+        if (const char* e = std::getenv("FWI_KKT_KM_KS")) p->ks = std::atoi(e) == 2 ? 2 : 1;
+        if (cols != 64) p->ws = 0, p->ks = 1;
+        if (K % p->ks != 0 || !p->ul) p->ks = 1;
+    }
+    const int ks = p->ks;
     for (int v = 0; v < 2; ++v) {
         const int h = p->hlo + v;
-        p->hb[v] = align128(size_t(p->RP) * (h + 2) * es);
+        p->pb[v] = uint32_t(size_t(p->RP) * (h + 2) * es);
+        p->hb[v] = align128(size_t(ks) * p->pb[v]);
         p->ub[v] = p->ul ? 0 : align128(size_t(W) * h * es);
-        p->tx[v] = uint32_t(2 * size_t(p->RP) * (h + 2) * es + (p->ul ? 0 : size_t(W) * h * es));
+        p->tx[v] = uint32_t(2 * size_t(ks) * p->pb[v] + (p->ul ? 0 : size_t(W) * h * es));
         p->stage_bytes = std::max(p->stage_bytes, 2 * p->hb[v] + p->ub[v]);
     }
     const size_t budget = 227 * 1024 - 128;
     // two stages in flight (three for complex64, half the bytes per stage): deeper rings are
     // measurably slower with the output stores sharing the memory system (C2: 3 stages 181 us,
     // 4 stages 209 us against 129 us)
-    int st = f32 ? 3 : 2;
+    int st = (f32 && p->ks == 1) ? 3 : 2;
     if (const char* e = std::getenv("FWI_KKT_KM_STAGES")) st = std::atoi(e);
-    const bool mb = p->G < p->nbands;
     auto valid = [&](int v) {
         if (mb) return cols == 64 && (v == 2 || v == 3);
+        if (p->ks == 2 && p->ws == 0) return v == 2 || v == 3;
+        if (p->ws == 2) return v >= 2 && v <= 4;
         return cols == 32 ? (v == 2 || v == 3) : cols == 128 ? (v == 2 || v == 3) : (v >= 2 && v <= 4);
     };
     while (st > 2 && (!valid(st) || size_t(st) * p->stage_bytes > budget)) --st;
@@ -1060,12 +1123,12 @@ KktKmPlan* build_km_plan(Ctx& c, bool f32) {
     p->smem = size_t(st) * p->stage_bytes + 128;
     if (const char* e = std::getenv("FWI_KKT_KM_PAD_KB"))  // diagnostics: unused extra shared memory
         p->smem = std::min<size_t>(227 * 1024, p->smem + size_t(std::atoi(e)) * 1024);
-#define FWI_KM_ATTR(COLSc, Sc, MBc)                                                                       \
+#define FWI_KM_ATTR(COLSc, Sc, MBc, WSc, KSc)                                                             \
     CK(MBc ? cudaFuncSetAttribute(kkt_km_kernel<A, COLSc, Sc, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                   int(p->smem))                                                             \
-           : cudaFuncSetAttribute(kkt_km1_kernel<A, COLSc, Sc>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                                  int(p->smem)))
-    FWI_KM_DISPATCH(cols, st, mb ? 1 : 0, FWI_KM_ATTR);
+           : cudaFuncSetAttribute(kkt_km1_kernel<A, COLSc, Sc, WSc, KSc>,                                     \
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)))
+    FWI_KM_DISPATCH(cols, st, mb ? 1 : 0, p->ws, p->ks, FWI_KM_ATTR);
 #undef FWI_KM_ATTR
     const void* ubase = f32 ? static_cast<const void*>(c.u32.p) : static_cast<const void*>(c.u.p);
     for (int v = 0; v < 2; ++v)
@@ -1079,8 +1142,8 @@ bool launch_km(Ctx& c, KktKmPlan* p, const typename A::T* du, const typename A::
                typename A::T* odu, typename A::R* ods, typename A::T* ola, bool f32) {
     CUtensorMap tdu[2], tla[2];
     for (int v = 0; v < 2; ++v) {
-        if (!encode(&tdu[v], f32, du, c.nx, c.nz, c.K, p->gr, p->RP / p->gr, p->hlo + v + 2)) return false;
-        if (!encode(&tla[v], f32, la, c.nx, c.nz, c.K, p->gr, p->RP / p->gr, p->hlo + v + 2)) return false;
+        if (!encode(&tdu[v], f32, du, c.nx, c.nz, c.K, p->gr, p->RP / p->gr, p->hlo + v + 2, p->ks)) return false;
+        if (!encode(&tla[v], f32, la, c.nx, c.nz, c.K, p->gr, p->RP / p->gr, p->hlo + v + 2, p->ks)) return false;
     }
     KmArgs<A> a;
     a.nx = c.nx;
@@ -1115,26 +1178,27 @@ bool launch_km(Ctx& c, KktKmPlan* p, const typename A::T* du, const typename A::
         a.hb[v] = p->hb[v];
         a.ub[v] = p->ub[v];
         a.tx[v] = p->tx[v];
+        a.pb[v] = p->pb[v];
     }
     a.stage_bytes = p->stage_bytes;
     a.ul = p->ul;
     // complex128 outputs bypass the L1 (st.global.L1::no_allocate): with L1-allocating streaming
     // stores the apply needs free L1 (unused shared memory and deeper rings slowed it); without
-    // allocation it does not, 126 -> 124.7 us. complex64 keeps .cs (0.088 vs 0.090 ms).
-    a.stmode = f32 ? 0 : 1;
+    // allocation it does not, 126 -> 124.7 us. complex64 with one source per stage keeps .cs (0.088 vs 0.090 ms); with two, no_allocate (82.9 vs 85.0 us).
+    a.stmode = (f32 && p->ks == 1) ? 0 : 1;
     if (const char* e = std::getenv("FWI_KKT_KM_ST")) a.stmode = std::atoi(e);
     a.u = reinterpret_cast<const typename A::T*>(f32 ? static_cast<const void*>(c.u32.p)
                                                     : static_cast<const void*>(c.u.p));
-#define FWI_KM_LAUNCH(COLSc, Sc, MBc)                                                                      \
+#define FWI_KM_LAUNCH(COLSc, Sc, MBc, WSc, KSc)                                                            \
     ((MBc ? kkt_km_kernel<A, COLSc, Sc, true><<<p->G, 512, p->smem, c.stream>>>(tdu[0], tla[0], p->tm_u[0],     \
                                                                               tdu[1], tla[1], p->tm_u[1], a)  \
-          : kkt_km1_kernel<A, COLSc, Sc><<<p->G, 512, p->smem, c.stream>>>(tdu[0], tla[0], p->tm_u[0], tdu[1],   \
-                                                                         tla[1], p->tm_u[1], a)),             \
+          : kkt_km1_kernel<A, COLSc, Sc, WSc, KSc><<<p->G, 512, p->smem, c.stream>>>(                          \
+                tdu[0], tla[0], p->tm_u[0], tdu[1], tla[1], p->tm_u[1], a)),                                   \
      c.kkt_kernel[f32 ? 1 : 0] = MBc ? (f32 ? "kkt_km_kernel<F32, " #COLSc ", " #Sc ", bands> (source-major TMA K1, csrc/kkt_tma.cu)" \
                                            : "kkt_km_kernel<F64, " #COLSc ", " #Sc ", bands> (source-major TMA K1, csrc/kkt_tma.cu)") \
-                                     : (f32 ? "kkt_km1_kernel<F32, " #COLSc ", " #Sc "> (source-major TMA K1, one band per CTA, csrc/kkt_tma.cu)" \
-                                           : "kkt_km1_kernel<F64, " #COLSc ", " #Sc "> (source-major TMA K1, one band per CTA, csrc/kkt_tma.cu)"))
-    FWI_KM_DISPATCH(p->cols, p->stages, p->G < p->nbands ? 1 : 0, FWI_KM_LAUNCH);
+                                     : (f32 ? "kkt_km1_kernel<F32, " #COLSc ", " #Sc ", " #WSc ", " #KSc "> (source-major TMA K1, one band per CTA, csrc/kkt_tma.cu)" \
+                                           : "kkt_km1_kernel<F64, " #COLSc ", " #Sc ", " #WSc ", " #KSc "> (source-major TMA K1, one band per CTA, csrc/kkt_tma.cu)"))
+    FWI_KM_DISPATCH(p->cols, p->stages, p->G < p->nbands ? 1 : 0, p->ws, p->ks, FWI_KM_LAUNCH);
 #undef FWI_KM_LAUNCH
     CK_LAUNCH();
     return true;

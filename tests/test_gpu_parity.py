@@ -294,6 +294,33 @@ def test_c64_apply_deviation(variant, monkeypatch):
     assert err < 1e-5
 
 
+@pytest.mark.parametrize("env", [{"FWI_KKT_KM_KS": "swap"}, {"FWI_KKT_KM_WS": "2", "FWI_KKT_KM_STAGES": "3"},
+                                 {"FWI_KKT_KM_WS": "2", "FWI_KKT_KM_KS": "2", "FWI_KKT_KM_STAGES": "4"}])
+@pytest.mark.parametrize("c64", [False, True])
+def test_km1_ring_variants_identical(env, c64, monkeypatch):
+    """The one-band source-major K1's ring disciplines (block barrier / per-stage empty barriers)
+    and sources per stage (complex64: two by default) give bit-identical applies on config 2."""
+    p = c2_problem()
+    x = random_kkt(p, 11)
+    prec = _abi.FWI_C64 if c64 else _abi.FWI_C128
+    xin = x.astype(np.float32) if c64 else x
+
+    def run():
+        dev = fw.GnState(p, exact=False, c64=c64)
+        try:
+            out = fw.kkt_apply(dev, fw.KktVector.from_host(dev, xin, prec)).to_host()
+            return out, dev.kkt_kernel(prec)
+        finally:
+            dev.close()
+
+    base, kbase = run()
+    for k, v in env.items():
+        monkeypatch.setenv(k, ("1" if c64 else "2") if v == "swap" else v)
+    got, kgot = run()
+    assert "kkt_km1_kernel" in kbase and "kkt_km1_kernel" in kgot and kbase != kgot, (kbase, kgot)
+    assert np.array_equal(got, base)
+
+
 # ---- generic GMRES known answers (tests/test_krylov.cpp:63-125, real systems)
 
 def test_gmres_identity_one_iteration():
