@@ -19,6 +19,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <climits>
+#include <vector>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -643,7 +646,12 @@ struct KmArgs {
     R* ods;
     int hlo;                          // rectangle heights are hlo or hlo + 1
     uint32_t hb[2], ub[2], tx[2];     // halo box bytes (128-aligned), u box bytes, stage fill (h = hlo, hlo+1)
-    uint32_t pb[2];                   // bytes of one source plane of a halo box (km1, KS planes per box)
+    uint32_t pb[2];                   // bytes of one source plane of a halo box
+    // one-band kernel (kkt_km1_kernel): a rectangle per CTA and up to kKmShapes box shapes
+    uint32_t shb[4], stx[4], spb[4];  // per shape: halo box bytes, stage fill, plane bytes
+    int srp[4];                       // per shape: shared-memory row pitch (complex)
+    const int4* rects;                // per CTA: x0, w, z0, h
+    const unsigned char* rshape;      // per CTA: its box shape
     uint32_t stage_bytes;
     const T* u;                       // u through registers instead of a TMA box (ul = 1)
     int ul;
@@ -698,12 +706,14 @@ __device__ __forceinline__ float2 ldg_na<float2>(const float2* p) {
 //   waits for the others — warps run up to S - 1 steps apart within the ring.
 // KS: sources per stage (one TMA box KS planes deep, K % KS == 0): complex64 moves half the
 //   bytes of complex128 per source, so KS = 2 gives its steps the same size.
+constexpr int kKmShapes = 4;
+struct KmMaps {  // TMA descriptors of the one-band kernel's box shapes (du, lambda)
+    CUtensorMap du[kKmShapes], la[kKmShapes];
+};
+
 template <class A, int COLS, int S, int WS, int KS>
 __global__ void __launch_bounds__(512, 1)
-    kkt_km1_kernel(const __grid_constant__ CUtensorMap tdu0, const __grid_constant__ CUtensorMap tla0,
-                  const __grid_constant__ CUtensorMap tu0, const __grid_constant__ CUtensorMap tdu1,
-                  const __grid_constant__ CUtensorMap tla1, const __grid_constant__ CUtensorMap tu1,
-                  const KmArgs<A> P) {
+    kkt_km1_kernel(const __grid_constant__ KmMaps M, const KmArgs<A> P) {
     using T = typename A::T;
     using R = typename A::R;
     constexpr int kSl = 512 / COLS;  // row slots; a thread owns rows slot and slot + kSl
@@ -711,17 +721,16 @@ __global__ void __launch_bounds__(512, 1)
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + size_t(S) * P.stage_bytes);
     unsigned* done = reinterpret_cast<unsigned*>(bar + S);  // WS = 2: warps finished with stage s
     const int tid = threadIdx.x, lx = tid % COLS, zs = tid / COLS;
-    const int nx = P.nx, nz = P.nz, K = P.K, RP = P.RP;
+    const int nx = P.nx, nz = P.nz, K = P.K;
     const int64_t n = P.n;
-    // this CTA's rectangle: strip b / per_strip, rows [z0, z1) of it
-    const int strip = blockIdx.x / P.per_strip, i = blockIdx.x % P.per_strip;
-    const int z0 = int(int64_t(i) * nz / P.per_strip), z1 = int(int64_t(i + 1) * nz / P.per_strip);
-    const int hi = (z1 - z0) - P.hlo;  // 0 or 1: which box shape
-    const int x0 = strip * P.W, w = min(P.W, nx - x0), h = z1 - z0;
-    const CUtensorMap* tdu = hi ? &tdu1 : &tdu0;
-    const CUtensorMap* tla = hi ? &tla1 : &tla0;
-    const CUtensorMap* tu = hi ? &tu1 : &tu0;
-    const uint32_t hb = P.hb[hi], tx = P.tx[hi], pb = P.pb[hi];
+    // this CTA's rectangle and its box shape (the plan balances the rectangles' areas)
+    const int4 rc = P.rects[blockIdx.x];
+    const int shp = P.rshape[blockIdx.x];
+    const int x0 = rc.x, w = rc.y, z0 = rc.z, h = rc.w;
+    const int RP = P.srp[shp];
+    const CUtensorMap* tdu = &M.du[shp];
+    const CUtensorMap* tla = &M.la[shp];
+    const uint32_t hb = P.shb[shp], tx = P.stx[shp], pb = P.spb[shp];
     const int steps = K / KS;
     auto issue = [&](int g) {  // step g: sources [g KS, g KS + KS)
         const int s = g % S;
@@ -729,7 +738,6 @@ __global__ void __launch_bounds__(512, 1)
         mbar_expect_tx(&bar[s], tx);
         tma_load_4d(st, tdu, 0, x0 / P.gr - 1, z0 - 1, g * KS, &bar[s]);
         tma_load_4d(st + hb, tla, 0, x0 / P.gr - 1, z0 - 1, g * KS, &bar[s]);
-        if (!P.ul) tma_load_4d(st + 2 * hb, tu, 0, x0 / P.gr, z0, g * KS, &bar[s]);
     };
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
@@ -769,13 +777,12 @@ __global__ void __launch_bounds__(512, 1)
         pl[r] = R(0);
     }
     const bool warp_full = __all_sync(0xffffffffu, full);
-    const int UP = P.W;  // u box row pitch (complex)
-    const int lxs = min(lx, P.W - 1);  // lanes beyond the strip read (and drop) its last column
-    T un[KS][2];  // ul: u of the next step's sources, loaded one step ahead
+    const int lxs = min(lx, w - 1);  // lanes beyond the rectangle read (and drop) its last column
+    T un[KS][2];  // u of the next step's sources, loaded one step ahead (u is read once per node)
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk)
 #pragma unroll
-        for (int r = 0; r < 2; ++r) un[kk][r] = (P.ul && act[r]) ? ldg_na(P.u + int64_t(kk) * n + cnode[r]) : A::zero();
+        for (int r = 0; r < 2; ++r) un[kk][r] = act[r] ? ldg_na(P.u + int64_t(kk) * n + cnode[r]) : A::zero();
     __syncthreads();
     for (int g = 0; g < steps; ++g) {
         T ucur[KS][2];
@@ -784,7 +791,7 @@ __global__ void __launch_bounds__(512, 1)
             ucur[kk][0] = un[kk][0];
             ucur[kk][1] = un[kk][1];
         }
-        if (P.ul && g + 1 < steps)
+        if (g + 1 < steps)
 #pragma unroll
             for (int kk = 0; kk < KS; ++kk)
 #pragma unroll
@@ -798,7 +805,6 @@ __global__ void __launch_bounds__(512, 1)
             const int k = g * KS + kk;
             const T* dus = reinterpret_cast<const T*>(st + kk * pb) + P.gr + lxs;
             const T* las = reinterpret_cast<const T*>(st + hb + kk * pb) + P.gr + lxs;
-            const T* us = reinterpret_cast<const T*>(st + 2 * hb) + kk * UP * h + lxs;
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const int row = zs + kSl * r;
@@ -811,7 +817,7 @@ __global__ void __launch_bounds__(512, 1)
                 else
                     node_step<A, false>(dr, lr, RP, hN[r], hW[r], hE[r], hS[r], cD[r], cN[r], cW[r], cE[r], cS[r],
                                         s_, t_);
-                const T duc = dr[0], lac = lr[0], uc = P.ul ? ucur[kk][r] : us[row * UP];
+                const T duc = dr[0], lac = lr[0], uc = ucur[kk][r];
                 pl[r] = A::radd(pl[r], A::re_pconj(P.w2, uc, lac));
                 if (!act[r]) continue;
                 const int64_t o = int64_t(k) * n + cnode[r];
@@ -1007,6 +1013,12 @@ struct KktKmPlan {
     uint32_t hb[2] = {0, 0}, ub[2] = {0, 0}, tx[2] = {0, 0}, pb[2] = {0, 0}, stage_bytes = 0;
     size_t smem = 0;
     CUtensorMap tm_u[2];
+    // one-band kernel: a rectangle per CTA, box shapes (box width in columns, rows)
+    int nshapes = 0, shw[4] = {0, 0, 0, 0}, shh[4] = {0, 0, 0, 0};
+    uint32_t shb[4] = {0, 0, 0, 0}, stx[4] = {0, 0, 0, 0}, spb[4] = {0, 0, 0, 0};
+    int max_area = 0;  // largest rectangle (nodes): the apply's time follows it (C2, round 2)
+    DevBuf<int4> rects;
+    DevBuf<unsigned char> rshape;
 };
 
 void kkt_km_plan_free(KktKmPlan* p) { delete p; }
@@ -1037,6 +1049,63 @@ namespace {
         default: CALL(64, 2, false, 0, 1); break;                                    \
     }
 
+// Area-balanced rectangles for the one-band kernel (FWI_KKT_KM_BALANCED=1, an experiment). Every
+// CTA walks all K sources over its own rectangle and the CTAs cannot share work (each node's
+// K-sum is one CTA's), so the apply takes as long as the slowest CTA: on C2, 128 CTAs of 16 x 64
+// nodes take 136.9 us against 125.2 us for 144 CTAs of at most 15 x 64. Strips of two widths
+// (multiples of the 8-complex TMA group), each cut into equal bands of 8..maxrows rows, bring the
+// largest rectangle to the smallest area achievable (C2: one 64-column strip of 19 bands and
+// eight 56-column strips of 16 bands = 147 CTAs of at most 896 nodes, against 960) — and measure
+// 137.0 us: a CTA's time follows its rows x 64 lanes (its warp-rows), not its area, so the
+// 56-column strips cost what 64-column ones do (tools/exp_km_rects.sh). Returns the strips as
+// (width, bands) pairs left to right, or an empty list.
+std::vector<std::pair<int, int>> balanced_strips(int nx, int nz, int sms, int cols, int maxrows, int minrows,
+                                                 int gr, int& area) {
+    std::vector<int> widths;
+    for (int w = cols; w >= gr; w -= gr) widths.push_back(w);
+    std::vector<int> targets;
+    for (int w : widths)
+        for (int h = minrows; h <= maxrows; ++h) targets.push_back(w * h);
+    std::sort(targets.begin(), targets.end());
+    targets.erase(std::unique(targets.begin(), targets.end()), targets.end());
+    for (int M : targets) {
+        if (int64_t(M) * sms < int64_t(nx) * nz) continue;
+        auto bands = [&](int w) {  // fewest bands of <= M nodes, or 0 when the rows fall short
+            const int h = std::min(maxrows, M / w);
+            if (h < minrows) return 0;
+            const int b = (nz + h - 1) / h;
+            return nz / b >= minrows ? b : 0;
+        };
+        int best = INT_MAX;
+        std::vector<std::pair<int, int>> pick;
+        for (int wa : widths) {
+            const int ba = bands(wa);
+            if (!ba) continue;
+            for (int wb : widths) {
+                if (wb > wa) continue;
+                const int bb = bands(wb);
+                if (!bb) continue;
+                for (int na = 1; na * wa <= nx; ++na) {
+                    const int rem = nx - na * wa;
+                    if (wb == wa ? rem != 0 : (rem == 0 || rem % wb != 0)) continue;
+                    const int nb = wb == wa ? 0 : rem / wb;
+                    const int total = na * ba + nb * bb;
+                    if (total <= sms && total < best) {
+                        best = total;
+                        pick.assign(size_t(na), {wa, ba});
+                        for (int q = 0; q < nb; ++q) pick.push_back({wb, bb});
+                    }
+                }
+            }
+        }
+        if (!pick.empty()) {
+            area = M;
+            return pick;
+        }
+    }
+    return {};
+}
+
 template <class A>
 KktKmPlan* build_km_plan(Ctx& c, bool f32) {
     auto p = std::make_unique<KktKmPlan>();
@@ -1044,46 +1113,64 @@ KktKmPlan* build_km_plan(Ctx& c, bool f32) {
     const int es = f32 ? 8 : 16;
     if (nx % 2 != 0 || !encode_fn()) return p.release();
     const int sms = sm_count();
-    // rectangles: per_strip = SMs / strips per strip, heights <= 2 x (512 / COLS) rows. 64-column
-    // strips (measured best on C2: 128 us per apply against 142 us with 128 columns and 131 us with
-    // 32); the kernel is chosen only when the rectangles have >= 8 rows — shorter ones spend too
-    // much on halo rows, and the chunked tile kernel does as well or better there (config 3).
-    // One band per CTA when every SM's share fits a band of <= 2 x 512/COLS rows (config 2: 8
-    // strips x 18 bands of 14-15 rows); otherwise bands of ~15 rows, several per CTA, each walked
-    // over all sources (config 5: 32 strips x 69 bands on 148 CTAs). FWI_KKT_KM_ROWS sets the band
-    // height (tests: several bands per CTA on small grids).
+    const bool force = std::getenv("FWI_KKT_KM_FORCE") != nullptr;
+    // Rectangles of <= 2 x (512 / COLS) rows. 64-column strips (measured best on C2 with equal
+    // strips: 128 us per apply against 142 us with 128 columns and 131 us with 32); the kernel is
+    // chosen only when the rectangles have >= 8 rows — shorter ones spend too much on halo rows.
+    // One rectangle per CTA when the grid fits (config 2: 8 strips x 18 bands of 14-15 rows);
+    // otherwise bands of ~15 rows, several per CTA, each walked over all sources (config 5: 32
+    // strips x 69 bands on 148 CTAs). FWI_KKT_KM_ROWS sets a uniform band height (tests: several
+    // bands per CTA on small grids). FWI_KKT_KM_BALANCED=1 plans area-balanced strips of two
+    // widths instead (balanced_strips; measured slower, kept as the documented experiment).
     int cols = 64;
-    if (const char* e = std::getenv("FWI_KKT_KM_COLS")) cols = std::atoi(e) == 128 ? 128 : std::atoi(e) == 32 ? 32 : 64;
-    const int maxrows = 2 * (512 / cols);
+    const char* ecols = std::getenv("FWI_KKT_KM_COLS");
+    if (ecols) cols = std::atoi(ecols) == 128 ? 128 : std::atoi(ecols) == 32 ? 32 : 64;
+    int maxrows = 2 * (512 / cols);
     const int nsx = (nx + cols - 1) / cols;
     int per = std::min(sms / nsx, nz);
     if (per < 1 || (nz + per - 1) / per > maxrows) per = (nz + 14) / 15;
-    if (const char* e = std::getenv("FWI_KKT_KM_ROWS")) per = (nz + std::max(1, std::atoi(e)) - 1) / std::max(1, std::atoi(e));
+    const bool rows_env = std::getenv("FWI_KKT_KM_ROWS") != nullptr;
+    if (rows_env) per = (nz + std::max(1, std::atoi(std::getenv("FWI_KKT_KM_ROWS"))) - 1) /
+                        std::max(1, std::atoi(std::getenv("FWI_KKT_KM_ROWS")));
     per = std::max(1, std::min(per, nz));
-    const int hmax = (nz + per - 1) / per;
-    if (hmax > maxrows) return p.release();
-    if (nz / per < 8 && !std::getenv("FWI_KKT_KM_FORCE")) return p.release();
     const int W = ((nx + nsx - 1) / nsx + 1) / 2 * 2;  // even strip width <= cols
-    if (W > cols) return p.release();
     int gr = 8;
     if (const char* e = std::getenv("FWI_KKT_GRP")) gr = std::max(1, std::atoi(e));
     if (nx % gr != 0 || W % gr != 0) gr = 2;
+    bool uniform_ok = (nz + per - 1) / per <= maxrows && (nz / per >= 8 || force) && W <= cols;
+    int uniform_area = W * ((nz + per - 1) / per);
+    int G = std::min(sms, nsx * per);
+    if (const char* e = std::getenv("FWI_KKT_KM_G")) G = std::max(1, std::min(G, std::atoi(e)));  // tests
+    bool mb = G < nsx * per;
+    // balanced one-rectangle-per-CTA layout (strips of two widths, multiples of the TMA group)
+    std::vector<std::pair<int, int>> strips;
+    int bal_area = 0;
+    if (std::getenv("FWI_KKT_KM_BALANCED") && !rows_env && !std::getenv("FWI_KKT_KM_G") && nx % 8 == 0 &&
+        !std::getenv("FWI_KKT_GRP")) {
+        const int bcols = ecols ? cols : 64;
+        strips = balanced_strips(nx, nz, sms, std::min(bcols, 64), 2 * (512 / std::min(bcols, 64)), force ? 1 : 8, 8,
+                                 bal_area);
+        if (!strips.empty() && uniform_ok && !mb && bal_area >= uniform_area) strips.clear();
+    }
+    if (!strips.empty()) {
+        int wmax = 0;
+        for (auto& sb : strips) wmax = std::max(wmax, sb.first);
+        if (wmax <= 32 && !ecols) cols = 32;  // every lane of a 32-column CTA has a column
+        maxrows = 2 * (512 / cols);
+        gr = 8;
+        mb = false;
+    } else if (!uniform_ok) {
+        return p.release();
+    }
     p->cols = cols;
-    p->per_strip = per;
-    p->nbands = nsx * per;
-    p->G = std::min(sms, p->nbands);
-    if (const char* e = std::getenv("FWI_KKT_KM_G")) p->G = std::max(1, std::min(p->G, std::atoi(e)));  // tests
-    p->W = W;
     p->gr = gr;
-    p->RP = W + 2 * gr;
-    p->hlo = nz / per;
+    p->ul = 1;
     // u through registers (non-allocating loads) rather than a third TMA box: shared memory is
     // carved out of the L1, and the L1 space is what keeps the TMA loads in flight (unused extra
-    // shared memory alone slows the C2 apply: +30 KB 128 -> 140 us, +60 KB 154 us)
-    p->ul = 1;
-    if (const char* e = std::getenv("FWI_KKT_KM_ULDG")) p->ul = std::atoi(e) != 0;
-    const bool mb = p->G < p->nbands;
-    // one-band kernel: ring discipline (FWI_KKT_KM_WS) and sources per stage (FWI_KKT_KM_KS)
+    // shared memory alone slows the C2 apply: +30 KB 128 -> 140 us, +60 KB 154 us). The banded
+    // kernel keeps the TMA form as a diagnostic (FWI_KKT_KM_ULDG=0).
+    if (mb)
+        if (const char* e = std::getenv("FWI_KKT_KM_ULDG")) p->ul = std::atoi(e) != 0;
     if (!mb) {
         // complex64: two sources per stage, so a step moves the bytes of a complex128 step
         // (C2: 91.6 -> 82.9 us with non-allocating stores, tools/exp_km_c64.sh); the per-stage
@@ -1093,21 +1180,73 @@ KktKmPlan* build_km_plan(Ctx& c, bool f32) {
         if (const char* e = std::getenv("FWI_KKT_KM_WS")) p->ws = std::atoi(e) == 2 ? 2 : 0;
         if (const char* e = std::getenv("FWI_KKT_KM_KS")) p->ks = std::atoi(e) == 2 ? 2 : 1;
         if (cols != 64) p->ws = 0, p->ks = 1;
-        if (K % p->ks != 0 || !p->ul) p->ks = 1;
-    }
-    const int ks = p->ks;
-    for (int v = 0; v < 2; ++v) {
-        const int h = p->hlo + v;
-        p->pb[v] = uint32_t(size_t(p->RP) * (h + 2) * es);
-        p->hb[v] = align128(size_t(ks) * p->pb[v]);
-        p->ub[v] = p->ul ? 0 : align128(size_t(W) * h * es);
-        p->tx[v] = uint32_t(2 * size_t(ks) * p->pb[v] + (p->ul ? 0 : size_t(W) * h * es));
-        p->stage_bytes = std::max(p->stage_bytes, 2 * p->hb[v] + p->ub[v]);
+        if (K % p->ks != 0) p->ks = 1;
+        // the rectangles and their box shapes
+        std::vector<int4> rc;
+        std::vector<unsigned char> rs;
+        auto shape_of = [&](int wbox, int h) {
+            for (int q = 0; q < p->nshapes; ++q)
+                if (p->shw[q] == wbox && p->shh[q] == h) return q;
+            if (p->nshapes == kKmShapes) return -1;
+            p->shw[p->nshapes] = wbox;
+            p->shh[p->nshapes] = h;
+            return p->nshapes++;
+        };
+        auto add_strip = [&](int x0, int w, int wbox, int bands) {
+            for (int b = 0; b < bands; ++b) {
+                const int z0 = int(int64_t(b) * nz / bands), z1 = int(int64_t(b + 1) * nz / bands);
+                const int q = shape_of(wbox, z1 - z0);
+                if (q < 0) return false;
+                rc.push_back(make_int4(x0, w, z0, z1 - z0));
+                rs.push_back((unsigned char)q);
+                p->max_area = std::max(p->max_area, w * (z1 - z0));
+            }
+            return true;
+        };
+        bool okr = true;
+        if (!strips.empty()) {
+            int x0 = 0;
+            for (auto& sb : strips) {
+                okr = okr && add_strip(x0, sb.first, sb.first, sb.second);
+                x0 += sb.first;
+            }
+        } else {
+            for (int q = 0; q < nsx; ++q) okr = okr && add_strip(q * W, std::min(W, nx - q * W), W, per);
+        }
+        if (!okr || int(rc.size()) > sms) return p.release();
+        p->G = int(rc.size());
+        p->nbands = p->G;
+        p->rects.alloc(rc.size());
+        p->rshape.alloc(rs.size());
+        CK(cudaMemcpy(p->rects.p, rc.data(), rc.size() * sizeof(int4), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(p->rshape.p, rs.data(), rs.size(), cudaMemcpyHostToDevice));
+        for (int q = 0; q < p->nshapes; ++q) {
+            const int rp = p->shw[q] + 2 * gr;
+            p->spb[q] = uint32_t(size_t(rp) * (p->shh[q] + 2) * es);
+            p->shb[q] = align128(size_t(p->ks) * p->spb[q]);
+            p->stx[q] = 2 * p->ks * p->spb[q];
+            p->stage_bytes = std::max(p->stage_bytes, 2 * p->shb[q]);
+        }
+    } else {
+        p->per_strip = per;
+        p->nbands = nsx * per;
+        p->G = G;
+        p->W = W;
+        p->RP = W + 2 * gr;
+        p->hlo = nz / per;
+        for (int v = 0; v < 2; ++v) {
+            const int h = p->hlo + v;
+            p->pb[v] = uint32_t(size_t(p->RP) * (h + 2) * es);
+            p->hb[v] = align128(size_t(p->pb[v]));
+            p->ub[v] = p->ul ? 0 : align128(size_t(W) * h * es);
+            p->tx[v] = uint32_t(2 * size_t(p->pb[v]) + (p->ul ? 0 : size_t(W) * h * es));
+            p->stage_bytes = std::max(p->stage_bytes, 2 * p->hb[v] + p->ub[v]);
+        }
     }
     const size_t budget = 227 * 1024 - 128;
-    // two stages in flight (three for complex64, half the bytes per stage): deeper rings are
+    // two stages in flight (three for complex64 with one source per stage): deeper rings are
     // measurably slower with the output stores sharing the memory system (C2: 3 stages 181 us,
-    // 4 stages 209 us against 129 us)
+    // 4 stages 209 us against 129 us, with L1-allocating stores)
     int st = (f32 && p->ks == 1) ? 3 : 2;
     if (const char* e = std::getenv("FWI_KKT_KM_STAGES")) st = std::atoi(e);
     auto valid = [&](int v) {
@@ -1130,9 +1269,22 @@ KktKmPlan* build_km_plan(Ctx& c, bool f32) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)))
     FWI_KM_DISPATCH(cols, st, mb ? 1 : 0, p->ws, p->ks, FWI_KM_ATTR);
 #undef FWI_KM_ATTR
-    const void* ubase = f32 ? static_cast<const void*>(c.u32.p) : static_cast<const void*>(c.u.p);
-    for (int v = 0; v < 2; ++v)
-        if (!ubase || !encode(&p->tm_u[v], f32, ubase, nx, nz, K, gr, W / gr, p->hlo + v)) return p.release();
+    if (mb) {
+        const void* ubase = f32 ? static_cast<const void*>(c.u32.p) : static_cast<const void*>(c.u.p);
+        for (int v = 0; v < 2; ++v)
+            if (!ubase || !encode(&p->tm_u[v], f32, ubase, nx, nz, K, gr, W / gr, p->hlo + v)) return p.release();
+    }
+    if (std::getenv("FWI_KKT_KM_LOG")) {
+        std::fprintf(stderr, "[fwi] K1 plan %dx%d K=%d %s: cols %d, %d CTAs, stages %d, ks %d, ws %d, ", nx, nz, K,
+                     f32 ? "c64" : "c128", cols, p->G, st, p->ks, p->ws);
+        if (mb)
+            std::fprintf(stderr, "%d bands of %d-%d rows x %d columns\n", p->nbands, p->hlo, p->hlo + 1, W);
+        else {
+            std::fprintf(stderr, "largest rectangle %d nodes, shapes", p->max_area);
+            for (int q = 0; q < p->nshapes; ++q) std::fprintf(stderr, " %dx%d", p->shw[q], p->shh[q]);
+            std::fprintf(stderr, "\n");
+        }
+    }
     p->ok = true;
     return p.release();
 }
@@ -1140,10 +1292,20 @@ KktKmPlan* build_km_plan(Ctx& c, bool f32) {
 template <class A>
 bool launch_km(Ctx& c, KktKmPlan* p, const typename A::T* du, const typename A::R* ds, const typename A::T* la,
                typename A::T* odu, typename A::R* ods, typename A::T* ola, bool f32) {
+    const bool mb = p->G < p->nbands;
     CUtensorMap tdu[2], tla[2];
-    for (int v = 0; v < 2; ++v) {
-        if (!encode(&tdu[v], f32, du, c.nx, c.nz, c.K, p->gr, p->RP / p->gr, p->hlo + v + 2, p->ks)) return false;
-        if (!encode(&tla[v], f32, la, c.nx, c.nz, c.K, p->gr, p->RP / p->gr, p->hlo + v + 2, p->ks)) return false;
+    KmMaps maps;
+    if (mb) {
+        for (int v = 0; v < 2; ++v) {
+            if (!encode(&tdu[v], f32, du, c.nx, c.nz, c.K, p->gr, p->RP / p->gr, p->hlo + v + 2)) return false;
+            if (!encode(&tla[v], f32, la, c.nx, c.nz, c.K, p->gr, p->RP / p->gr, p->hlo + v + 2)) return false;
+        }
+    } else {
+        for (int q = 0; q < p->nshapes; ++q) {
+            const int pairs = (p->shw[q] + 2 * p->gr) / p->gr;
+            if (!encode(&maps.du[q], f32, du, c.nx, c.nz, c.K, p->gr, pairs, p->shh[q] + 2, p->ks)) return false;
+            if (!encode(&maps.la[q], f32, la, c.nx, c.nz, c.K, p->gr, pairs, p->shh[q] + 2, p->ks)) return false;
+        }
     }
     KmArgs<A> a;
     a.nx = c.nx;
@@ -1180,6 +1342,14 @@ bool launch_km(Ctx& c, KktKmPlan* p, const typename A::T* du, const typename A::
         a.tx[v] = p->tx[v];
         a.pb[v] = p->pb[v];
     }
+    for (int q = 0; q < kKmShapes; ++q) {
+        a.shb[q] = p->shb[q];
+        a.stx[q] = p->stx[q];
+        a.spb[q] = p->spb[q];
+        a.srp[q] = p->shw[q] + 2 * p->gr;
+    }
+    a.rects = p->rects.p;
+    a.rshape = p->rshape.p;
     a.stage_bytes = p->stage_bytes;
     a.ul = p->ul;
     // complex128 outputs bypass the L1 (st.global.L1::no_allocate): with L1-allocating streaming
@@ -1192,13 +1362,12 @@ bool launch_km(Ctx& c, KktKmPlan* p, const typename A::T* du, const typename A::
 #define FWI_KM_LAUNCH(COLSc, Sc, MBc, WSc, KSc)                                                            \
     ((MBc ? kkt_km_kernel<A, COLSc, Sc, true><<<p->G, 512, p->smem, c.stream>>>(tdu[0], tla[0], p->tm_u[0],     \
                                                                               tdu[1], tla[1], p->tm_u[1], a)  \
-          : kkt_km1_kernel<A, COLSc, Sc, WSc, KSc><<<p->G, 512, p->smem, c.stream>>>(                          \
-                tdu[0], tla[0], p->tm_u[0], tdu[1], tla[1], p->tm_u[1], a)),                                   \
+          : kkt_km1_kernel<A, COLSc, Sc, WSc, KSc><<<p->G, 512, p->smem, c.stream>>>(maps, a)),               \
      c.kkt_kernel[f32 ? 1 : 0] = MBc ? (f32 ? "kkt_km_kernel<F32, " #COLSc ", " #Sc ", bands> (source-major TMA K1, csrc/kkt_tma.cu)" \
                                            : "kkt_km_kernel<F64, " #COLSc ", " #Sc ", bands> (source-major TMA K1, csrc/kkt_tma.cu)") \
                                      : (f32 ? "kkt_km1_kernel<F32, " #COLSc ", " #Sc ", " #WSc ", " #KSc "> (source-major TMA K1, one band per CTA, csrc/kkt_tma.cu)" \
                                            : "kkt_km1_kernel<F64, " #COLSc ", " #Sc ", " #WSc ", " #KSc "> (source-major TMA K1, one band per CTA, csrc/kkt_tma.cu)"))
-    FWI_KM_DISPATCH(p->cols, p->stages, p->G < p->nbands ? 1 : 0, p->ws, p->ks, FWI_KM_LAUNCH);
+    FWI_KM_DISPATCH(p->cols, p->stages, mb ? 1 : 0, p->ws, p->ks, FWI_KM_LAUNCH);
 #undef FWI_KM_LAUNCH
     CK_LAUNCH();
     return true;

@@ -123,7 +123,7 @@ def test_kkt_apply_c2_parity():
     assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("variant", ["plain", "tma", "tma_bands", "tile"])
+@pytest.mark.parametrize("variant", ["plain", "tma", "tma_bands", "tma_balanced", "tile"])
 @pytest.mark.parametrize("mk", PROBLEMS + [lambda: c2_problem(K=5, R=17),
                                            lambda: small_problem(nx=70, nz=42, n_pml=5, K=3, R=11,
                                                                  duplicate_receiver=True, seed=7)])
@@ -135,6 +135,9 @@ def test_kkt_apply_kernel_variants_bit_exact(mk, variant, monkeypatch):
     if variant != "plain":
         monkeypatch.setenv("FWI_KKT_FORCE_TMA", "1")
         monkeypatch.setenv("FWI_KKT_KM_FORCE", "1")  # source-major kernel even for 1-row rectangles
+    if variant == "tma_balanced":  # area-balanced strips of two widths (the rectangle table)
+        monkeypatch.setenv("FWI_KKT_KERNEL", "tma")
+        monkeypatch.setenv("FWI_KKT_KM_BALANCED", "1")
     if variant == "tma_bands":  # several 3-row bands per CTA (the config-5 form)
         monkeypatch.setenv("FWI_KKT_KM_ROWS", "3")
         monkeypatch.setenv("FWI_KKT_KM_G", "2")
