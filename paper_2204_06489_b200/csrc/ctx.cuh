@@ -117,6 +117,7 @@ void kkt_km_plan_free(KktKmPlan*);
 double dev_dot(Ctx* c, cudaStream_t st, const double* x, const double* y, int64_t len);
 void dev_axpy(cudaStream_t st, double a, const double* x, double* y, int64_t len);
 void dev_scal(cudaStream_t st, double a, double* x, int64_t len);
+void dev_scal_rsqrt(cudaStream_t st, const double* h2_dev, double* x, int64_t len);  // x /= sqrt(*h2)
 // fused GMRES helpers
 void dev_mgs_step(cudaStream_t st, double* w, const double* vprev, const double* hprev_dev,
                   const double* vnext, double* h_out_dev, double* partials, unsigned* ticket,

@@ -75,6 +75,28 @@ struct GmresWork {
     std::vector<DevBuf<double>> vecs;
     DevBuf<double> hdev, ydev;
     Scratch sc;
+    // device-side Givens state of the pipelined loop (gmres_core): Hessenberg columns, rotations,
+    // g; per-iteration status slots (||b - A x_cand||^2, ||w||, |g_{j+1}|) copied to pinned memory
+    DevBuf<double> gst, stat;
+    double* hstat = nullptr;
+    cudaEvent_t ev_stat[2] = {nullptr, nullptr};
+    int gst_restart = 0;
+    ~GmresWork() {
+        if (hstat) cudaFreeHost(hstat);
+        for (auto& e : ev_stat)
+            if (e) cudaEventDestroy(e);
+    }
+    void pipeline(int restart) {
+        if (gst_restart < restart) {
+            gst.alloc(size_t(restart) * (restart + 2) + 3 * size_t(restart) + 4);
+            gst_restart = restart;
+        }
+        if (!hstat) {
+            stat.alloc(8);
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&hstat), 8 * sizeof(double), cudaHostAllocDefault));
+            for (auto& e : ev_stat) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+    }
     DevBuf<double> take(int64_t n) {
         if (n != len) {
             vecs.clear();
@@ -99,6 +121,63 @@ struct GmresWork {
 void gmres_work_free(GmresWork* w) { delete w; }
 
 namespace {
+
+// The reference's Givens step and triangular y-solve (include/fwi/krylov.hpp:190-230, S = double)
+// for column j, on the device so the iteration needs no host round trip: the same operations
+// in the same order as the host code in gmres_core, each rounded explicitly (no contraction),
+// so h, the rotations, g and y are bit-identical to it. h_dev: the MGS kernel's h_0..h_{j+1}
+// (h_{j+1} = ||w||^2). Layout of gst (restart R): H (column-major, R+2 per column), c[R], s[R],
+// g[R+2]. stat: [1] = ||w||, [2] = |g_{j+1}|; y_dev: y_0..y_j.
+__global__ void givens_kernel(const double* __restrict__ h_dev, int j, int R, double* __restrict__ gst,
+                              double* __restrict__ y_dev, double* __restrict__ stat) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double* H = gst;
+    double* gc = gst + size_t(R) * (R + 2);
+    double* gs = gc + R;
+    double* g = gs + R;
+    double* h = H + size_t(j) * (R + 2);
+    for (int i = 0; i <= j + 1; ++i) h[i] = h_dev[i];
+    const double wn = __dsqrt_rn(h[j + 1]);
+    h[j + 1] = wn;
+    for (int i = 0; i < j; ++i) {
+        const double t = __dadd_rn(__dmul_rn(gc[i], h[i]), __dmul_rn(gs[i], h[i + 1]));
+        h[i + 1] = __dadd_rn(__dmul_rn(-gs[i], h[i]), __dmul_rn(gc[i], h[i + 1]));
+        h[i] = t;
+    }
+    double c, s, rr;
+    const double an = fabs(h[j]), bn = fabs(h[j + 1]);
+    const double t = __dsqrt_rn(__dadd_rn(__dmul_rn(an, an), __dmul_rn(bn, bn)));
+    if (bn == 0.0) {
+        c = 1.0;
+        s = 0.0;
+        rr = h[j];
+    } else if (an == 0.0) {
+        c = 0.0;
+        s = __ddiv_rn(h[j + 1], bn);
+        rr = bn;
+    } else {
+        c = __ddiv_rn(an, t);
+        s = __ddiv_rn(__dmul_rn(__ddiv_rn(h[j], an), h[j + 1]), t);
+        rr = __dmul_rn(__ddiv_rn(h[j], an), t);
+    }
+    gc[j] = c;
+    gs[j] = s;
+    h[j] = rr;
+    h[j + 1] = 0.0;
+    g[j + 1] = __dmul_rn(-s, g[j]);
+    g[j] = __dmul_rn(c, g[j]);
+    for (int i = j; i >= 0; --i) {
+        double acc = g[i];
+        for (int k2 = i + 1; k2 <= j; ++k2) acc = __dsub_rn(acc, __dmul_rn(H[size_t(k2) * (R + 2) + i], y_dev[k2]));
+        y_dev[i] = __ddiv_rn(acc, H[size_t(i) * (R + 2) + i]);
+    }
+    stat[1] = wn;
+    stat[2] = fabs(g[j + 1]);
+}
+
+__global__ void givens_init_kernel(double* gst, int R, double beta) {
+    gst[size_t(R) * (R + 2) + 2 * size_t(R)] = beta;  // g_0
+}
 
 double seconds_since(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -284,7 +363,7 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
     B.dev.resize(nbasis);
     B.host.assign(nbasis, nullptr);
     double* best_host = nullptr;
-    DevBuf<double> tmp, w, xc, best;
+    DevBuf<double> tmp, w, xc, best, xc2;  // xc2: the pipelined loop's second x_cand buffer
     // buffers come from (and go back to) the context's workspace unless the basis spills to the host
     struct Giveback {
         GmresWork& ws;
@@ -425,6 +504,100 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
     DevBuf<double>& hdev = WS.hdev;
     DevBuf<double>& ydev = WS.ydev;
     std::vector<double> hh(restart + 2);
+
+    // Pipelined loop (device-resident basis, no observer): the Givens step runs on the device
+    // (givens_kernel, bit-identical to the host code below), the basis normalisation reads ||w||
+    // from the device, and iteration j + 1 is enqueued before the host waits for iteration j's
+    // residual — the device never idles on the host's convergence test. A speculative iteration
+    // past convergence writes only buffers the result does not use (x_cand alternates between two
+    // buffers) and is dropped. FWI_GMRES_SYNC=1 selects the synchronous loop below.
+    if (!host_mode && !ops.observer && restart + 1 <= 63 && !std::getenv("FWI_GMRES_SYNC")) {
+        WS.pipeline(restart);
+        grab(xc2);
+        DevBuf<double>* xcb[2] = {&xc, &xc2};
+        const std::vector<double> no_y;
+        double res_prev = 1.0, rate = 1.0;  // last true residual and reduction factor (prediction)
+        while (iter < maxit && !log.converged) {
+            // r0 = M^{-1}(b - A x)
+            ops.apply(x, w.p);
+            CK(cudaMemcpyAsync(xc.p, b, bytes, cudaMemcpyDeviceToDevice, st));
+            dev_axpy(st, -1.0, w.p, xc.p, len);
+            ops.precond(xc.p, w.p);
+            const double beta = dnorm(sc, st, w.p, len);
+            const double cycle_start_res = true_res;
+            if (beta == 0.0) break;
+            dev_scal(st, 1.0 / beta, w.p, len);
+            put_basis(0, w);
+            givens_init_kernel<<<1, 1, 0, st>>>(WS.gst.p, restart, beta);
+            CK_LAUNCH();
+            auto issue = [&](int j) {
+                double* stj = WS.stat.p + 4 * (j & 1);
+                ops.apply(B.dptr(j), w.p);
+                ops.precond(w.p, tmp.p);
+                std::swap(w, tmp);
+                std::vector<const double*> vp(j + 1);
+                for (int i = 0; i <= j; ++i) vp[i] = B.dptr(i);
+                if (!dev_mgs_all(st, w.p, vp.data(), j + 1, hdev.p, sc.partials.p, sc.ticket.p, sc.flag.p, sc.epoch,
+                                 len)) {
+                    for (int i = 0; i <= j; ++i) mgs_step_any(sc, B, w.p, i - 1, hdev.p + (i - 1), i, hdev.p + i);
+                    mgs_step_any(sc, B, w.p, j, hdev.p + j, -1, hdev.p + j + 1);
+                }
+                givens_kernel<<<1, 32, 0, st>>>(hdev.p, j, restart, WS.gst.p, ydev.p, stj);
+                CK_LAUNCH();
+                multi_axpy_any(B, xcb[j & 1]->p, x, no_y, ydev.p, j + 1);
+                ops.apply(xcb[j & 1]->p, tmp.p);
+                dev_sub_norm2(st, b, tmp.p, stj, sc.partials.p, sc.ticket.p, len);
+                CK(cudaMemcpyAsync(WS.hstat + 4 * (j & 1), stj, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+                CK(cudaEventRecord(WS.ev_stat[j & 1], st));
+            };
+            bool happy = false;
+            int jl = 0;
+            issue(0);
+            for (int j = 0;; ++j) {
+                ++iter;
+                const bool more = j + 1 < restart && iter < maxit;
+                // iteration j + 1 is enqueued before j's residual is known unless j is predicted
+                // to converge (the last residual times the last reduction factor within twice the
+                // tolerance): a speculative iteration after convergence would cost a whole
+                // iteration, the wait costs one host round trip
+                const bool ahead = more && !(res_prev * rate <= 2.0 * tol);
+                if (ahead) {  // v_{j+1} = w / ||w||, then iteration j + 1
+                    dev_scal_rsqrt(st, hdev.p + j + 1, w.p, len);
+                    put_basis(j + 1, w);
+                    issue(j + 1);
+                }
+                CK(cudaEventSynchronize(WS.ev_stat[j & 1]));
+                const double* hs = WS.hstat + 4 * (j & 1);
+                const double r2 = hs[0], wn = hs[1], prec_res = hs[2] / pbnorm;
+                true_res = std::sqrt(r2) / bnorm;
+                log.entries.push_back({iter, true_res, {}, prec_res, elapsed()});
+                if (true_res < best_res) {
+                    best_res = true_res;
+                    save_best(xcb[j & 1]->p);
+                }
+                jl = j;
+                if (res_prev > 0.0) rate = std::min(1.0, true_res / res_prev);
+                res_prev = true_res;
+                if (true_res <= tol) log.converged = true;
+                if (wn == 0.0) happy = true;
+                if (log.converged || happy || !more) break;
+                if (!ahead) {  // predicted convergence did not happen: continue synchronously
+                    dev_scal_rsqrt(st, hdev.p + j + 1, w.p, len);
+                    put_basis(j + 1, w);
+                    issue(j + 1);
+                }
+            }
+            const bool stag = !log.converged && (true_res >= cycle_start_res * (1.0 - 1e-12) || happy);
+            CK(cudaMemcpyAsync(x, xcb[jl & 1]->p, bytes, cudaMemcpyDeviceToDevice, st));
+            if (stag) {
+                log.stagnated = true;
+                load_best(x);
+                break;
+            }
+        }
+        CK(cudaStreamSynchronize(st));
+        return log;
+    }
 
     while (iter < maxit && !log.converged && !stop_requested) {
         // r0 = M^{-1}(b - A x)

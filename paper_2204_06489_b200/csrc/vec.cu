@@ -418,6 +418,24 @@ void dev_scal(cudaStream_t st, double a, double* x, int64_t len) {
     CK_LAUNCH();
 }
 
+// x *= 1 / sqrt(*h2): the basis normalisation v_{j+1} = w / ||w|| with ||w||^2 read from the
+// device (the MGS kernel's last h), rounded as the host's 1.0 / std::sqrt(h2)
+__global__ void scal_rsqrt_kernel(const double* __restrict__ h2, double2* __restrict__ x, int64_t m) {
+    const double a = __ddiv_rn(1.0, __dsqrt_rn(__ldg(h2)));
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        double2 v = x[i];
+        v.x = __dmul_rn(a, v.x);
+        v.y = __dmul_rn(a, v.y);
+        x[i] = v;
+    }
+}
+
+void dev_scal_rsqrt(cudaStream_t st, const double* h2_dev, double* x, int64_t len) {
+    scal_rsqrt_kernel<<<ew_blocks(len / 2), 256, 0, st>>>(h2_dev, reinterpret_cast<double2*>(x), len / 2);
+    CK_LAUNCH();
+}
+
 void dev_mgs_step(cudaStream_t st, double* w, const double* vprev, const double* hprev_dev,
                   const double* vnext, double* h_out_dev, double* partials, unsigned* ticket,
                   int64_t len) {
