@@ -50,6 +50,12 @@ struct BcrFactor {
     DevBuf<double2> store;  // M, P, Q, U of every level
     DevBuf<double2> t, r;   // solve scratch (grown to the widest batch)
     DevBuf<double2> part;   // split-K partial tiles of the narrow GEMMs
+    // level 0: the even blocks are the lines' tridiagonal T_{2b}; their LU with partial pivoting
+    // (LAPACK zgttrf form: dl, 1/d, du, du2 per block, row interchanges in tpiv) replaces the dense
+    // M_b products of the level-0 solve by O(nb) sweeps (M_b stays for the factorisation)
+    DevBuf<double2> tri;
+    DevBuf<unsigned char> tpiv;
+    bool tri_ok = false;
     size_t t_blocks = 0;    // sum over levels of ne
     int nrhs_cap = 0;
 };
@@ -60,6 +66,7 @@ void bcr_free(BcrFactor* f) { delete f; }
 // operand reuse), narrower ones the warp-tile kernel (every SM busy)
 constexpr int kBcrTiledBatch = 64;
 constexpr int kBcrTiledBatch2 = 64;  // the same for the two-product levels (two tiled launches)
+constexpr size_t kTriSmem = 112 * 1024;  // level-0 tridiagonal solve: shared memory per CTA (2 CTAs/SM)
 int64_t bcr_bytes(const BcrFactor* f) {
     return f ? int64_t(f->store.bytes() + f->t.bytes() + f->r.bytes() + f->part.bytes()) : 0;
 }
@@ -295,6 +302,160 @@ __global__ void l0_up_rhs(int nb, int m, int64_t blk, const double2* __restrict_
     }
 }
 
+__device__ __forceinline__ double cabs1(double2 z) { return fabs(z.x) + fabs(z.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+
+// LU with partial pivoting of every level-0 even block T_{2b} (one thread per block; LAPACK's
+// zgttrf: interchange rows i, i+1 when |dl_i| > |d_i| in the 1-norm of re/im, one extra
+// superdiagonal du2 of fill). Stores dl (multipliers), 1/d, du/d, du2/d as trf[b][4][nb].
+__global__ void l0_gttrf(bool col_lines, int nx, int nb, int ne, const double2* __restrict__ diag,
+                         const double2* __restrict__ east, const double2* __restrict__ south,
+                         double2* __restrict__ trf, unsigned char* __restrict__ piv) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= ne) return;
+    const int line = 2 * b;
+    double2* dl = trf + int64_t(b) * 4 * nb;
+    double2* dv = dl + nb;
+    double2* du = dv + nb;
+    double2* du2 = du + nb;
+    unsigned char* pv = piv + int64_t(b) * nb;
+    for (int i = 0; i < nb; ++i) {
+        dv[i] = tri(col_lines, nx, nb, line, i, i, diag, east, south);
+        du[i] = i + 1 < nb ? tri(col_lines, nx, nb, line, i, i + 1, diag, east, south) : make_double2(0.0, 0.0);
+        dl[i] = i + 1 < nb ? tri(col_lines, nx, nb, line, i + 1, i, diag, east, south) : make_double2(0.0, 0.0);
+        du2[i] = make_double2(0.0, 0.0);
+        pv[i] = 0;
+    }
+    for (int i = 0; i + 1 < nb; ++i) {
+        if (cabs1(dv[i]) >= cabs1(dl[i])) {
+            if (dv[i].x != 0.0 || dv[i].y != 0.0) {
+                const double2 f = cdiv(dl[i], dv[i]);
+                dl[i] = f;
+                dv[i + 1] = csub(dv[i + 1], cm(f, du[i]));
+            }
+        } else {
+            const double2 f = cdiv(dv[i], dl[i]);
+            dv[i] = dl[i];
+            dl[i] = f;
+            const double2 t = du[i];
+            du[i] = dv[i + 1];
+            dv[i + 1] = csub(t, cm(f, dv[i + 1]));
+            if (i + 2 < nb) {
+                du2[i] = du[i + 1];
+                du[i + 1] = make_double2(-f.x * du[i + 1].x + f.y * du[i + 1].y, -f.x * du[i + 1].y - f.y * du[i + 1].x);
+            }
+            pv[i] = 1;
+        }
+    }
+    // 1/d and the rows of U scaled by it: x_i = x_i / d_i - (du_i / d_i) x_{i+1} - (du2_i / d_i) x_{i+2}
+    for (int i = 0; i < nb; ++i) {
+        const double2 r =
+            (dv[i].x == 0.0 && dv[i].y == 0.0) ? make_double2(0.0, 0.0) : cdiv(make_double2(1.0, 0.0), dv[i]);
+        dv[i] = r;
+        du[i] = cm(du[i], r);
+        du2[i] = cm(du2[i], r);
+    }
+}
+
+// Level-0 solves with the tridiagonal factors: one CTA per (even block b, chunk of kc right-hand
+// sides). UP = false (down): T[b] = T_{2b}^{-1} W[2b]. UP = true: W[2b] = T_{2b}^{-1}(W[2b] -
+// E_{2b-1} x_{2b-1} - E_{2b} x_{2b+1}) with the odd neighbours' solutions already in W. The
+// chunk's columns are staged in shared memory (row pitch nb + 1: conflict-free per-thread
+// walks) by all threads with several loads in flight; one thread per column then runs the
+// forward and back substitution, carrying the running values in registers so the only
+// dependent chain is one complex multiply-subtract per row.
+constexpr int kTriThreads = 256;
+constexpr int kTriCols = 16;
+template <bool UP>
+__global__ void __launch_bounds__(kTriThreads, 4) l0_tri_solve(int nb, int m, int kc, int nrhs, int64_t blk,
+                                                            const double2* __restrict__ trf,
+                                                            const unsigned char* __restrict__ piv,
+                                                            const double2* __restrict__ coup,
+                                                            double2* __restrict__ W, double2* __restrict__ T) {
+    extern __shared__ double2 ts[];
+    const int b = blockIdx.x, j = 2 * b, k0 = blockIdx.y * kc;
+    const int kn = min(kc, nrhs - k0);
+    const int pitch = nb + 1;
+    double2* f = ts;            // dl, 1/d, du, du2
+    double2* xs = ts + 4 * nb;  // kn columns
+    unsigned char* ps = reinterpret_cast<unsigned char*>(xs + int64_t(kc) * pitch);
+    const double2* fb = trf + int64_t(b) * 4 * nb;
+    for (int i = threadIdx.x; i < 4 * nb; i += blockDim.x) f[i] = fb[i];
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) ps[i] = piv[int64_t(b) * nb + i];
+    const int64_t off = int64_t(k0) * nb;
+    const double2* wj = W + int64_t(j) * blk + off;
+    const double2* wl = W + int64_t(j - 1) * blk + off;
+    const double2* wr = W + int64_t(j + 1) * blk + off;
+    const double2* el = coup + int64_t(j - 1) * nb;
+    const double2* er = coup + int64_t(j) * nb;
+    const bool hl = UP && j > 0, hr = UP && j + 1 < m;
+    const int tot = kn * nb;
+    constexpr int U = UP ? 2 : 4;  // loads in flight per thread and array (64 registers)
+    for (int e0 = threadIdx.x; e0 < tot; e0 += U * kTriThreads) {
+        double2 v[U], l[U], r[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const int e = e0 + q * kTriThreads;
+            if (e < tot) {
+                v[q] = wj[e];
+                if (hl) l[q] = wl[e];
+                if (hr) r[q] = wr[e];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const int e = e0 + q * kTriThreads;
+            if (e >= tot) continue;
+            const int c = e % nb;
+            double2 x = v[q];
+            if (UP) {
+                double2 s = make_double2(0.0, 0.0);
+                if (hl) s = cm(el[c], l[q]);
+                if (hr) {
+                    const double2 w2 = cm(er[c], r[q]);
+                    s.x += w2.x;
+                    s.y += w2.y;
+                }
+                x = csub(x, s);
+            }
+            xs[(e / nb) * pitch + c] = x;
+        }
+    }
+    __syncthreads();
+    const double2 *dl = f, *di = f + nb, *ud = f + 2 * nb, *ud2 = f + 3 * nb;
+    for (int k = threadIdx.x; k < kn; k += blockDim.x) {
+        double2* x = xs + k * pitch;
+        // forward: the interchanges and L; cur = the running row i (rows < i are final)
+        double2 cur = x[0];
+#pragma unroll 4
+        for (int i = 0; i + 1 < nb; ++i) {
+            // row i's final value s (the next row when rows i, i+1 were interchanged) and the
+            // running row i+1: o - l s (branch-free: the selects sit beside the chain)
+            const double2 nxt = x[i + 1], d = dl[i];
+            const bool p = ps[i] != 0;
+            const double2 s = p ? nxt : cur, o = p ? cur : nxt;
+            x[i] = s;
+            cur = make_double2(fma(-d.x, s.x, fma(d.y, s.y, o.x)), fma(-d.x, s.y, fma(-d.y, s.x, o.y)));
+        }
+        // back: x_i = x_i / d_i - (du_i / d_i) x_{i+1} - (du2_i / d_i) x_{i+2}
+        double2 x1 = cm(cur, di[nb - 1]), x2 = make_double2(0.0, 0.0);
+        x[nb - 1] = x1;
+#pragma unroll 4
+        for (int i = nb - 2; i >= 0; --i) {
+            const double2 a = csub(cm(x[i], di[i]), cm(ud2[i], x2));  // off the x1 chain
+            const double2 u = ud[i];
+            const double2 v =
+                make_double2(fma(-u.x, x1.x, fma(u.y, x1.y, a.x)), fma(-u.x, x1.y, fma(-u.y, x1.x, a.y)));
+            x[i] = v;
+            x2 = x1;
+            x1 = v;
+        }
+    }
+    __syncthreads();
+    double2* out = UP ? W + int64_t(j) * blk + off : T + int64_t(b) * blk + off;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) out[e] = xs[(e / nb) * pitch + e % nb];
+}
+
 dim3 ew_grid(int64_t work, int batch) {
     int64_t g = (work + 255) / 256;
     if (g > 1024) g = 1024;
@@ -366,6 +527,17 @@ BcrFactor* bcr_factor(Ctx& c, bool col_lines, int nb, int L, const double2* coup
         l0_even<<<ew_grid(nn, v.ne), 256, 0, st>>>(col_lines, c.nx, nb, v.ne, c.diag.p, c.east.p, c.south.p, v.M);
         CK_LAUNCH();
         gj(v.M, v.ne, 0, 2);
+        // FWI_BCR_L0=gemm keeps the dense M_b products at level 0 (diagnostics)
+        const char* e0 = std::getenv("FWI_BCR_L0");
+        if (!(e0 && std::string(e0) == "gemm") && size_t(4 * nb) * sizeof(double2) + size_t(nb) + 8 * size_t(nb + 1) *
+                                                     sizeof(double2) <= kTriSmem) {
+            f->tri.alloc(size_t(v.ne) * 4 * nb);
+            f->tpiv.alloc(size_t(v.ne) * nb);
+            l0_gttrf<<<(v.ne + 63) / 64, 64, 0, st>>>(col_lines, c.nx, nb, v.ne, c.diag.p, c.east.p, c.south.p,
+                                                      f->tri.p, f->tpiv.p);
+            CK_LAUNCH();
+            f->tri_ok = true;
+        }
         if (v.no > 0) {
             BcrLevel& w = f->lv[1];
             l0_schur<<<ew_grid(nn, v.no), 256, 0, st>>>(col_lines, c.nx, nb, v.m, v.no, c.diag.p, c.east.p, c.south.p,
@@ -438,13 +610,33 @@ void bcr_solve(Ctx& c, BcrFactor& f, const double2* coup, double2* W, int nrhs) 
     };
     auto emit = [&](const CgemmTerm& ta, const CgemmTerm* tb, const double2* C0, int64_t sC0, double2* C, int64_t sC,
                     int batch) { cgemm2(st, nrhs, nb, nb, ta, tb, C0, nb, sC0, C, nb, sC, batch); };
+    // level-0 tridiagonal solves: column chunks of kc right-hand sides per CTA
+    auto tri_solve = [&](bool up, const BcrLevel& v, double2* Tl) {
+        const size_t fixed = size_t(4 * nb) * sizeof(double2) + size_t(nb + 15) / 16 * 16;
+        const int kc = int(std::min<size_t>(std::min(nrhs, kTriCols), (kTriSmem - fixed) / (size_t(nb + 1) * sizeof(double2))));
+        const size_t smem = fixed + size_t(kc) * (nb + 1) * sizeof(double2);
+        static bool attr = false;
+        if (!attr) {
+            CK(cudaFuncSetAttribute(l0_tri_solve<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTriSmem)));
+            CK(cudaFuncSetAttribute(l0_tri_solve<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTriSmem)));
+            attr = true;
+        }
+        const dim3 g(unsigned(v.ne), unsigned((nrhs + kc - 1) / kc));
+        if (up)
+            l0_tri_solve<true><<<g, kTriThreads, smem, st>>>(nb, v.m, kc, nrhs, blk, f.tri.p, f.tpiv.p, coup, W, Tl);
+        else
+            l0_tri_solve<false><<<g, kTriThreads, smem, st>>>(nb, v.m, kc, nrhs, blk, f.tri.p, f.tpiv.p, coup, W, Tl);
+        CK_LAUNCH();
+    };
     // down
     for (size_t l = 0; l < f.lv.size(); ++l) {
         const BcrLevel& v = f.lv[l];
         double2* Tl = T + v.t_off * blk;
         const int64_t sw = 2 * int64_t(v.step) * blk;  // W stride between same-parity blocks
-        // t_b = M_b b_{2b} (rows k of b times M^T)
-        if (tiled || (v.ne >= kBcrTiledBatch && !warp_only))
+        // t_b = M_b b_{2b} (rows k of b times M^T); level 0: the tridiagonal factors
+        if (l == 0 && f.tri_ok)
+            tri_solve(false, v, Tl);
+        else if (tiled || (v.ne >= kBcrTiledBatch && !warp_only))
             cgemm_batched(st, true, nrhs, nb, nb, 1.0, Wl(v, 0), nb, sw, v.M, nb, nn, nullptr, 0, 0, Tl, nb, blk, v.ne,
                           f.part.p, f.part.count);
         else
@@ -474,7 +666,9 @@ void bcr_solve(Ctx& c, BcrFactor& f, const double2* coup, double2* W, int nrhs) 
         const BcrLevel& v = f.lv[li];
         double2* Tl = T + v.t_off * blk;
         const int64_t sw = 2 * int64_t(v.step) * blk;
-        if (li == 0) {
+        if (li == 0 && f.tri_ok) {  // x_{2b} = T_{2b}^{-1}(b_{2b} - E x_{2b-1} - E x_{2b+1})
+            tri_solve(true, v, Tl);
+        } else if (li == 0) {
             if (v.m > 1) {
                 l0_up_rhs<<<ew_grid(blk, v.ne), 256, 0, st>>>(nb, v.m, blk, coup, W, f.r.p);
                 CK_LAUNCH();

@@ -217,10 +217,14 @@ def test_host_basis_returns_the_device_mode_solution(mode, restart, maxit):
                                 lambda: small_problem(nx=22, nz=37, n_pml=3, K=2, R=4, seed=5),
                                 lambda: small_problem(nx=31, nz=23, n_pml=4, K=9, R=7, seed=3),
                                 lambda: small_problem(nx=150, nz=130, n_pml=8, K=3, R=6)])
-def test_cyclic_reduction_matches_reference(mk, monkeypatch):
+@pytest.mark.parametrize("l0", ["tri", "gemm"])
+def test_cyclic_reduction_matches_reference(mk, l0, monkeypatch):
     """Block cyclic reduction (csrc/bcr.cu; forced with FWI_EXACT_BCR=1: odd and even line
-    counts, both orientations, nb > 112) against the reference LU (src/lu.cpp:168-209)."""
+    counts, both orientations, nb > 112) against the reference LU (src/lu.cpp:168-209); level 0
+    by the tridiagonal LU sweeps (default) and by the dense M_b products (FWI_BCR_L0=gemm)."""
     monkeypatch.setenv("FWI_EXACT_BCR", "1")
+    if l0 == "gemm":
+        monkeypatch.setenv("FWI_BCR_L0", "gemm")
     p = mk()
     ref = po.Ref(p, full=False, exact=True)
     dev = fw.GnState(p, exact=True)
