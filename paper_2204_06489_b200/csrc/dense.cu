@@ -770,6 +770,84 @@ __global__ void __launch_bounds__(128) zgemm2_warp_kernel(int M, int N, int K, G
     zgemm2_tile(M, N, K, t0, t1, nterms, C0, ldc0, sC0, C, ldc, sC, m0, n0, z, lane);
 }
 
+// The same products for narrow batches (the upper cyclic-reduction levels: a few products, so
+// a warp's walk over K — chunks of operands from DRAM/L2 one after another — is the launch's
+// latency): one CTA per 8x8 output tile, its four warps each take a quarter of K with all of
+// their operand loads issued at once, and warp 0 sums the quarters in warp order (deterministic)
+// before alpha, C0 and the store.
+__global__ void __launch_bounds__(128) zgemm2_splitk_tile_kernel(int M, int N, int K, Gemm2Term t0, Gemm2Term t1,
+                                                                int nterms, const double2* C0, int64_t ldc0,
+                                                                int64_t sC0, double2* C, int64_t ldc, int64_t sC) {
+    __shared__ double red[2][4][32][6];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int n0 = blockIdx.x * 8, m0 = blockIdx.y * 8, z = blockIdx.z;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int m = m0 + g, n = n0 + g;
+    const bool mok = m < M, nok = n < N;
+    const int kq = ((K + 15) / 16) * 4;  // a warp's quarter of K, a multiple of 4
+    const int k0 = w * kq, k1 = min(K, k0 + kq);
+    constexpr int CH = 8;                 // k4-steps per warp held in registers (K <= 128 in one pass)
+    for (int tt = 0; tt < nterms; ++tt) {
+        const Gemm2Term& T = tt == 0 ? t0 : t1;
+        double P[2] = {0.0, 0.0}, Q[2] = {0.0, 0.0}, I[2] = {0.0, 0.0};
+        if (z >= T.lo && z < T.hi) {
+            const double2* A = T.A + (z - T.lo) * T.sA;
+            const double2* B = T.B + (z - T.lo) * T.sB;
+            for (int kb = k0; kb < k1; kb += 4 * CH) {
+                double2 ra[CH], rb[CH];
+#pragma unroll
+                for (int q = 0; q < CH; ++q) {
+                    const int kk = kb + 4 * q + t4;
+                    const bool kok = kk < k1;
+                    ra[q] = (mok && kok) ? __ldg(A + int64_t(m) * T.lda + kk) : make_double2(0.0, 0.0);
+                    rb[q] = (nok && kok) ? __ldg(T.bt ? B + int64_t(n) * T.ldb + kk : B + int64_t(kk) * T.ldb + n)
+                                         : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int q = 0; q < CH; ++q) {
+                    dmma(P, ra[q].x, rb[q].x);
+                    dmma(Q, ra[q].y, rb[q].y);
+                    dmma(I, ra[q].x + ra[q].y, rb[q].x + rb[q].y);
+                }
+            }
+        }
+        double* r = red[tt][w][lane];
+        r[0] = P[0];
+        r[1] = P[1];
+        r[2] = Q[0];
+        r[3] = Q[1];
+        r[4] = I[0];
+        r[5] = I[1];
+    }
+    __syncthreads();
+    if (w != 0) return;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        double re = 0.0, im = 0.0;
+        for (int tt = 0; tt < nterms; ++tt) {
+            const Gemm2Term& T = tt == 0 ? t0 : t1;
+            if (z < T.lo || z >= T.hi) continue;
+            double P = 0.0, Q = 0.0, I = 0.0;
+            for (int q = 0; q < 4; ++q) {
+                P += red[tt][q][lane][e];
+                Q += red[tt][q][lane][2 + e];
+                I += red[tt][q][lane][4 + e];
+            }
+            re += T.alpha * (P - Q);
+            im += T.alpha * (I - P - Q);
+        }
+        const int mm = m0 + g, nn = n0 + 2 * t4 + e;
+        if (mm >= M || nn >= N) continue;
+        double2 v = make_double2(re, im);
+        if (C0) {
+            const double2 c = C0[z * sC0 + int64_t(mm) * ldc0 + nn];
+            v.x += c.x;
+            v.y += c.y;
+        }
+        C[z * sC + int64_t(mm) * ldc + nn] = v;
+    }
+}
+
 __global__ void zgemm_splitk_reduce(int M, int N, int S, double alpha, const double2* __restrict__ part,
                                     const double2* C0, int64_t ldc0, int64_t sC0, double2* C, int64_t ldc,
                                     int64_t sC) {
@@ -870,6 +948,15 @@ void cgemm2(cudaStream_t st, int M, int N, int K, const CgemmTerm& a, const Cgem
         return g;
     };
     const Gemm2Term t0 = conv(a), t1 = b ? conv(*b) : t0;
+    // narrow batches (a launch's warps fewer than ~4 per SM): the split-K tile kernel
+    // (FWI_CGEMM2_SPLIT=<batch> moves the switch point, 0 disables it)
+    static const int split_max = std::getenv("FWI_CGEMM2_SPLIT") ? std::atoi(std::getenv("FWI_CGEMM2_SPLIT")) : 8;
+    if (batch <= split_max && K <= 4 * 4 * 32) {
+        const dim3 g((N + 7) / 8, (M + 7) / 8, unsigned(batch));
+        zgemm2_splitk_tile_kernel<<<g, 128, 0, st>>>(M, N, K, t0, t1, b ? 2 : 1, C0, ldc0, sC0, C, ldc, sC);
+        CK_LAUNCH();
+        return;
+    }
     const dim3 g((N + 31) / 32, (M + 7) / 8, unsigned(batch));
     zgemm2_warp_kernel<<<g, 128, 0, st>>>(M, N, K, t0, t1, b ? 2 : 1, C0, ldc0, sC0, C, ldc, sC);
     CK_LAUNCH();

@@ -128,51 +128,77 @@ namespace {
 // so h, the rotations, g and y are bit-identical to it. h_dev: the MGS kernel's h_0..h_{j+1}
 // (h_{j+1} = ||w||^2). Layout of gst (restart R): H (column-major, R+2 per column), c[R], s[R],
 // g[R+2]. stat: [1] = ||w||, [2] = |g_{j+1}|; y_dev: y_0..y_j.
-__global__ void givens_kernel(const double* __restrict__ h_dev, int j, int R, double* __restrict__ gst,
-                              double* __restrict__ y_dev, double* __restrict__ stat) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void __launch_bounds__(32) givens_kernel(const double* __restrict__ h_dev, int j, int R,
+                                                    double* __restrict__ gst, double* __restrict__ y_dev,
+                                                    double* __restrict__ stat) {
+    // the warp stages columns 0..j of H (rows 0..j+1), the rotations and g in shared memory
+    // (one round of loads instead of a dependent global load per operation); lane 0 computes
+    extern __shared__ double gs_sm[];
+    const int P = R + 2;
+    double* Hs = gs_sm;                       // (j+1) columns of pitch P
+    double* cs = Hs + size_t(j + 1) * P;      // c[0..j], s[0..j]
+    double* ss = cs + (j + 1);
+    double* gg = ss + (j + 1);                // g[0..j+1]
+    double* ys = gg + (j + 2);                // y[0..j]
     double* H = gst;
-    double* gc = gst + size_t(R) * (R + 2);
-    double* gs = gc + R;
-    double* g = gs + R;
-    double* h = H + size_t(j) * (R + 2);
-    for (int i = 0; i <= j + 1; ++i) h[i] = h_dev[i];
-    const double wn = __dsqrt_rn(h[j + 1]);
-    h[j + 1] = wn;
-    for (int i = 0; i < j; ++i) {
-        const double t = __dadd_rn(__dmul_rn(gc[i], h[i]), __dmul_rn(gs[i], h[i + 1]));
-        h[i + 1] = __dadd_rn(__dmul_rn(-gs[i], h[i]), __dmul_rn(gc[i], h[i + 1]));
-        h[i] = t;
+    double* gc = gst + size_t(R) * P;
+    double* gsn = gc + R;
+    double* g = gsn + R;
+    const int lane = threadIdx.x;
+    for (int q = lane; q < j * P; q += 32) Hs[q] = H[q];  // columns 0..j-1
+    for (int q = lane; q <= j + 1; q += 32) Hs[size_t(j) * P + q] = h_dev[q];
+    for (int q = lane; q < j; q += 32) {
+        cs[q] = gc[q];
+        ss[q] = gsn[q];
     }
-    double c, s, rr;
-    const double an = fabs(h[j]), bn = fabs(h[j + 1]);
-    const double t = __dsqrt_rn(__dadd_rn(__dmul_rn(an, an), __dmul_rn(bn, bn)));
-    if (bn == 0.0) {
-        c = 1.0;
-        s = 0.0;
-        rr = h[j];
-    } else if (an == 0.0) {
-        c = 0.0;
-        s = __ddiv_rn(h[j + 1], bn);
-        rr = bn;
-    } else {
-        c = __ddiv_rn(an, t);
-        s = __ddiv_rn(__dmul_rn(__ddiv_rn(h[j], an), h[j + 1]), t);
-        rr = __dmul_rn(__ddiv_rn(h[j], an), t);
+    for (int q = lane; q <= j; q += 32) gg[q] = g[q];
+    __syncwarp();
+    if (lane == 0) {
+        double* h = Hs + size_t(j) * P;
+        const double wn = __dsqrt_rn(h[j + 1]);
+        h[j + 1] = wn;
+        for (int i = 0; i < j; ++i) {
+            const double t = __dadd_rn(__dmul_rn(cs[i], h[i]), __dmul_rn(ss[i], h[i + 1]));
+            h[i + 1] = __dadd_rn(__dmul_rn(-ss[i], h[i]), __dmul_rn(cs[i], h[i + 1]));
+            h[i] = t;
+        }
+        double c, s, rr;
+        const double an = fabs(h[j]), bn = fabs(h[j + 1]);
+        const double t = __dsqrt_rn(__dadd_rn(__dmul_rn(an, an), __dmul_rn(bn, bn)));
+        if (bn == 0.0) {
+            c = 1.0;
+            s = 0.0;
+            rr = h[j];
+        } else if (an == 0.0) {
+            c = 0.0;
+            s = __ddiv_rn(h[j + 1], bn);
+            rr = bn;
+        } else {
+            c = __ddiv_rn(an, t);
+            s = __ddiv_rn(__dmul_rn(__ddiv_rn(h[j], an), h[j + 1]), t);
+            rr = __dmul_rn(__ddiv_rn(h[j], an), t);
+        }
+        cs[j] = c;
+        ss[j] = s;
+        h[j] = rr;
+        h[j + 1] = 0.0;
+        gg[j + 1] = __dmul_rn(-s, gg[j]);
+        gg[j] = __dmul_rn(c, gg[j]);
+        for (int i = j; i >= 0; --i) {
+            double acc = gg[i];
+            for (int k2 = i + 1; k2 <= j; ++k2) acc = __dsub_rn(acc, __dmul_rn(Hs[size_t(k2) * P + i], ys[k2]));
+            ys[i] = __ddiv_rn(acc, Hs[size_t(i) * P + i]);
+        }
+        gc[j] = c;
+        gsn[j] = s;
+        g[j] = gg[j];
+        g[j + 1] = gg[j + 1];
+        stat[1] = wn;
+        stat[2] = fabs(gg[j + 1]);
     }
-    gc[j] = c;
-    gs[j] = s;
-    h[j] = rr;
-    h[j + 1] = 0.0;
-    g[j + 1] = __dmul_rn(-s, g[j]);
-    g[j] = __dmul_rn(c, g[j]);
-    for (int i = j; i >= 0; --i) {
-        double acc = g[i];
-        for (int k2 = i + 1; k2 <= j; ++k2) acc = __dsub_rn(acc, __dmul_rn(H[size_t(k2) * (R + 2) + i], y_dev[k2]));
-        y_dev[i] = __ddiv_rn(acc, H[size_t(i) * (R + 2) + i]);
-    }
-    stat[1] = wn;
-    stat[2] = fabs(g[j + 1]);
+    __syncwarp();
+    for (int q = lane; q <= j + 1; q += 32) H[size_t(j) * P + q] = Hs[size_t(j) * P + q];
+    for (int q = lane; q <= j; q += 32) y_dev[q] = ys[q];
 }
 
 __global__ void givens_init_kernel(double* gst, int R, double beta) {
@@ -542,7 +568,8 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
                     for (int i = 0; i <= j; ++i) mgs_step_any(sc, B, w.p, i - 1, hdev.p + (i - 1), i, hdev.p + i);
                     mgs_step_any(sc, B, w.p, j, hdev.p + j, -1, hdev.p + j + 1);
                 }
-                givens_kernel<<<1, 32, 0, st>>>(hdev.p, j, restart, WS.gst.p, ydev.p, stj);
+                const size_t gsm = (size_t(j + 1) * (restart + 2) + 4 * size_t(j) + 8) * sizeof(double);
+                givens_kernel<<<1, 32, gsm, st>>>(hdev.p, j, restart, WS.gst.p, ydev.p, stj);
                 CK_LAUNCH();
                 multi_axpy_any(B, xcb[j & 1]->p, x, no_y, ydev.p, j + 1);
                 ops.apply(xcb[j & 1]->p, tmp.p);

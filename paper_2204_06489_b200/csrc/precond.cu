@@ -23,6 +23,7 @@ __global__ void precond_ds_kernel(int K, int64_t n, double w2, double eps,
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
         double pl = 0.0;
+#pragma unroll 8
         for (int k = 0; k < K; ++k) {
             const double2 uc = u[int64_t(k) * n + i], z = la[int64_t(k) * n + i];
             const double a = __dmul_rn(uc.x, w2), b = __dmul_rn(-uc.y, w2);
