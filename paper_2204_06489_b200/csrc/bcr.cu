@@ -141,6 +141,7 @@ __global__ void l0_schur(bool col_lines, int nx, int nb, int m, int no, const do
 // strided block copy: dst[b] = src[b * sstride] (nn elements per block)
 __global__ void copy_blocks(int64_t nn, int nblk, const double2* __restrict__ src, int64_t sstride,
                             double2* __restrict__ dst, int64_t dstride) {
+    pdl_enter();
     const int b = blockIdx.y;
     if (b >= nblk) return;
     for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < nn; t += int64_t(gridDim.x) * blockDim.x)
@@ -270,6 +271,7 @@ __global__ void __launch_bounds__(512) gj_batched(int nb, double2* __restrict__ 
 // down, odd j = 2b+1: b_j -= E_{j-1} t_b + E_j t_{b+1}
 __global__ void l0_down(int nb, int m, int64_t blk, const double2* __restrict__ coup, const double2* __restrict__ T,
                         double2* __restrict__ W) {
+    pdl_enter();
     const int b = blockIdx.y, j = 2 * b + 1;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < blk; e += int64_t(gridDim.x) * blockDim.x) {
         const int c = int(e % nb);
@@ -288,6 +290,7 @@ __global__ void l0_down(int nb, int m, int64_t blk, const double2* __restrict__ 
 // up, even j = 2b: R_b = E_{j-1} x_{j-1} + E_j x_{j+1}  (then x_j = t_b - M_b R_b)
 __global__ void l0_up_rhs(int nb, int m, int64_t blk, const double2* __restrict__ coup, const double2* __restrict__ W,
                           double2* __restrict__ R) {
+    pdl_enter();
     const int b = blockIdx.y, j = 2 * b;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < blk; e += int64_t(gridDim.x) * blockDim.x) {
         const int c = int(e % nb);
@@ -372,6 +375,7 @@ __global__ void __launch_bounds__(kTriThreads, 4) l0_tri_solve(int nb, int m, in
                                                             const unsigned char* __restrict__ piv,
                                                             const double2* __restrict__ coup,
                                                             double2* __restrict__ W, double2* __restrict__ T) {
+    pdl_enter();
     extern __shared__ double2 ts[];
     const int b = blockIdx.x, j = 2 * b, k0 = blockIdx.y * kc;
     const int kn = min(kc, nrhs - k0);
@@ -550,7 +554,7 @@ BcrFactor* bcr_factor(Ctx& c, bool col_lines, int nb, int L, const double2* coup
         BcrLevel& v = f->lv[l];
         const int m = v.m;
         // M_b = D_{2b}^{-1}
-        copy_blocks<<<ew_grid(nn, v.ne), 256, 0, st>>>(nn, v.ne, D.p, 2 * nn, v.M, nn);
+        launch_pdl<kPdlDense>(copy_blocks, dim3(ew_grid(nn, v.ne)), dim3(256), 0, st, nn, v.ne, D.p, 2 * nn, v.M, nn);
         CK_LAUNCH();
         gj(v.M, v.ne, v.line0, 2 * v.step);
         // P_b = M_b U_{2b-1}^T (b >= 1), Q_b = M_b U_{2b} (2b < m-1)
@@ -566,7 +570,7 @@ BcrFactor* bcr_factor(Ctx& c, bool col_lines, int nb, int L, const double2* coup
         transpose_blocks<<<dim3((nb + 31) / 32, (nb + 31) / 32, unsigned(m - 1)), dim3(32, 8), 0, st>>>(nb, v.U, S1.p);
         CK_LAUNCH();
         // (the odd D blocks move to S2 first: D is rewritten as the next level's D)
-        copy_blocks<<<ew_grid(nn, v.no), 256, 0, st>>>(nn, v.no, D.p + nn, 2 * nn, S2.p, nn);
+        launch_pdl<kPdlDense>(copy_blocks, dim3(ew_grid(nn, v.no)), dim3(256), 0, st, nn, v.no, D.p + nn, 2 * nn, S2.p, nn);
         CK_LAUNCH();
         cgemm_batched(st, false, nb, nb, nb, -1.0, S1.p, nb, 2 * nn, v.Q, nb, nn, S2.p, nb, nn, D.p, nb, nn, v.no);
         const int np = std::min(v.no, v.ne - 1);  // b with 2b+2 < m
@@ -623,9 +627,9 @@ void bcr_solve(Ctx& c, BcrFactor& f, const double2* coup, double2* W, int nrhs) 
         }
         const dim3 g(unsigned(v.ne), unsigned((nrhs + kc - 1) / kc));
         if (up)
-            l0_tri_solve<true><<<g, kTriThreads, smem, st>>>(nb, v.m, kc, nrhs, blk, f.tri.p, f.tpiv.p, coup, W, Tl);
+            launch_pdl<kPdlDense>(l0_tri_solve<true>, dim3(g), dim3(kTriThreads), smem, st, nb, v.m, kc, nrhs, blk, f.tri.p, f.tpiv.p, coup, W, Tl);
         else
-            l0_tri_solve<false><<<g, kTriThreads, smem, st>>>(nb, v.m, kc, nrhs, blk, f.tri.p, f.tpiv.p, coup, W, Tl);
+            launch_pdl<kPdlDense>(l0_tri_solve<false>, dim3(g), dim3(kTriThreads), smem, st, nb, v.m, kc, nrhs, blk, f.tri.p, f.tpiv.p, coup, W, Tl);
         CK_LAUNCH();
     };
     // down
@@ -643,7 +647,7 @@ void bcr_solve(Ctx& c, BcrFactor& f, const double2* coup, double2* W, int nrhs) 
             emit(term(Wl(v, 0), sw, v.M, nn, 1.0, true, 0, v.ne, nb), nullptr, nullptr, 0, Tl, blk, v.ne);
         if (v.no == 0) break;
         if (l == 0) {
-            l0_down<<<ew_grid(blk, v.no), 256, 0, st>>>(nb, v.m, blk, coup, Tl, W);
+            launch_pdl<kPdlDense>(l0_down, dim3(ew_grid(blk, v.no)), dim3(256), 0, st, nb, v.m, blk, coup, Tl, W);
             CK_LAUNCH();
         } else {
             // b_{2b+1} -= U_{2b}^T t_b (rows: t_b U_{2b}) + U_{2b+1} t_{b+1} (rows: t_{b+1} U_{2b+1}^T)
@@ -670,7 +674,7 @@ void bcr_solve(Ctx& c, BcrFactor& f, const double2* coup, double2* W, int nrhs) 
             tri_solve(true, v, Tl);
         } else if (li == 0) {
             if (v.m > 1) {
-                l0_up_rhs<<<ew_grid(blk, v.ne), 256, 0, st>>>(nb, v.m, blk, coup, W, f.r.p);
+                launch_pdl<kPdlDense>(l0_up_rhs, dim3(ew_grid(blk, v.ne)), dim3(256), 0, st, nb, v.m, blk, coup, W, f.r.p);
                 CK_LAUNCH();
             } else {
                 CK(cudaMemsetAsync(f.r.p, 0, size_t(blk) * sizeof(double2), st));
@@ -686,7 +690,7 @@ void bcr_solve(Ctx& c, BcrFactor& f, const double2* coup, double2* W, int nrhs) 
             // x_{2b} = t_b - x_{2b-1} P_b^T (b >= 1) - x_{2b+1} Q_b^T (2b+1 < m)
             const int nq = v.m / 2;
             if (v.ne >= kBcrTiledBatch2 && !warp_only) {  // copy t, then both products in place
-                copy_blocks<<<ew_grid(blk, v.ne), 256, 0, st>>>(blk, v.ne, Tl, blk, Wl(v, 0), sw);
+                launch_pdl<kPdlDense>(copy_blocks, dim3(ew_grid(blk, v.ne)), dim3(256), 0, st, blk, v.ne, Tl, blk, Wl(v, 0), sw);
                 CK_LAUNCH();
                 if (v.ne > 1)
                     cgemm_batched(st, true, nrhs, nb, nb, -1.0, Wl(v, 1), nb, sw, v.P + nn, nb, nn, Wl(v, 2), nb, sw,

@@ -49,6 +49,38 @@ inline void require(bool ok, const std::string& msg) {
 }
 
 // ---------------------------------------------------------------------------
+// programmatic dependent launch (the Krylov iteration's chain of short kernels)
+// ---------------------------------------------------------------------------
+// A kernel launched with launch_pdl may be scheduled while the previous kernel in the stream
+// is still draining; pdl_enter() lets the next kernel be scheduled likewise and then waits
+// until the previous grid has completed and its memory is visible (griddepcontrol.wait), so
+// the kernel's own reads and writes are ordered exactly as in a plain stream launch. In a
+// kernel launched without the attribute both instructions are no-ops. FWI_PDL=0 disables it.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+// kernel groups (FWI_PDL_OFF=<mask> turns PDL off per group: 1 Krylov vector passes, 2 exact
+// line solver, 4 cyclic reduction and dense GEMMs, 8 KKT apply, 16 preconditioner glue, 32 the fused
+// MGS sweep)
+enum { kPdlVec = 1, kPdlExact = 2, kPdlDense = 4, kPdlKkt = 8, kPdlPrecond = 16, kPdlMgs = 32 };
+bool pdl_enabled(int group = 0);
+template <int G, typename... KA, typename... A>
+void launch_pdl(void (*k)(KA...), dim3 g, dim3 b, size_t smem, cudaStream_t st, A... args) {
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled(G) ? 1 : 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k, static_cast<KA>(args)...));
+}
+
+// ---------------------------------------------------------------------------
 // device buffers
 // ---------------------------------------------------------------------------
 template <class T>

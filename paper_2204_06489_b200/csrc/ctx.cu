@@ -306,4 +306,12 @@ void stencil_to_host(const Ctx& c, double* diag, double* east, double* south) {
     if (south) CK(cudaMemcpy(south, c.south.p, b, cudaMemcpyDeviceToHost));
 }
 
+bool pdl_enabled(int group) {
+    static const bool on = !(std::getenv("FWI_PDL") && std::atoi(std::getenv("FWI_PDL")) == 0);
+    // the fused MGS sweep (software grid barrier) runs slower as a dependent launch at config 3
+    // (2.05 against 2.45 ms per GMRES iteration with it), so it is off by default
+    static const int off = std::getenv("FWI_PDL_OFF") ? std::atoi(std::getenv("FWI_PDL_OFF")) : kPdlMgs;
+    return on && !(group & off);
+}
+
 }  // namespace fwi_b200

@@ -463,6 +463,7 @@ __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, do
                                                          const double2* __restrict__ B, int64_t ldb,
                                                          const double2* C0, int64_t ldc0, double2* C, int64_t ldc,
                                                          GemmStrides bs) {
+    pdl_enter();
     extern __shared__ __align__(16) double2 psm[];
     A += blockIdx.z * bs.a;
     B += blockIdx.z * bs.b;
@@ -582,7 +583,7 @@ void zgemm_pipe_launch(cudaStream_t st, int M, int N, int K, double alpha, const
         CK(cudaFuncSetAttribute(zgemm_pipe_kernel<BM, BT, G3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
     }
-    zgemm_pipe_kernel<BM, BT, G3><<<dim3((N + kPBN - 1) / kPBN, (M + BM - 1) / BM, batch), 256, smem, st>>>(
+    launch_pdl<kPdlDense>(zgemm_pipe_kernel<BM, BT, G3>, dim3(dim3((N + kPBN - 1) / kPBN, (M + BM - 1) / BM, batch)), dim3(256), smem, st, 
         M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs);
     CK_LAUNCH();
 }
@@ -655,6 +656,7 @@ __global__ void __launch_bounds__(128) zgemm_splitk_kernel(int M, int N, int K, 
                                                           const double2* __restrict__ A, int64_t lda, int64_t sA,
                                                           const double2* __restrict__ B, int64_t ldb, int64_t sB,
                                                           double2* __restrict__ part) {
+    pdl_enter();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int n0 = (blockIdx.x * 4 + w) * 8, m0 = blockIdx.y * 8;
     const int z = blockIdx.z / S, s = blockIdx.z % S;
@@ -764,6 +766,7 @@ __device__ __forceinline__ void zgemm2_tile(int M, int N, int K, const Gemm2Term
 __global__ void __launch_bounds__(128) zgemm2_warp_kernel(int M, int N, int K, Gemm2Term t0, Gemm2Term t1,
                                                          int nterms, const double2* C0, int64_t ldc0, int64_t sC0,
                                                          double2* C, int64_t ldc, int64_t sC) {
+    pdl_enter();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int n0 = (blockIdx.x * 4 + w) * 8, m0 = blockIdx.y * 8, z = blockIdx.z;
     if (n0 >= N) return;
@@ -778,6 +781,7 @@ __global__ void __launch_bounds__(128) zgemm2_warp_kernel(int M, int N, int K, G
 __global__ void __launch_bounds__(128) zgemm2_splitk_tile_kernel(int M, int N, int K, Gemm2Term t0, Gemm2Term t1,
                                                                 int nterms, const double2* C0, int64_t ldc0,
                                                                 int64_t sC0, double2* C, int64_t ldc, int64_t sC) {
+    pdl_enter();
     __shared__ double red[2][4][32][6];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int n0 = blockIdx.x * 8, m0 = blockIdx.y * 8, z = blockIdx.z;
@@ -851,6 +855,7 @@ __global__ void __launch_bounds__(128) zgemm2_splitk_tile_kernel(int M, int N, i
 __global__ void zgemm_splitk_reduce(int M, int N, int S, double alpha, const double2* __restrict__ part,
                                     const double2* C0, int64_t ldc0, int64_t sC0, double2* C, int64_t ldc,
                                     int64_t sC) {
+    pdl_enter();
     const int z = blockIdx.y;
     const int64_t mn = int64_t(M) * N;
     for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < mn; t += int64_t(gridDim.x) * blockDim.x) {
@@ -890,13 +895,12 @@ void cgemm_batched(cudaStream_t st, bool bt, int M, int N, int K, double alpha, 
         if (need <= scratch_count && int64_t(batch) * S <= 65535) {
             const dim3 g((N + 31) / 32, (M + 7) / 8, unsigned(batch * S));
             if (bt)
-                zgemm_splitk_kernel<true><<<g, 128, 0, st>>>(M, N, K, kc, S, A, lda, sA, B, ldb, sB, scratch);
+                launch_pdl<kPdlDense>(zgemm_splitk_kernel<true>, dim3(g), dim3(128), 0, st, M, N, K, kc, S, A, lda, sA, B, ldb, sB, scratch);
             else
-                zgemm_splitk_kernel<false><<<g, 128, 0, st>>>(M, N, K, kc, S, A, lda, sA, B, ldb, sB, scratch);
+                launch_pdl<kPdlDense>(zgemm_splitk_kernel<false>, dim3(g), dim3(128), 0, st, M, N, K, kc, S, A, lda, sA, B, ldb, sB, scratch);
             CK_LAUNCH();
             const int64_t mn = int64_t(M) * N;
-            zgemm_splitk_reduce<<<dim3(unsigned(std::min<int64_t>((mn + 255) / 256, 64)), unsigned(batch)), 256, 0,
-                                  st>>>(M, N, S, alpha, scratch, C0, ldc0, sC0, C, ldc, sC);
+            launch_pdl<kPdlDense>(zgemm_splitk_reduce, dim3(dim3(unsigned(std::min<int64_t>((mn + 255) / 256, 64)), unsigned(batch))), dim3(256), 0, st, M, N, S, alpha, scratch, C0, ldc0, sC0, C, ldc, sC);
             CK_LAUNCH();
             return;
         }
@@ -953,12 +957,12 @@ void cgemm2(cudaStream_t st, int M, int N, int K, const CgemmTerm& a, const Cgem
     static const int split_max = std::getenv("FWI_CGEMM2_SPLIT") ? std::atoi(std::getenv("FWI_CGEMM2_SPLIT")) : 8;
     if (batch <= split_max && K <= 4 * 4 * 32) {
         const dim3 g((N + 7) / 8, (M + 7) / 8, unsigned(batch));
-        zgemm2_splitk_tile_kernel<<<g, 128, 0, st>>>(M, N, K, t0, t1, b ? 2 : 1, C0, ldc0, sC0, C, ldc, sC);
+        launch_pdl<kPdlDense>(zgemm2_splitk_tile_kernel, dim3(g), dim3(128), 0, st, M, N, K, t0, t1, b ? 2 : 1, C0, ldc0, sC0, C, ldc, sC);
         CK_LAUNCH();
         return;
     }
     const dim3 g((N + 31) / 32, (M + 7) / 8, unsigned(batch));
-    zgemm2_warp_kernel<<<g, 128, 0, st>>>(M, N, K, t0, t1, b ? 2 : 1, C0, ldc0, sC0, C, ldc, sC);
+    launch_pdl<kPdlDense>(zgemm2_warp_kernel, dim3(g), dim3(128), 0, st, M, N, K, t0, t1, b ? 2 : 1, C0, ldc0, sC0, C, ldc, sC);
     CK_LAUNCH();
 }
 

@@ -261,6 +261,7 @@ __global__ void __launch_bounds__(512) line_factor_kernel(
 // coalesced for column lines; row lines are a plain strided copy.
 __global__ void gather_lines(bool col_lines, int nx, int nz, int L, int nb, int nrhs, bool conj,
                              const double2* __restrict__ src, double2* __restrict__ W) {
+    pdl_enter();
     __shared__ double2 tile[32][33];
     const int k = blockIdx.z;
     const int64_t n = int64_t(nx) * nz;
@@ -294,6 +295,7 @@ __global__ void gather_lines(bool col_lines, int nx, int nz, int L, int nb, int 
 
 __global__ void scatter_lines(bool col_lines, int nx, int nz, int L, int nb, int nrhs, bool conj,
                               const double2* __restrict__ W, double2* __restrict__ dst) {
+    pdl_enter();
     __shared__ double2 tile[32][33];
     const int k = blockIdx.z;
     const int64_t n = int64_t(nx) * nz;
@@ -732,6 +734,7 @@ __device__ __forceinline__ void cmac(double2& c, const double2 g, const double2 
 
 template <int CS, int KG, int KR, bool TRACE, bool EVEN>
 __global__ void __launch_bounds__((KG / KR + 1) * 32) sweep_warp_kernel(const WSweepArgs a) {
+    pdl_enter();
     constexpr int NW = KG / KR;  // consumer warps
     extern __shared__ __align__(128) unsigned char wsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -948,6 +951,7 @@ __global__ void __launch_bounds__((KG / KR + 1) * 32) sweep_warp_kernel(const WS
 __global__ void middle_rhs(int nb, int64_t blk, const double2* __restrict__ b, const double2* __restrict__ eA,
                            const double2* __restrict__ yA, const double2* __restrict__ eB,
                            const double2* __restrict__ yB, double2* __restrict__ T) {
+    pdl_enter();
     const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (t >= blk) return;
     const int m = int(t % nb);
@@ -963,6 +967,7 @@ __global__ void middle_rhs(int nb, int64_t blk, const double2* __restrict__ b, c
 template <int KMAX>
 __global__ void __launch_bounds__(256) middle_gemv(int nb, int nrhs, const double2* __restrict__ G, int gp,
                                                    const double2* __restrict__ T, double2* __restrict__ X) {
+    pdl_enter();
     const int lane = threadIdx.x & 31;
     const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (r >= nb) return;
@@ -1083,13 +1088,15 @@ bool warp_launch(const WarpPlan& p, int nrhs, cudaStream_t st) {
     cfg.blockDim = dim3((KG / KR + 1) * 32);
     cfg.dynamicSmemBytes = p.smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // pdl_enter() in the kernel
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     CK(cudaLaunchKernelEx(&cfg, sweep_warp_kernel<CS, KG, KR, TRACE, EVEN>, args));
     return true;
 }
@@ -1523,7 +1530,7 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
     dim3 tb(32, 8);
     dim3 tg = f.col_lines ? dim3((f.L + 31) / 32, (f.nb + 31) / 32, nrhs)
                           : dim3((f.nb + 31) / 32, (f.L + 31) / 32, nrhs);
-    gather_lines<<<tg, tb, 0, c.stream>>>(f.col_lines, c.nx, c.nz, f.L, f.nb, nrhs, adjoint, b, W);
+    launch_pdl<kPdlExact>(gather_lines, dim3(tg), dim3(tb), 0, c.stream, f.col_lines, c.nx, c.nz, f.L, f.nb, nrhs, adjoint, b, W);
     CK_LAUNCH();
     bool done = false;
     if (f.bcr) {
@@ -1599,13 +1606,13 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
                     ExactFactor& fm = const_cast<ExactFactor&>(f);
                     if (fm.tbuf.count < size_t(nrhs) * f.nb) fm.tbuf.alloc(size_t(nrhs) * f.nb);
                     const int64_t blk = int64_t(nrhs) * f.nb;
-                    middle_rhs<<<int((blk + 255) / 256), 256, 0, c.stream>>>(
+                    launch_pdl<kPdlExact>(middle_rhs, dim3(int((blk + 255) / 256)), dim3(256), 0, c.stream, 
                         f.nb, blk, W + m * blk, f.coup.p + int64_t(m - 1) * f.nb, f.ybuf.p + (m - 1) * blk,
                         f.coup.p + int64_t(m) * f.nb, f.ybuf.p + (m + 1) * blk, fm.tbuf.p);
                     CK_LAUNCH();
                     const double2* Gm = f.G.p + int64_t(m) * f.nb * f.gp;
                     if (nrhs <= 8) {
-                        middle_gemv<8><<<(f.nb + 7) / 8, 256, 0, c.stream>>>(f.nb, nrhs, Gm, f.gp, fm.tbuf.p,
+                        launch_pdl<kPdlExact>(middle_gemv<8>, dim3((f.nb + 7) / 8), dim3(256), 0, c.stream, f.nb, nrhs, Gm, f.gp, fm.tbuf.p,
                                                                              W + m * blk);
                         CK_LAUNCH();
                     } else {
@@ -1656,7 +1663,7 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
             f.L, f.nb, nrhs, f.G.p, f.gp, f.coup.p, W);
         CK_LAUNCH();
     }
-    scatter_lines<<<tg, tb, 0, c.stream>>>(f.col_lines, c.nx, c.nz, f.L, f.nb, nrhs, adjoint, W, x);
+    launch_pdl<kPdlExact>(scatter_lines, dim3(tg), dim3(tb), 0, c.stream, f.col_lines, c.nx, c.nz, f.L, f.nb, nrhs, adjoint, W, x);
     CK_LAUNCH();
     c.solve_count[FWI_PRECOND_EXACT] += nrhs;
 }

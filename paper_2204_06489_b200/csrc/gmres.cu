@@ -131,6 +131,7 @@ namespace {
 __global__ void __launch_bounds__(32) givens_kernel(const double* __restrict__ h_dev, int j, int R,
                                                     double* __restrict__ gst, double* __restrict__ y_dev,
                                                     double* __restrict__ stat) {
+    pdl_enter();
     // the warp stages columns 0..j of H (rows 0..j+1), the rotations and g in shared memory
     // (one round of loads instead of a dependent global load per operation); lane 0 computes
     extern __shared__ double gs_sm[];
@@ -569,7 +570,7 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
                     mgs_step_any(sc, B, w.p, j, hdev.p + j, -1, hdev.p + j + 1);
                 }
                 const size_t gsm = (size_t(j + 1) * (restart + 2) + 4 * size_t(j) + 8) * sizeof(double);
-                givens_kernel<<<1, 32, gsm, st>>>(hdev.p, j, restart, WS.gst.p, ydev.p, stj);
+                launch_pdl<kPdlVec>(givens_kernel, dim3(1), dim3(32), gsm, st, hdev.p, j, restart, WS.gst.p, ydev.p, stj);
                 CK_LAUNCH();
                 multi_axpy_any(B, xcb[j & 1]->p, x, no_y, ydev.p, j + 1);
                 ops.apply(xcb[j & 1]->p, tmp.p);

@@ -20,6 +20,7 @@ namespace {
 __global__ void precond_ds_kernel(int K, int64_t n, double w2, double eps,
                                   const double2* __restrict__ u, const double2* __restrict__ la,
                                   const double* __restrict__ vds, double* __restrict__ ods) {
+    pdl_enter();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
         double pl = 0.0;
@@ -37,6 +38,7 @@ __global__ void precond_ds_kernel(int K, int64_t n, double w2, double eps,
 __global__ void precond_rhs_kernel(int64_t kn, int64_t n, double w2, const double2* __restrict__ u,
                                    const double* __restrict__ ds, const double2* __restrict__ vla,
                                    double2* __restrict__ rhs) {
+    pdl_enter();
     for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < kn;
          t += int64_t(gridDim.x) * blockDim.x) {
         const double2 uc = u[t];
@@ -115,13 +117,13 @@ void precond_apply_raw(Ctx& c, int mode, const double* v, double* out) {
     // (1)
     block_solve(c, mode, true, c.du_of(vv), c.la_of(out), K);
     // (2)
-    precond_ds_kernel<<<ew(n), 256, 0, c.stream>>>(K, n, c.w2, c.eps, c.u.p, c.la_of(out), c.ds_of(vv),
+    launch_pdl<kPdlPrecond>(precond_ds_kernel, dim3(ew(n)), dim3(256), 0, c.stream, K, n, c.w2, c.eps, c.u.p, c.la_of(out), c.ds_of(vv),
                                                   c.ds_of(out));
     CK_LAUNCH();
     // (3)
     // the right-hand side is built in out.du and solved in place (both block solvers
     // read their whole input before writing)
-    precond_rhs_kernel<<<ew(kn), 256, 0, c.stream>>>(kn, n, c.w2, c.u.p, c.ds_of(out), c.la_of(vv),
+    launch_pdl<kPdlPrecond>(precond_rhs_kernel, dim3(ew(kn)), dim3(256), 0, c.stream, kn, n, c.w2, c.u.p, c.ds_of(out), c.la_of(vv),
                                                     c.du_of(out));
     CK_LAUNCH();
     block_solve(c, mode, false, c.du_of(out), c.du_of(out), K);

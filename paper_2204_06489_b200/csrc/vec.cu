@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(kRedThreads) dot_kernel(const double2* __restr
                                                           const double2* __restrict__ y, int64_t m,
                                                           double* partials, unsigned* ticket,
                                                           double* out) {
+    pdl_enter();
     __shared__ double sh[32];
     double acc = 0.0;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(kRedThreads) dot_kernel(const double2* __restr
 }
 
 __global__ void axpy_kernel(double a, const double2* __restrict__ x, double2* __restrict__ y, int64_t m) {
+    pdl_enter();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
          i += int64_t(gridDim.x) * blockDim.x) {
         const double2 xv = x[i];
@@ -100,6 +102,7 @@ __global__ void axpy_kernel(double a, const double2* __restrict__ x, double2* __
 }
 
 __global__ void scal_kernel(double a, double2* __restrict__ x, int64_t m) {
+    pdl_enter();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
          i += int64_t(gridDim.x) * blockDim.x) {
         double2 v = x[i];
@@ -207,6 +210,7 @@ __global__ void __launch_bounds__(kRedThreads) mgs_kernel(double2* __restrict__ 
                                                           const double2* __restrict__ vnext, int64_t m,
                                                           double* partials, unsigned* ticket,
                                                           double* out) {
+    pdl_enter();
     __shared__ double sh[32];
     const double nh = vprev ? -*hprev : 0.0;
     double acc = mgs_pass(w, vprev, nh, vnext, m, blockIdx.x * int64_t(blockDim.x) + threadIdx.x,
@@ -223,6 +227,7 @@ __global__ void __launch_bounds__(kRedThreads) mgs_partial_kernel(double2* __res
                                                                   const double* __restrict__ hprev,
                                                                   const double2* __restrict__ vnext, int64_t m,
                                                                   double* partials_out) {
+    pdl_enter();
     __shared__ double sh[32];
     const double nh = vprev ? -*hprev : 0.0;
     double acc = mgs_pass(w, vprev, nh, vnext, m, blockIdx.x * int64_t(blockDim.x) + threadIdx.x,
@@ -233,6 +238,7 @@ __global__ void __launch_bounds__(kRedThreads) mgs_partial_kernel(double2* __res
 
 __global__ void __launch_bounds__(kRedThreads) sum_ordered_kernel(const double* __restrict__ p, int count,
                                                                   double* out) {
+    pdl_enter();
     __shared__ double sh[32];
     double v = 0.0;
     for (int i = threadIdx.x; i < count; i += blockDim.x) v += p[i];
@@ -254,6 +260,7 @@ template <int QMAX>
 __global__ void __launch_bounds__(kRedThreads) mgs_all_kernel(double2* __restrict__ w, MgsAllArgs a, int m,
                                                               int64_t len2, double* partials, unsigned* ticket,
                                                               volatile unsigned* flag, unsigned epoch, double* h) {
+    pdl_enter();
     __shared__ double sh[32];
     __shared__ bool last;
     // QMAX > 0: this thread's grid-stride elements of w (at most QMAX) stay in registers
@@ -341,6 +348,7 @@ struct MultiAxpyArgs {
 __global__ void multi_axpy_kernel(double2* __restrict__ out, const double2* __restrict__ x,
                                   MultiAxpyArgs args, const double* __restrict__ y, int mvec,
                                   int64_t m) {
+    pdl_enter();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
          i += int64_t(gridDim.x) * blockDim.x) {
         double2 acc = x ? ld_na(x + i) : make_double2(0.0, 0.0);
@@ -359,6 +367,7 @@ __global__ void __launch_bounds__(kRedThreads) sub_norm2_kernel(const double2* _
                                                                 const double2* __restrict__ ax, int64_t m,
                                                                 double* partials, unsigned* ticket,
                                                                 double* out) {
+    pdl_enter();
     __shared__ double sh[32];
     double acc = 0.0;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -393,7 +402,7 @@ static int ew_blocks(int64_t m) { return grid_blocks(m, 256, 16 * sm_count()); }
 
 void dev_dot_async(cudaStream_t st, const double* x, const double* y, double* out_dev,
                    double* partials, unsigned* ticket, int64_t len) {
-    dot_kernel<<<reduce_blocks(), kRedThreads, 0, st>>>(reinterpret_cast<const double2*>(x),
+    launch_pdl<kPdlVec>(dot_kernel, dim3(reduce_blocks()), dim3(kRedThreads), 0, st, reinterpret_cast<const double2*>(x),
                                                         reinterpret_cast<const double2*>(y), len / 2,
                                                         partials, ticket, out_dev);
     CK_LAUNCH();
@@ -408,19 +417,20 @@ double dev_dot(Ctx* c, cudaStream_t st, const double* x, const double* y, int64_
 }
 
 void dev_axpy(cudaStream_t st, double a, const double* x, double* y, int64_t len) {
-    axpy_kernel<<<ew_blocks(len / 2), 256, 0, st>>>(a, reinterpret_cast<const double2*>(x),
+    launch_pdl<kPdlVec>(axpy_kernel, dim3(ew_blocks(len / 2)), dim3(256), 0, st, a, reinterpret_cast<const double2*>(x),
                                                     reinterpret_cast<double2*>(y), len / 2);
     CK_LAUNCH();
 }
 
 void dev_scal(cudaStream_t st, double a, double* x, int64_t len) {
-    scal_kernel<<<ew_blocks(len / 2), 256, 0, st>>>(a, reinterpret_cast<double2*>(x), len / 2);
+    launch_pdl<kPdlVec>(scal_kernel, dim3(ew_blocks(len / 2)), dim3(256), 0, st, a, reinterpret_cast<double2*>(x), len / 2);
     CK_LAUNCH();
 }
 
 // x *= 1 / sqrt(*h2): the basis normalisation v_{j+1} = w / ||w|| with ||w||^2 read from the
 // device (the MGS kernel's last h), rounded as the host's 1.0 / std::sqrt(h2)
 __global__ void scal_rsqrt_kernel(const double* __restrict__ h2, double2* __restrict__ x, int64_t m) {
+    pdl_enter();
     const double a = __ddiv_rn(1.0, __dsqrt_rn(__ldg(h2)));
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
          i += int64_t(gridDim.x) * blockDim.x) {
@@ -432,14 +442,14 @@ __global__ void scal_rsqrt_kernel(const double* __restrict__ h2, double2* __rest
 }
 
 void dev_scal_rsqrt(cudaStream_t st, const double* h2_dev, double* x, int64_t len) {
-    scal_rsqrt_kernel<<<ew_blocks(len / 2), 256, 0, st>>>(h2_dev, reinterpret_cast<double2*>(x), len / 2);
+    launch_pdl<kPdlVec>(scal_rsqrt_kernel, dim3(ew_blocks(len / 2)), dim3(256), 0, st, h2_dev, reinterpret_cast<double2*>(x), len / 2);
     CK_LAUNCH();
 }
 
 void dev_mgs_step(cudaStream_t st, double* w, const double* vprev, const double* hprev_dev,
                   const double* vnext, double* h_out_dev, double* partials, unsigned* ticket,
                   int64_t len) {
-    mgs_kernel<<<reduce_blocks(), kRedThreads, 0, st>>>(
+    launch_pdl<kPdlVec>(mgs_kernel, dim3(reduce_blocks()), dim3(kRedThreads), 0, st, 
         reinterpret_cast<double2*>(w), reinterpret_cast<const double2*>(vprev), hprev_dev,
         reinterpret_cast<const double2*>(vnext), len / 2, partials, ticket, h_out_dev);
     CK_LAUNCH();
@@ -447,7 +457,7 @@ void dev_mgs_step(cudaStream_t st, double* w, const double* vprev, const double*
 
 void dev_mgs_step_parts(cudaStream_t st, double* w, const double* vprev, const double* hprev_dev,
                         const double* vnext, double* partials_out, int64_t len) {
-    mgs_partial_kernel<<<reduce_blocks(), kRedThreads, 0, st>>>(
+    launch_pdl<kPdlVec>(mgs_partial_kernel, dim3(reduce_blocks()), dim3(kRedThreads), 0, st, 
         reinterpret_cast<double2*>(w), reinterpret_cast<const double2*>(vprev), hprev_dev,
         reinterpret_cast<const double2*>(vnext), len / 2, partials_out);
     CK_LAUNCH();
@@ -468,8 +478,8 @@ bool dev_mgs_all(cudaStream_t st, double* w, const double* const* v, int m, doub
     for (int i = 0; i < m; ++i) a.v[i] = reinterpret_cast<const double2*>(v[i]);
     const int64_t len2 = len / 2, per = int64_t(reduce_blocks()) * kRedThreads;
     auto go = [&](auto kern) {
-        kern<<<reduce_blocks(), kRedThreads, 0, st>>>(reinterpret_cast<double2*>(w), a, m, len2, partials, ticket, flag,
-                                                      epoch, h_dev);
+        launch_pdl<kPdlMgs>(kern, dim3(reduce_blocks()), dim3(kRedThreads), 0, st, reinterpret_cast<double2*>(w), a, m, len2,
+                   partials, ticket, flag, epoch, h_dev);
     };
     if (len2 <= 2 * per) go(mgs_all_kernel<2>);
     else if (len2 <= 4 * per) go(mgs_all_kernel<4>);
@@ -480,7 +490,7 @@ bool dev_mgs_all(cudaStream_t st, double* w, const double* const* v, int m, doub
 }
 
 void dev_sum_ordered(cudaStream_t st, const double* partials, int count, double* out_dev) {
-    sum_ordered_kernel<<<1, kRedThreads, 0, st>>>(partials, count, out_dev);
+    launch_pdl<kPdlVec>(sum_ordered_kernel, dim3(1), dim3(kRedThreads), 0, st, partials, count, out_dev);
     CK_LAUNCH();
 }
 
@@ -489,7 +499,7 @@ void dev_multi_axpy(cudaStream_t st, double* out, const double* x, const double*
     MultiAxpyArgs a{};
     require(m <= 64, "gmres: restart larger than 63 is not supported by the fused update");
     for (int i = 0; i < m; ++i) a.v[i] = reinterpret_cast<const double2*>(v[i]);
-    multi_axpy_kernel<<<ew_blocks(len / 2), 256, 0, st>>>(reinterpret_cast<double2*>(out),
+    launch_pdl<kPdlVec>(multi_axpy_kernel, dim3(ew_blocks(len / 2)), dim3(256), 0, st, reinterpret_cast<double2*>(out),
                                                           reinterpret_cast<const double2*>(x), a,
                                                           y_dev, m, len / 2);
     CK_LAUNCH();
@@ -497,7 +507,7 @@ void dev_multi_axpy(cudaStream_t st, double* out, const double* x, const double*
 
 void dev_sub_norm2(cudaStream_t st, const double* b, const double* ax, double* out_dev,
                    double* partials, unsigned* ticket, int64_t len) {
-    sub_norm2_kernel<<<reduce_blocks(), kRedThreads, 0, st>>>(
+    launch_pdl<kPdlVec>(sub_norm2_kernel, dim3(reduce_blocks()), dim3(kRedThreads), 0, st, 
         reinterpret_cast<const double2*>(b), reinterpret_cast<const double2*>(ax), len / 2, partials,
         ticket, out_dev);
     CK_LAUNCH();
