@@ -102,6 +102,8 @@ Ctx::~Ctx() {
     if (ilu) ilu_free(ilu);
     for (auto*& p : kplan)
         if (p) kkt_plan_free(p);
+    for (auto*& p : kplan_alt)
+        if (p) kkt_plan_free(p);
     for (auto*& p : kmplan)
         if (p) kkt_km_plan_free(p);
     for (auto& e : ev_in)

@@ -61,6 +61,7 @@ struct Ctx {
     int64_t solve_count[2] = {0, 0};
     double t_ilu_factor = 0.0;  // host ILU(p) factorisation time of the current factors, s
     KktPlan* kplan[2] = {nullptr, nullptr};      // tile-TMA apply plans (c128, c64), built lazily
+    KktPlan* kplan_alt[2] = {nullptr, nullptr};  // the same for applies on a second stream (GMRES)
     KktKmPlan* kmplan[2] = {nullptr, nullptr};   // source-major TMA apply plans (c128, c64), built lazily
     // 0: source-major TMA kernel (falling back to the tile-TMA kernel, then the plain kernel),
     // 1: plain kernel (FWI_KKT_KERNEL=plain), 2: tile-TMA kernel (FWI_KKT_KERNEL=tile)
@@ -108,6 +109,8 @@ void stencil_to_host(const Ctx& c, double* diag, double* east, double* south);
 void kkt_apply(Ctx& c, const Vec& xi, Vec& out);
 void kkt_rhs(Ctx& c, Vec& out);
 void kkt_apply_raw(Ctx& c, const double* xi, double* out);  // c128 flat device buffers
+// the same on stream s, concurrently with applies on c.stream (its own tile-kernel plan)
+void kkt_apply_raw_on(Ctx& c, const double* xi, double* out, cudaStream_t s);
 bool kkt_apply_tma(Ctx& c, bool f32, const void* xi, void* out);
 void kkt_apply_host(Ctx& c, const double* in, double* out);
 void kkt_plan_free(KktPlan*);

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <cmath>
 #include <functional>
+#include <memory>
 #include <future>
 #include <optional>
 
@@ -47,6 +48,9 @@ struct GmresOps {
     int64_t len = 0;
     cudaStream_t st = nullptr;
     std::function<void(const double*, double*)> apply, precond;
+    // optional: the operator on a second stream, concurrent with apply/precond on st (lets the
+    // pipelined loop run x_cand and the true residual beside the next iteration)
+    std::function<void(const double*, double*, cudaStream_t)> apply_alt;
     std::function<bool(int, const double*)> observer;  // may be empty
 };
 
@@ -81,10 +85,27 @@ struct GmresWork {
     double* hstat = nullptr;
     cudaEvent_t ev_stat[2] = {nullptr, nullptr};
     int gst_restart = 0;
+    // the residual branch's stream (x_cand, A x_cand, its norm), its reduction scratch, and the
+    // events ordering it against the main chain
+    cudaStream_t s2 = nullptr;
+    std::unique_ptr<Scratch> sc2;
+    cudaEvent_t ev_mgs[2] = {nullptr, nullptr}, ev_x = nullptr;
     ~GmresWork() {
+        if (s2) cudaStreamSynchronize(s2);
         if (hstat) cudaFreeHost(hstat);
         for (auto& e : ev_stat)
             if (e) cudaEventDestroy(e);
+        for (auto& e : ev_mgs)
+            if (e) cudaEventDestroy(e);
+        if (ev_x) cudaEventDestroy(ev_x);
+        if (s2) cudaStreamDestroy(s2);
+    }
+    void second_stream() {
+        if (s2) return;
+        CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        sc2 = std::make_unique<Scratch>();
+        for (auto& e : ev_mgs) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_x, cudaEventDisableTiming));
     }
     void pipeline(int restart) {
         if (gst_restart < restart) {
@@ -113,7 +134,7 @@ struct GmresWork {
         if (b.p && int64_t(b.count) == len) vecs.push_back(std::move(b));
     }
     void small(int restart) {
-        if (hdev.count < size_t(restart) + 2) hdev.alloc(size_t(restart) + 2);
+        if (hdev.count < 2 * (size_t(restart) + 2)) hdev.alloc(2 * (size_t(restart) + 2));  // two slots
         if (ydev.count < size_t(restart) + 1) ydev.alloc(size_t(restart) + 1);
     }
 };
@@ -390,7 +411,7 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
     B.dev.resize(nbasis);
     B.host.assign(nbasis, nullptr);
     double* best_host = nullptr;
-    DevBuf<double> tmp, w, xc, best, xc2;  // xc2: the pipelined loop's second x_cand buffer
+    DevBuf<double> tmp, w, xc, best, xc2, axb;  // pipelined loop: second x_cand, A x_cand (second stream)
     // buffers come from (and go back to) the context's workspace unless the basis spills to the host
     struct Giveback {
         GmresWork& ws;
@@ -537,12 +558,25 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
     // from the device, and iteration j + 1 is enqueued before the host waits for iteration j's
     // residual — the device never idles on the host's convergence test. A speculative iteration
     // past convergence writes only buffers the result does not use (x_cand alternates between two
-    // buffers) and is dropped. FWI_GMRES_SYNC=1 selects the synchronous loop below.
+    // buffers) and is dropped. With a second-stream operator (ops.apply_alt) iteration j's
+    // residual branch — Givens step, x_cand = x + V y, A x_cand and its norm — runs on its own
+    // stream beside iteration j + 1's operator and preconditioner (h in two slots by iteration
+    // parity). FWI_GMRES_SYNC=1 selects the synchronous loop below, FWI_GMRES_ONESTREAM=1 keeps
+    // the residual branch on the main stream.
     if (!host_mode && !ops.observer && restart + 1 <= 63 && !std::getenv("FWI_GMRES_SYNC")) {
         WS.pipeline(restart);
+        const bool two = bool(ops.apply_alt) && !std::getenv("FWI_GMRES_ONESTREAM");
+        if (two) WS.second_stream();
+        const cudaStream_t sb = two ? WS.s2 : st;  // the residual branch's stream
+        Scratch& scb = two ? *WS.sc2 : sc;
         grab(xc2);
+        if (two) grab(axb);
         DevBuf<double>* xcb[2] = {&xc, &xc2};
-        const std::vector<double> no_y;
+        const int hp = restart + 2;  // h slot pitch
+        auto hslot = [&](int j) { return hdev.p + (two ? (j & 1) * hp : 0); };
+        auto copy_best = [&](const double* src) {
+            CK(cudaMemcpyAsync(best.p, src, bytes, cudaMemcpyDeviceToDevice, sb));
+        };
         double res_prev = 1.0, rate = 1.0;  // last true residual and reduction factor (prediction)
         while (iter < maxit && !log.converged) {
             // r0 = M^{-1}(b - A x)
@@ -559,24 +593,35 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
             CK_LAUNCH();
             auto issue = [&](int j) {
                 double* stj = WS.stat.p + 4 * (j & 1);
+                double* hj = hslot(j);
                 ops.apply(B.dptr(j), w.p);
                 ops.precond(w.p, tmp.p);
                 std::swap(w, tmp);
                 std::vector<const double*> vp(j + 1);
                 for (int i = 0; i <= j; ++i) vp[i] = B.dptr(i);
-                if (!dev_mgs_all(st, w.p, vp.data(), j + 1, hdev.p, sc.partials.p, sc.ticket.p, sc.flag.p, sc.epoch,
+                // h slot j & 1 is free once iteration j - 2's residual branch has read it
+                if (two && j >= 2) CK(cudaStreamWaitEvent(st, WS.ev_stat[j & 1], 0));
+                if (!dev_mgs_all(st, w.p, vp.data(), j + 1, hj, sc.partials.p, sc.ticket.p, sc.flag.p, sc.epoch,
                                  len)) {
-                    for (int i = 0; i <= j; ++i) mgs_step_any(sc, B, w.p, i - 1, hdev.p + (i - 1), i, hdev.p + i);
-                    mgs_step_any(sc, B, w.p, j, hdev.p + j, -1, hdev.p + j + 1);
+                    for (int i = 0; i <= j; ++i) mgs_step_any(sc, B, w.p, i - 1, hj + (i - 1), i, hj + i);
+                    mgs_step_any(sc, B, w.p, j, hj + j, -1, hj + j + 1);
+                }
+                if (two) {
+                    CK(cudaEventRecord(WS.ev_mgs[j & 1], st));
+                    CK(cudaStreamWaitEvent(sb, WS.ev_mgs[j & 1], 0));
                 }
                 const size_t gsm = (size_t(j + 1) * (restart + 2) + 4 * size_t(j) + 8) * sizeof(double);
-                launch_pdl<kPdlVec>(givens_kernel, dim3(1), dim3(32), gsm, st, hdev.p, j, restart, WS.gst.p, ydev.p, stj);
+                launch_pdl<kPdlVec>(givens_kernel, dim3(1), dim3(32), gsm, sb, hj, j, restart, WS.gst.p, ydev.p, stj);
                 CK_LAUNCH();
-                multi_axpy_any(B, xcb[j & 1]->p, x, no_y, ydev.p, j + 1);
-                ops.apply(xcb[j & 1]->p, tmp.p);
-                dev_sub_norm2(st, b, tmp.p, stj, sc.partials.p, sc.ticket.p, len);
-                CK(cudaMemcpyAsync(WS.hstat + 4 * (j & 1), stj, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
-                CK(cudaEventRecord(WS.ev_stat[j & 1], st));
+                dev_multi_axpy(sb, xcb[j & 1]->p, x, vp.data(), ydev.p, j + 1, len);
+                double* ax = two ? axb.p : tmp.p;
+                if (two)
+                    ops.apply_alt(xcb[j & 1]->p, ax, sb);
+                else
+                    ops.apply(xcb[j & 1]->p, ax);
+                dev_sub_norm2(sb, b, ax, stj, scb.partials.p, scb.ticket.p, len);
+                CK(cudaMemcpyAsync(WS.hstat + 4 * (j & 1), stj, 3 * sizeof(double), cudaMemcpyDeviceToHost, sb));
+                CK(cudaEventRecord(WS.ev_stat[j & 1], sb));
             };
             bool happy = false;
             int jl = 0;
@@ -590,7 +635,7 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
                 // iteration, the wait costs one host round trip
                 const bool ahead = more && !(res_prev * rate <= 2.0 * tol);
                 if (ahead) {  // v_{j+1} = w / ||w||, then iteration j + 1
-                    dev_scal_rsqrt(st, hdev.p + j + 1, w.p, len);
+                    dev_scal_rsqrt(st, hslot(j) + j + 1, w.p, len);
                     put_basis(j + 1, w);
                     issue(j + 1);
                 }
@@ -601,7 +646,7 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
                 log.entries.push_back({iter, true_res, {}, prec_res, elapsed()});
                 if (true_res < best_res) {
                     best_res = true_res;
-                    save_best(xcb[j & 1]->p);
+                    copy_best(xcb[j & 1]->p);
                 }
                 jl = j;
                 if (res_prev > 0.0) rate = std::min(1.0, true_res / res_prev);
@@ -610,20 +655,25 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
                 if (wn == 0.0) happy = true;
                 if (log.converged || happy || !more) break;
                 if (!ahead) {  // predicted convergence did not happen: continue synchronously
-                    dev_scal_rsqrt(st, hdev.p + j + 1, w.p, len);
+                    dev_scal_rsqrt(st, hslot(j) + j + 1, w.p, len);
                     put_basis(j + 1, w);
                     issue(j + 1);
                 }
             }
             const bool stag = !log.converged && (true_res >= cycle_start_res * (1.0 - 1e-12) || happy);
-            CK(cudaMemcpyAsync(x, xcb[jl & 1]->p, bytes, cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(x, xcb[jl & 1]->p, bytes, cudaMemcpyDeviceToDevice, sb));
             if (stag) {
                 log.stagnated = true;
-                load_best(x);
-                break;
+                CK(cudaMemcpyAsync(x, best.p, bytes, cudaMemcpyDeviceToDevice, sb));
             }
+            if (two) {  // the next cycle (or the caller) reads x on the main stream
+                CK(cudaEventRecord(WS.ev_x, sb));
+                CK(cudaStreamWaitEvent(st, WS.ev_x, 0));
+            }
+            if (stag) break;
         }
         CK(cudaStreamSynchronize(st));
+        if (two) CK(cudaStreamSynchronize(sb));
         return log;
     }
 
@@ -873,6 +923,7 @@ void fsgn_gmres_step(Ctx& c, const fwi_fsgn_options& o, double* ds_host, fwi_con
     ops.len = len;
     ops.st = st;
     ops.apply = [&c](const double* in, double* out) { kkt_apply_raw(c, in, out); };
+    ops.apply_alt = [&c](const double* in, double* out, cudaStream_t s) { kkt_apply_raw_on(c, in, out, s); };
     const int mode = o.mode;
     ops.precond = [&c, mode](const double* in, double* out) { precond_apply_raw(c, mode, in, out); };
     if (o.ecg_stride > 0) {

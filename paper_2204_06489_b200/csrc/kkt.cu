@@ -146,6 +146,23 @@ void kkt_apply_raw(Ctx& c, const double* xi, double* out) {
     c.kkt_kernel[0] = "kkt_apply_kernel<F64> (plain K1, csrc/kkt.cu)";
 }
 
+void kkt_apply_raw_on(Ctx& c, const double* xi, double* out, cudaStream_t s) {
+    // the chunked tile kernel's plan holds its work counters: a concurrent apply needs its own
+    struct Swap {
+        Ctx& c;
+        cudaStream_t s0;
+        Swap(Ctx& cc, cudaStream_t s) : c(cc), s0(cc.stream) {
+            c.stream = s;
+            std::swap(c.kplan, c.kplan_alt);
+        }
+        ~Swap() {
+            std::swap(c.kplan, c.kplan_alt);
+            c.stream = s0;
+        }
+    } sw(c, s);
+    kkt_apply_raw(c, xi, out);
+}
+
 // kkt_apply on host buffers (the reference's own signature,
 // src/kkt.cpp:78): the flat input is streamed in source chunks on one copy
 // stream, each chunk is applied as soon as it lands, and its output block

@@ -1,5 +1,6 @@
 """The pipelined GMRES loop (device Givens step, iteration j + 1 enqueued before iteration j's
-residual reaches the host; csrc/gmres.cu) against the synchronous loop (host Givens, two host
+residual reaches the host, the residual branch on a second stream; csrc/gmres.cu) against the
+synchronous loop (host Givens, two host
 round trips per iteration, FWI_GMRES_SYNC=1): bit-identical residual histories, preconditioned
 residuals, flags and solutions — the Givens/y-solve arithmetic of include/fwi/krylov.hpp:190-230
 restated on the device with explicit rounding, and speculative iterations after convergence
@@ -14,11 +15,15 @@ from paper_2204_06489_b200.problem import c1_problem, small_problem
 pytestmark = pytest.mark.gpu
 
 
-def run(state, opts, sync, monkeypatch):
+def run(state, opts, sync, monkeypatch, onestream=False):
     if sync:
         monkeypatch.setenv("FWI_GMRES_SYNC", "1")
     else:
         monkeypatch.delenv("FWI_GMRES_SYNC", raising=False)
+    if onestream:
+        monkeypatch.setenv("FWI_GMRES_ONESTREAM", "1")
+    else:
+        monkeypatch.delenv("FWI_GMRES_ONESTREAM", raising=False)
     return fw.fsgn_gmres_step(state, opts)
 
 
@@ -49,6 +54,7 @@ def test_pipelined_gmres_bit_identical_to_sync(c1_state, mode, tol, maxit, resta
     b = run(c1_state, opts, True, monkeypatch)
     same(a, b)
     assert len(a[1].entries) > 1
+    same(run(c1_state, opts, False, monkeypatch, onestream=True), b)  # residual branch on the main stream
 
 
 def test_pipelined_gmres_converges_early_small(monkeypatch):
