@@ -711,12 +711,13 @@ struct KmMaps {  // TMA descriptors of the one-band kernel's box shapes (du, lam
     CUtensorMap du[kKmShapes], la[kKmShapes];
 };
 
-template <class A, int COLS, int S, int WS, int KS>
-__global__ void __launch_bounds__(512, 1)
+template <class A, int COLS, int S, int WS, int KS, int THR>
+__global__ void __launch_bounds__(THR, 1)
     kkt_km1_kernel(const __grid_constant__ KmMaps M, const KmArgs<A> P) {
     using T = typename A::T;
     using R = typename A::R;
-    constexpr int kSl = 512 / COLS;  // row slots; a thread owns rows slot and slot + kSl
+    constexpr int kSl = THR / COLS;  // row slots; a thread owns rows slot (and slot + kSl when RPT = 2)
+    constexpr int RPT = 1024 / THR;  // rows per thread: 2 with 512 threads, 1 with 1024
     extern __shared__ __align__(1024) unsigned char sm[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + size_t(S) * P.stage_bytes);
     unsigned* done = reinterpret_cast<unsigned*>(bar + S);  // WS = 2: warps finished with stage s
@@ -747,14 +748,14 @@ __global__ void __launch_bounds__(512, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int g = 0; g < S && g < steps; ++g) issue(g);
     }
-    bool act[2], hN[2], hW[2], hE[2], hS[2];
-    T cD[2], cN[2], cW[2], cE[2], cS[2];
-    R dsv[2], pl[2];
-    int qr[2], qe[2];
-    int64_t cnode[2];
+    bool act[RPT], hN[RPT], hW[RPT], hE[RPT], hS[RPT];
+    T cD[RPT], cN[RPT], cW[RPT], cE[RPT], cS[RPT];
+    R dsv[RPT], pl[RPT];
+    int qr[RPT], qe[RPT];
+    int64_t cnode[RPT];
     bool full = true;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < RPT; ++r) {
         const int row = zs + kSl * r;
         act[r] = lx < w && row < h;
         const int ix = x0 + lx, iz = z0 + row;
@@ -778,24 +779,23 @@ __global__ void __launch_bounds__(512, 1)
     }
     const bool warp_full = __all_sync(0xffffffffu, full);
     const int lxs = min(lx, w - 1);  // lanes beyond the rectangle read (and drop) its last column
-    T un[KS][2];  // u of the next step's sources, loaded one step ahead (u is read once per node)
+    T un[KS][RPT];  // u of the next step's sources, loaded one step ahead (u is read once per node)
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk)
 #pragma unroll
-        for (int r = 0; r < 2; ++r) un[kk][r] = act[r] ? ldg_na(P.u + int64_t(kk) * n + cnode[r]) : A::zero();
+        for (int r = 0; r < RPT; ++r) un[kk][r] = act[r] ? ldg_na(P.u + int64_t(kk) * n + cnode[r]) : A::zero();
     __syncthreads();
     for (int g = 0; g < steps; ++g) {
-        T ucur[KS][2];
+        T ucur[KS][RPT];
 #pragma unroll
-        for (int kk = 0; kk < KS; ++kk) {
-            ucur[kk][0] = un[kk][0];
-            ucur[kk][1] = un[kk][1];
-        }
+        for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) ucur[kk][r] = un[kk][r];
         if (g + 1 < steps)
 #pragma unroll
             for (int kk = 0; kk < KS; ++kk)
 #pragma unroll
-                for (int r = 0; r < 2; ++r)
+                for (int r = 0; r < RPT; ++r)
                     if (act[r]) un[kk][r] = ldg_na(P.u + int64_t((g + 1) * KS + kk) * n + cnode[r]);
         const int s = g % S;
         mbar_wait(&bar[s], (g / S) & 1);
@@ -806,7 +806,7 @@ __global__ void __launch_bounds__(512, 1)
             const T* dus = reinterpret_cast<const T*>(st + kk * pb) + P.gr + lxs;
             const T* las = reinterpret_cast<const T*>(st + hb + kk * pb) + P.gr + lxs;
 #pragma unroll
-            for (int r = 0; r < 2; ++r) {
+            for (int r = 0; r < RPT; ++r) {
                 const int row = zs + kSl * r;
                 if (row >= h) continue;  // CTA-uniform per slot: the rectangle's last rows
                 T s_, t_;
@@ -840,7 +840,7 @@ __global__ void __launch_bounds__(512, 1)
                 unsigned old;
                 asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
                              : "=r"(old) : "r"(smem_u32(&done[s])) : "memory");
-                if (old % 16u == 15u && g + S < steps) {
+                if (old % unsigned(THR / 32) == unsigned(THR / 32 - 1) && g + S < steps) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     issue(g + S);
                 }
@@ -851,7 +851,7 @@ __global__ void __launch_bounds__(512, 1)
         }
     }
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+    for (int r = 0; r < RPT; ++r)
         if (act[r]) P.ods[cnode[r]] = A::rsub(A::rmulr(P.eps, dsv[r]), pl[r]);
 }
 template <class A, int COLS, int S, bool MB>
@@ -1010,6 +1010,7 @@ struct KktKmPlan {
     bool ok = false;
     int cols = 128, stages = 0, G = 0, per_strip = 0, W = 0, gr = 8, RP = 0, hlo = 0, ul = 1, nbands = 0;
     int ws = 0, ks = 1;  // one-band kernel: ring discipline, sources per stage
+    int thr = 512;       // one-band kernel: threads per CTA (1024: one row per thread)
     uint32_t hb[2] = {0, 0}, ub[2] = {0, 0}, tx[2] = {0, 0}, pb[2] = {0, 0}, stage_bytes = 0;
     size_t smem = 0;
     CUtensorMap tm_u[2];
@@ -1027,26 +1028,31 @@ namespace {
 
 // instantiations: (COLS, S, MB, WS, KS); MB: several bands per CTA (kkt_km_kernel), else the
 // one-band kkt_km1_kernel with its ring discipline WS and sources per stage KS
-#define FWI_KM_KEY(COLSv, Sv, MBv, WSv, KSv) (((((COLSv) * 16 + (Sv)) * 2 + (MBv)) * 4 + (WSv)) * 4 + (KSv))
-#define FWI_KM_DISPATCH(COLSv, Sv, MBv, WSv, KSv, CALL)                              \
-    switch (FWI_KM_KEY(COLSv, Sv, MBv, WSv, KSv)) {                                  \
-        case FWI_KM_KEY(128, 2, 0, 0, 1): CALL(128, 2, false, 0, 1); break;          \
-        case FWI_KM_KEY(128, 3, 0, 0, 1): CALL(128, 3, false, 0, 1); break;          \
-        case FWI_KM_KEY(64, 3, 0, 0, 1): CALL(64, 3, false, 0, 1); break;            \
-        case FWI_KM_KEY(64, 4, 0, 0, 1): CALL(64, 4, false, 0, 1); break;            \
-        case FWI_KM_KEY(32, 2, 0, 0, 1): CALL(32, 2, false, 0, 1); break;            \
-        case FWI_KM_KEY(32, 3, 0, 0, 1): CALL(32, 3, false, 0, 1); break;            \
-        case FWI_KM_KEY(64, 2, 0, 2, 1): CALL(64, 2, false, 2, 1); break;            \
-        case FWI_KM_KEY(64, 3, 0, 2, 1): CALL(64, 3, false, 2, 1); break;            \
-        case FWI_KM_KEY(64, 4, 0, 2, 1): CALL(64, 4, false, 2, 1); break;            \
-        case FWI_KM_KEY(64, 2, 0, 0, 2): CALL(64, 2, false, 0, 2); break;            \
-        case FWI_KM_KEY(64, 3, 0, 0, 2): CALL(64, 3, false, 0, 2); break;            \
-        case FWI_KM_KEY(64, 2, 0, 2, 2): CALL(64, 2, false, 2, 2); break;            \
-        case FWI_KM_KEY(64, 3, 0, 2, 2): CALL(64, 3, false, 2, 2); break;            \
-        case FWI_KM_KEY(64, 4, 0, 2, 2): CALL(64, 4, false, 2, 2); break;            \
-        case FWI_KM_KEY(64, 2, 1, 0, 1): CALL(64, 2, true, 0, 1); break;             \
-        case FWI_KM_KEY(64, 3, 1, 0, 1): CALL(64, 3, true, 0, 1); break;             \
-        default: CALL(64, 2, false, 0, 1); break;                                    \
+#define FWI_KM_KEY(COLSv, Sv, MBv, WSv, KSv, THRv) \
+    ((((((COLSv) * 16 + (Sv)) * 2 + (MBv)) * 4 + (WSv)) * 4 + (KSv)) * 2 + ((THRv) == 1024 ? 1 : 0))
+#define FWI_KM_DISPATCH(COLSv, Sv, MBv, WSv, KSv, THRv, CALL)                             \
+    switch (FWI_KM_KEY(COLSv, Sv, MBv, WSv, KSv, THRv)) {                                 \
+        case FWI_KM_KEY(128, 2, 0, 0, 1, 512): CALL(128, 2, false, 0, 1, 512); break;     \
+        case FWI_KM_KEY(128, 3, 0, 0, 1, 512): CALL(128, 3, false, 0, 1, 512); break;     \
+        case FWI_KM_KEY(64, 3, 0, 0, 1, 512): CALL(64, 3, false, 0, 1, 512); break;       \
+        case FWI_KM_KEY(64, 4, 0, 0, 1, 512): CALL(64, 4, false, 0, 1, 512); break;       \
+        case FWI_KM_KEY(32, 2, 0, 0, 1, 512): CALL(32, 2, false, 0, 1, 512); break;       \
+        case FWI_KM_KEY(32, 3, 0, 0, 1, 512): CALL(32, 3, false, 0, 1, 512); break;       \
+        case FWI_KM_KEY(64, 2, 0, 2, 1, 512): CALL(64, 2, false, 2, 1, 512); break;       \
+        case FWI_KM_KEY(64, 3, 0, 2, 1, 512): CALL(64, 3, false, 2, 1, 512); break;       \
+        case FWI_KM_KEY(64, 4, 0, 2, 1, 512): CALL(64, 4, false, 2, 1, 512); break;       \
+        case FWI_KM_KEY(64, 2, 0, 0, 2, 512): CALL(64, 2, false, 0, 2, 512); break;       \
+        case FWI_KM_KEY(64, 3, 0, 0, 2, 512): CALL(64, 3, false, 0, 2, 512); break;       \
+        case FWI_KM_KEY(64, 2, 0, 2, 2, 512): CALL(64, 2, false, 2, 2, 512); break;       \
+        case FWI_KM_KEY(64, 3, 0, 2, 2, 512): CALL(64, 3, false, 2, 2, 512); break;       \
+        case FWI_KM_KEY(64, 4, 0, 2, 2, 512): CALL(64, 4, false, 2, 2, 512); break;       \
+        case FWI_KM_KEY(64, 2, 0, 0, 1, 1024): CALL(64, 2, false, 0, 1, 1024); break;     \
+        case FWI_KM_KEY(64, 3, 0, 0, 1, 1024): CALL(64, 3, false, 0, 1, 1024); break;     \
+        case FWI_KM_KEY(64, 2, 0, 0, 2, 1024): CALL(64, 2, false, 0, 2, 1024); break;     \
+        case FWI_KM_KEY(64, 3, 0, 0, 2, 1024): CALL(64, 3, false, 0, 2, 1024); break;     \
+        case FWI_KM_KEY(64, 2, 1, 0, 1, 512): CALL(64, 2, true, 0, 1, 512); break;        \
+        case FWI_KM_KEY(64, 3, 1, 0, 1, 512): CALL(64, 3, true, 0, 1, 512); break;        \
+        default: CALL(64, 2, false, 0, 1, 512); break;                                    \
     }
 
 // Area-balanced rectangles for the one-band kernel (FWI_KKT_KM_BALANCED=1, an experiment). Every
@@ -1179,7 +1185,11 @@ KktKmPlan* build_km_plan(Ctx& c, bool f32) {
         p->ks = f32 ? 2 : 1;
         if (const char* e = std::getenv("FWI_KKT_KM_WS")) p->ws = std::atoi(e) == 2 ? 2 : 0;
         if (const char* e = std::getenv("FWI_KKT_KM_KS")) p->ks = std::atoi(e) == 2 ? 2 : 1;
+        // 1024 threads, one row per thread (twice the warps to hide latency; the register budget
+        // halves to 64)
+        if (const char* e = std::getenv("FWI_KKT_KM_THR")) p->thr = std::atoi(e) == 1024 ? 1024 : 512;
         if (cols != 64) p->ws = 0, p->ks = 1;
+        if (p->ws != 0) p->thr = 512;
         if (K % p->ks != 0) p->ks = 1;
         // the rectangles and their box shapes
         std::vector<int4> rc;
@@ -1262,12 +1272,12 @@ KktKmPlan* build_km_plan(Ctx& c, bool f32) {
     p->smem = size_t(st) * p->stage_bytes + 128;
     if (const char* e = std::getenv("FWI_KKT_KM_PAD_KB"))  // diagnostics: unused extra shared memory
         p->smem = std::min<size_t>(227 * 1024, p->smem + size_t(std::atoi(e)) * 1024);
-#define FWI_KM_ATTR(COLSc, Sc, MBc, WSc, KSc)                                                             \
+#define FWI_KM_ATTR(COLSc, Sc, MBc, WSc, KSc, THRc)                                                       \
     CK(MBc ? cudaFuncSetAttribute(kkt_km_kernel<A, COLSc, Sc, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                   int(p->smem))                                                             \
-           : cudaFuncSetAttribute(kkt_km1_kernel<A, COLSc, Sc, WSc, KSc>,                                     \
+           : cudaFuncSetAttribute(kkt_km1_kernel<A, COLSc, Sc, WSc, KSc, THRc>,                               \
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)))
-    FWI_KM_DISPATCH(cols, st, mb ? 1 : 0, p->ws, p->ks, FWI_KM_ATTR);
+    FWI_KM_DISPATCH(cols, st, mb ? 1 : 0, p->ws, p->ks, p->thr, FWI_KM_ATTR);
 #undef FWI_KM_ATTR
     if (mb) {
         const void* ubase = f32 ? static_cast<const void*>(c.u32.p) : static_cast<const void*>(c.u.p);
@@ -1359,15 +1369,15 @@ bool launch_km(Ctx& c, KktKmPlan* p, const typename A::T* du, const typename A::
     if (const char* e = std::getenv("FWI_KKT_KM_ST")) a.stmode = std::atoi(e);
     a.u = reinterpret_cast<const typename A::T*>(f32 ? static_cast<const void*>(c.u32.p)
                                                     : static_cast<const void*>(c.u.p));
-#define FWI_KM_LAUNCH(COLSc, Sc, MBc, WSc, KSc)                                                            \
+#define FWI_KM_LAUNCH(COLSc, Sc, MBc, WSc, KSc, THRc)                                                      \
     ((MBc ? kkt_km_kernel<A, COLSc, Sc, true><<<p->G, 512, p->smem, c.stream>>>(tdu[0], tla[0], p->tm_u[0],     \
                                                                               tdu[1], tla[1], p->tm_u[1], a)  \
-          : kkt_km1_kernel<A, COLSc, Sc, WSc, KSc><<<p->G, 512, p->smem, c.stream>>>(maps, a)),               \
+          : kkt_km1_kernel<A, COLSc, Sc, WSc, KSc, THRc><<<p->G, THRc, p->smem, c.stream>>>(maps, a)),        \
      c.kkt_kernel[f32 ? 1 : 0] = MBc ? (f32 ? "kkt_km_kernel<F32, " #COLSc ", " #Sc ", bands> (source-major TMA K1, csrc/kkt_tma.cu)" \
                                            : "kkt_km_kernel<F64, " #COLSc ", " #Sc ", bands> (source-major TMA K1, csrc/kkt_tma.cu)") \
-                                     : (f32 ? "kkt_km1_kernel<F32, " #COLSc ", " #Sc ", " #WSc ", " #KSc "> (source-major TMA K1, one band per CTA, csrc/kkt_tma.cu)" \
-                                           : "kkt_km1_kernel<F64, " #COLSc ", " #Sc ", " #WSc ", " #KSc "> (source-major TMA K1, one band per CTA, csrc/kkt_tma.cu)"))
-    FWI_KM_DISPATCH(p->cols, p->stages, mb ? 1 : 0, p->ws, p->ks, FWI_KM_LAUNCH);
+                                     : (f32 ? "kkt_km1_kernel<F32, " #COLSc ", " #Sc ", " #WSc ", " #KSc ", " #THRc "> (source-major TMA K1, one band per CTA, csrc/kkt_tma.cu)" \
+                                           : "kkt_km1_kernel<F64, " #COLSc ", " #Sc ", " #WSc ", " #KSc ", " #THRc "> (source-major TMA K1, one band per CTA, csrc/kkt_tma.cu)"))
+    FWI_KM_DISPATCH(p->cols, p->stages, mb ? 1 : 0, p->ws, p->ks, p->thr, FWI_KM_LAUNCH);
 #undef FWI_KM_LAUNCH
     CK_LAUNCH();
     return true;

@@ -297,7 +297,8 @@ def test_c64_apply_deviation(variant, monkeypatch):
     assert err < 1e-5
 
 
-@pytest.mark.parametrize("env", [{"FWI_KKT_KM_KS": "swap"}, {"FWI_KKT_KM_WS": "2", "FWI_KKT_KM_STAGES": "3"},
+@pytest.mark.parametrize("env", [{"FWI_KKT_KM_KS": "swap"}, {"FWI_KKT_KM_THR": "swap"},
+                                 {"FWI_KKT_KM_WS": "2", "FWI_KKT_KM_STAGES": "3"},
                                  {"FWI_KKT_KM_WS": "2", "FWI_KKT_KM_KS": "2", "FWI_KKT_KM_STAGES": "4"}])
 @pytest.mark.parametrize("c64", [False, True])
 def test_km1_ring_variants_identical(env, c64, monkeypatch):
@@ -318,7 +319,8 @@ def test_km1_ring_variants_identical(env, c64, monkeypatch):
 
     base, kbase = run()
     for k, v in env.items():
-        monkeypatch.setenv(k, ("1" if c64 else "2") if v == "swap" else v)
+        swap = {"FWI_KKT_KM_KS": ("1", "2"), "FWI_KKT_KM_THR": ("1024", "1024")}[k] if v == "swap" else None
+        monkeypatch.setenv(k, (swap[0] if c64 else swap[1]) if swap else v)
     got, kgot = run()
     assert "kkt_km1_kernel" in kbase and "kkt_km1_kernel" in kgot and kbase != kgot, (kbase, kgot)
     assert np.array_equal(got, base)
