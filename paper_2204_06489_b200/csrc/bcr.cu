@@ -64,8 +64,13 @@ void bcr_free(BcrFactor* f) { delete f; }
 
 // one-product levels of at least this many blocks use the tiled DMMA kernel (shared-memory
 // operand reuse), narrower ones the warp-tile kernel (every SM busy)
-constexpr int kBcrTiledBatch = 64;
-constexpr int kBcrTiledBatch2 = 64;  // the same for the two-product levels (two tiled launches)
+// (FWI_BCR_TILED_MIN=<batch> moves both switch points)
+static int bcr_tiled_min() {
+    static const int v = std::getenv("FWI_BCR_TILED_MIN") ? std::atoi(std::getenv("FWI_BCR_TILED_MIN")) : 64;
+    return v;
+}
+#define kBcrTiledBatch bcr_tiled_min()
+#define kBcrTiledBatch2 bcr_tiled_min()
 constexpr size_t kTriSmem = 112 * 1024;  // level-0 tridiagonal solve: shared memory per CTA (2 CTAs/SM)
 int64_t bcr_bytes(const BcrFactor* f) {
     return f ? int64_t(f->store.bytes() + f->t.bytes() + f->r.bytes() + f->part.bytes()) : 0;

@@ -444,10 +444,10 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int BM, bool BT>
+template <int BM, bool BT, int BN = kPBN>
 constexpr int zgemm_pipe_smem() {
-    // A: [BM][kPPitchK]; B: BT ? [kPBN][kPPitchK] : [kPBK][kPPitchN]   (double2 elements)
-    return kPStages * (BM * kPPitchK + (BT ? kPBN * kPPitchK : kPBK * kPPitchN)) * 16;
+    // A: [BM][kPPitchK]; B: BT ? [BN][kPPitchK] : [kPBK][BN + 2]   (double2 elements)
+    return kPStages * (BM * kPPitchK + (BT ? BN * kPPitchK : kPBK * (BN + 2))) * 16;
 }
 
 // G3: Gauss's three-product form, S = (Ar+Ai)(Br+Bi): real = P - Q, imag = S - P - Q
@@ -457,7 +457,9 @@ struct GemmStrides {
     int64_t a = 0, b = 0, c0 = 0, c = 0;
 };
 
-template <int BM, bool BT, bool G3>
+// BN: the CTA's N tile (64, or 32 for narrow batches: twice the CTAs, so a batch of ~100
+// products spreads over the SMs more evenly); warps 2 (m) x 4 (n), warp tile (BM/2) x (BN/4)
+template <int BM, bool BT, bool G3, int BN = kPBN>
 __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, double alpha,
                                                          const double2* __restrict__ A, int64_t lda,
                                                          const double2* __restrict__ B, int64_t ldb,
@@ -469,11 +471,13 @@ __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, do
     B += blockIdx.z * bs.b;
     if (C0) C0 += blockIdx.z * bs.c0;
     C += blockIdx.z * bs.c;
-    constexpr int ASZ = BM * kPPitchK, BSZ = BT ? kPBN * kPPitchK : kPBK * kPPitchN;
-    constexpr int TM = BM / 16;  // m8 tiles per warp (warp tile (BM/2) x 16)
+    constexpr int PN = BN + 2;  // B row pitch (non-transposed)
+    constexpr int ASZ = BM * kPPitchK, BSZ = BT ? BN * kPPitchK : kPBK * PN;
+    constexpr int TM = BM / 16;  // m8 tiles per warp (warp tile (BM/2) x (BN/4))
+    constexpr int UN = BN / 32;  // n8 tiles per warp
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp & 1, wn = warp >> 1;
-    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * kPBN;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     const int g = lane >> 2, t4 = lane & 3;
     const int KT = (K + kPBK - 1) / kPBK;
 
@@ -488,21 +492,21 @@ __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, do
             cp_async16(As + mm * kPPitchK + kk, ok ? A + int64_t(m) * lda + k : A, ok);
         }
 #pragma unroll
-        for (int q = 0; q < kPBN * kPBK / 256; ++q) {
+        for (int q = 0; q < BN * kPBK / 256; ++q) {
             const int e = tid + q * 256;
             if (BT) {
                 const int kk = e % kPBK, nn = e / kPBK, n = n0 + nn, k = k0 + kk;
                 const bool ok = n < N && k < K;
                 cp_async16(Bs + nn * kPPitchK + kk, ok ? B + int64_t(n) * ldb + k : B, ok);
             } else {
-                const int nn = e % kPBN, kk = e / kPBN, n = n0 + nn, k = k0 + kk;
+                const int nn = e % BN, kk = e / BN, n = n0 + nn, k = k0 + kk;
                 const bool ok = n < N && k < K;
-                cp_async16(Bs + kk * kPPitchN + nn, ok ? B + int64_t(k) * ldb + n : B, ok);
+                cp_async16(Bs + kk * PN + nn, ok ? B + int64_t(k) * ldb + n : B, ok);
             }
         }
     };
 
-    double P[TM][2][2] = {}, Q[TM][2][2] = {}, I[TM][2][2] = {};
+    double P[TM][UN][2] = {}, Q[TM][UN][2] = {}, I[TM][UN][2] = {};
 #pragma unroll
     for (int s = 0; s < kPStages - 1; ++s) {
         if (s < KT) load_stage(s, s * kPBK);
@@ -518,8 +522,8 @@ __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, do
         }
         const double2* As = psm + (kt % kPStages) * (ASZ + BSZ);
         const double2* Bs = As + ASZ;
-        double2 fa[2][TM], fb[2][2];
-        double sa[2][TM], sb[2][2];  // G3 operand sums
+        double2 fa[2][TM], fb[2][UN];
+        double sa[2][TM], sb[2][UN];  // G3 operand sums
         auto frag = [&](int buf, int ks) {
 #pragma unroll
             for (int t = 0; t < TM; ++t) {
@@ -527,9 +531,9 @@ __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, do
                 if (G3) sa[buf][t] = fa[buf][t].x + fa[buf][t].y;
             }
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                fb[buf][u] = BT ? Bs[(wn * 16 + u * 8 + g) * kPPitchK + ks + t4]
-                                : Bs[(ks + t4) * kPPitchN + wn * 16 + u * 8 + g];
+            for (int u = 0; u < UN; ++u) {
+                fb[buf][u] = BT ? Bs[(wn * (BN / 4) + u * 8 + g) * kPPitchK + ks + t4]
+                                : Bs[(ks + t4) * PN + wn * (BN / 4) + u * 8 + g];
                 if (G3) sb[buf][u] = fb[buf][u].x + fb[buf][u].y;
             }
         };
@@ -541,7 +545,7 @@ __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, do
 #pragma unroll
             for (int t = 0; t < TM; ++t)
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < UN; ++u) {
                     dmma(P[t][u], fa[cur][t].x, fb[cur][u].x);
                     dmma(Q[t][u], fa[cur][t].y, fb[cur][u].y);
                     if (G3) {
@@ -557,10 +561,10 @@ __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, do
 #pragma unroll
     for (int t = 0; t < TM; ++t)
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
+        for (int u = 0; u < UN; ++u)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int m = m0 + wm * (BM / 2) + t * 8 + g, n = n0 + wn * 16 + u * 8 + 2 * t4 + e;
+                const int m = m0 + wm * (BM / 2) + t * 8 + g, n = n0 + wn * (BN / 4) + u * 8 + 2 * t4 + e;
                 if (m >= M || n >= N) continue;
                 const double im = G3 ? I[t][u][e] - P[t][u][e] - Q[t][u][e] : I[t][u][e];
                 double2 v = make_double2(alpha * (P[t][u][e] - Q[t][u][e]), alpha * im);
@@ -573,18 +577,19 @@ __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, do
             }
 }
 
-template <int BM, bool BT, bool G3>
+template <int BM, bool BT, bool G3, int BN = kPBN>
 void zgemm_pipe_launch(cudaStream_t st, int M, int N, int K, double alpha, const double2* A, int64_t lda,
                        const double2* B, int64_t ldb, const double2* C0, int64_t ldc0, double2* C, int64_t ldc,
                        GemmStrides bs = {}, int batch = 1) {
-    constexpr int smem = zgemm_pipe_smem<BM, BT>();
+    constexpr int smem = zgemm_pipe_smem<BM, BT, BN>();
     static bool attr = false;
     if (!attr) {
-        CK(cudaFuncSetAttribute(zgemm_pipe_kernel<BM, BT, G3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CK(cudaFuncSetAttribute(zgemm_pipe_kernel<BM, BT, G3, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem));
         attr = true;
     }
-    launch_pdl<kPdlDense>(zgemm_pipe_kernel<BM, BT, G3>, dim3(dim3((N + kPBN - 1) / kPBN, (M + BM - 1) / BM, batch)), dim3(256), smem, st, 
-        M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs);
+    launch_pdl<kPdlDense>(zgemm_pipe_kernel<BM, BT, G3, BN>, dim3((N + BN - 1) / BN, (M + BM - 1) / BM, batch),
+                          dim3(256), smem, st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs);
     CK_LAUNCH();
 }
 
@@ -913,10 +918,24 @@ void cgemm_batched(cudaStream_t st, bool bt, int M, int N, int K, double alpha, 
     // 48-row tiles for 48 rows (config 3's 48 right-hand sides: no padded rows); otherwise
     // 64-row tiles only when they still give every SM a tile (Gauss's 3-product form)
     if (M == 48) {
-        if (bt)
+        // 32-wide N tiles when 64-wide ones would leave the last wave of SMs short (a batch of
+        // ~100 products: 192 tiles on 148 SMs take two tile-times, 384 half tiles ~1.5);
+        // FWI_CGEMM_BN=32|64 forces the width
+        static const int bn_env = std::getenv("FWI_CGEMM_BN") ? std::atoi(std::getenv("FWI_CGEMM_BN")) : 0;
+        const int64_t t64 = int64_t((N + 63) / 64) * batch;
+        const int sms = sm_count();
+        const int64_t w64 = 2 * ((t64 + sms - 1) / sms), w32 = (2 * t64 + sms - 1) / sms;  // in half tiles
+        const bool narrow = bn_env ? bn_env == 32 : 5 * w32 <= 4 * w64;
+        if (narrow) {
+            if (bt)
+                zgemm_pipe_launch<48, true, true, 32>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs, batch);
+            else
+                zgemm_pipe_launch<48, false, true, 32>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs, batch);
+        } else if (bt) {
             zgemm_pipe_launch<48, true, true>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs, batch);
-        else
+        } else {
             zgemm_pipe_launch<48, false, true>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs, batch);
+        }
         return;
     }
     const int64_t tiles64 = int64_t((N + kPBN - 1) / kPBN) * ((M + 63) / 64) * batch;
