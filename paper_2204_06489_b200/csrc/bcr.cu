@@ -575,7 +575,8 @@ BcrFactor* bcr_factor(Ctx& c, bool col_lines, int nb, int L, const double2* coup
         transpose_blocks<<<dim3((nb + 31) / 32, (nb + 31) / 32, unsigned(m - 1)), dim3(32, 8), 0, st>>>(nb, v.U, S1.p);
         CK_LAUNCH();
         // (the odd D blocks move to S2 first: D is rewritten as the next level's D)
-        launch_pdl<kPdlDense>(copy_blocks, dim3(ew_grid(nn, v.no)), dim3(256), 0, st, nn, v.no, D.p + nn, 2 * nn, S2.p, nn);
+        launch_pdl<kPdlDense>(copy_blocks, dim3(ew_grid(nn, v.no)), dim3(256), 0, st, nn, v.no, D.p + nn, 2 * nn, S2.p,
+                              nn);
         CK_LAUNCH();
         cgemm_batched(st, false, nb, nb, nb, -1.0, S1.p, nb, 2 * nn, v.Q, nb, nn, S2.p, nb, nn, D.p, nb, nn, v.no);
         const int np = std::min(v.no, v.ne - 1);  // b with 2b+2 < m
@@ -622,7 +623,8 @@ void bcr_solve(Ctx& c, BcrFactor& f, const double2* coup, double2* W, int nrhs) 
     // level-0 tridiagonal solves: column chunks of kc right-hand sides per CTA
     auto tri_solve = [&](bool up, const BcrLevel& v, double2* Tl) {
         const size_t fixed = size_t(4 * nb) * sizeof(double2) + size_t(nb + 15) / 16 * 16;
-        const int kc = int(std::min<size_t>(std::min(nrhs, kTriCols), (kTriSmem - fixed) / (size_t(nb + 1) * sizeof(double2))));
+        const size_t fit = (kTriSmem - fixed) / (size_t(nb + 1) * sizeof(double2));
+        const int kc = int(std::min<size_t>(std::min(nrhs, kTriCols), fit));
         const size_t smem = fixed + size_t(kc) * (nb + 1) * sizeof(double2);
         static bool attr = false;
         if (!attr) {
@@ -632,9 +634,11 @@ void bcr_solve(Ctx& c, BcrFactor& f, const double2* coup, double2* W, int nrhs) 
         }
         const dim3 g(unsigned(v.ne), unsigned((nrhs + kc - 1) / kc));
         if (up)
-            launch_pdl<kPdlDense>(l0_tri_solve<true>, dim3(g), dim3(kTriThreads), smem, st, nb, v.m, kc, nrhs, blk, f.tri.p, f.tpiv.p, coup, W, Tl);
+            launch_pdl<kPdlDense>(l0_tri_solve<true>, dim3(g), dim3(kTriThreads), smem, st, nb, v.m, kc, nrhs, blk,
+                                  f.tri.p, f.tpiv.p, coup, W, Tl);
         else
-            launch_pdl<kPdlDense>(l0_tri_solve<false>, dim3(g), dim3(kTriThreads), smem, st, nb, v.m, kc, nrhs, blk, f.tri.p, f.tpiv.p, coup, W, Tl);
+            launch_pdl<kPdlDense>(l0_tri_solve<false>, dim3(g), dim3(kTriThreads), smem, st, nb, v.m, kc, nrhs, blk,
+                                  f.tri.p, f.tpiv.p, coup, W, Tl);
         CK_LAUNCH();
     };
     // down
@@ -679,7 +683,8 @@ void bcr_solve(Ctx& c, BcrFactor& f, const double2* coup, double2* W, int nrhs) 
             tri_solve(true, v, Tl);
         } else if (li == 0) {
             if (v.m > 1) {
-                launch_pdl<kPdlDense>(l0_up_rhs, dim3(ew_grid(blk, v.ne)), dim3(256), 0, st, nb, v.m, blk, coup, W, f.r.p);
+                launch_pdl<kPdlDense>(l0_up_rhs, dim3(ew_grid(blk, v.ne)), dim3(256), 0, st, nb, v.m, blk, coup, W,
+                                      f.r.p);
                 CK_LAUNCH();
             } else {
                 CK(cudaMemsetAsync(f.r.p, 0, size_t(blk) * sizeof(double2), st));
@@ -695,7 +700,8 @@ void bcr_solve(Ctx& c, BcrFactor& f, const double2* coup, double2* W, int nrhs) 
             // x_{2b} = t_b - x_{2b-1} P_b^T (b >= 1) - x_{2b+1} Q_b^T (2b+1 < m)
             const int nq = v.m / 2;
             if (v.ne >= kBcrTiledBatch2 && !warp_only) {  // copy t, then both products in place
-                launch_pdl<kPdlDense>(copy_blocks, dim3(ew_grid(blk, v.ne)), dim3(256), 0, st, blk, v.ne, Tl, blk, Wl(v, 0), sw);
+                launch_pdl<kPdlDense>(copy_blocks, dim3(ew_grid(blk, v.ne)), dim3(256), 0, st, blk, v.ne, Tl, blk,
+                                      Wl(v, 0), sw);
                 CK_LAUNCH();
                 if (v.ne > 1)
                     cgemm_batched(st, true, nrhs, nb, nb, -1.0, Wl(v, 1), nb, sw, v.P + nn, nb, nn, Wl(v, 2), nb, sw,

@@ -900,12 +900,16 @@ void cgemm_batched(cudaStream_t st, bool bt, int M, int N, int K, double alpha, 
         if (need <= scratch_count && int64_t(batch) * S <= 65535) {
             const dim3 g((N + 31) / 32, (M + 7) / 8, unsigned(batch * S));
             if (bt)
-                launch_pdl<kPdlDense>(zgemm_splitk_kernel<true>, dim3(g), dim3(128), 0, st, M, N, K, kc, S, A, lda, sA, B, ldb, sB, scratch);
+                launch_pdl<kPdlDense>(zgemm_splitk_kernel<true>, dim3(g), dim3(128), 0, st, M, N, K, kc, S, A, lda, sA,
+                                      B, ldb, sB, scratch);
             else
-                launch_pdl<kPdlDense>(zgemm_splitk_kernel<false>, dim3(g), dim3(128), 0, st, M, N, K, kc, S, A, lda, sA, B, ldb, sB, scratch);
+                launch_pdl<kPdlDense>(zgemm_splitk_kernel<false>, dim3(g), dim3(128), 0, st, M, N, K, kc, S, A, lda, sA,
+                                      B, ldb, sB, scratch);
             CK_LAUNCH();
             const int64_t mn = int64_t(M) * N;
-            launch_pdl<kPdlDense>(zgemm_splitk_reduce, dim3(dim3(unsigned(std::min<int64_t>((mn + 255) / 256, 64)), unsigned(batch))), dim3(256), 0, st, M, N, S, alpha, scratch, C0, ldc0, sC0, C, ldc, sC);
+            launch_pdl<kPdlDense>(zgemm_splitk_reduce,
+                                  dim3(dim3(unsigned(std::min<int64_t>((mn + 255) / 256, 64)), unsigned(batch))),
+                                  dim3(256), 0, st, M, N, S, alpha, scratch, C0, ldc0, sC0, C, ldc, sC);
             CK_LAUNCH();
             return;
         }
@@ -976,12 +980,14 @@ void cgemm2(cudaStream_t st, int M, int N, int K, const CgemmTerm& a, const Cgem
     static const int split_max = std::getenv("FWI_CGEMM2_SPLIT") ? std::atoi(std::getenv("FWI_CGEMM2_SPLIT")) : 8;
     if (batch <= split_max && K <= 4 * 4 * 32) {
         const dim3 g((N + 7) / 8, (M + 7) / 8, unsigned(batch));
-        launch_pdl<kPdlDense>(zgemm2_splitk_tile_kernel, dim3(g), dim3(128), 0, st, M, N, K, t0, t1, b ? 2 : 1, C0, ldc0, sC0, C, ldc, sC);
+        launch_pdl<kPdlDense>(zgemm2_splitk_tile_kernel, dim3(g), dim3(128), 0, st, M, N, K, t0, t1, b ? 2 : 1, C0,
+                              ldc0, sC0, C, ldc, sC);
         CK_LAUNCH();
         return;
     }
     const dim3 g((N + 31) / 32, (M + 7) / 8, unsigned(batch));
-    launch_pdl<kPdlDense>(zgemm2_warp_kernel, dim3(g), dim3(128), 0, st, M, N, K, t0, t1, b ? 2 : 1, C0, ldc0, sC0, C, ldc, sC);
+    launch_pdl<kPdlDense>(zgemm2_warp_kernel, dim3(g), dim3(128), 0, st, M, N, K, t0, t1, b ? 2 : 1, C0, ldc0, sC0, C,
+                          ldc, sC);
     CK_LAUNCH();
 }
 

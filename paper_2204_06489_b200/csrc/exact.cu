@@ -1530,7 +1530,8 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
     dim3 tb(32, 8);
     dim3 tg = f.col_lines ? dim3((f.L + 31) / 32, (f.nb + 31) / 32, nrhs)
                           : dim3((f.nb + 31) / 32, (f.L + 31) / 32, nrhs);
-    launch_pdl<kPdlExact>(gather_lines, dim3(tg), dim3(tb), 0, c.stream, f.col_lines, c.nx, c.nz, f.L, f.nb, nrhs, adjoint, b, W);
+    launch_pdl<kPdlExact>(gather_lines, dim3(tg), dim3(tb), 0, c.stream, f.col_lines, c.nx, c.nz, f.L, f.nb, nrhs,
+                          adjoint, b, W);
     CK_LAUNCH();
     bool done = false;
     if (f.bcr) {
@@ -1606,14 +1607,14 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
                     ExactFactor& fm = const_cast<ExactFactor&>(f);
                     if (fm.tbuf.count < size_t(nrhs) * f.nb) fm.tbuf.alloc(size_t(nrhs) * f.nb);
                     const int64_t blk = int64_t(nrhs) * f.nb;
-                    launch_pdl<kPdlExact>(middle_rhs, dim3(int((blk + 255) / 256)), dim3(256), 0, c.stream, 
-                        f.nb, blk, W + m * blk, f.coup.p + int64_t(m - 1) * f.nb, f.ybuf.p + (m - 1) * blk,
-                        f.coup.p + int64_t(m) * f.nb, f.ybuf.p + (m + 1) * blk, fm.tbuf.p);
+                    launch_pdl<kPdlExact>(middle_rhs, dim3(int((blk + 255) / 256)), dim3(256), 0, c.stream, f.nb, blk,
+                                          W + m * blk, f.coup.p + int64_t(m - 1) * f.nb, f.ybuf.p + (m - 1) * blk,
+                                          f.coup.p + int64_t(m) * f.nb, f.ybuf.p + (m + 1) * blk, fm.tbuf.p);
                     CK_LAUNCH();
                     const double2* Gm = f.G.p + int64_t(m) * f.nb * f.gp;
                     if (nrhs <= 8) {
-                        launch_pdl<kPdlExact>(middle_gemv<8>, dim3((f.nb + 7) / 8), dim3(256), 0, c.stream, f.nb, nrhs, Gm, f.gp, fm.tbuf.p,
-                                                                             W + m * blk);
+                        launch_pdl<kPdlExact>(middle_gemv<8>, dim3((f.nb + 7) / 8), dim3(256), 0, c.stream, f.nb, nrhs,
+                                              Gm, f.gp, fm.tbuf.p, W + m * blk);
                         CK_LAUNCH();
                     } else {
                         cgemm(c.stream, true, nrhs, f.nb, f.nb, 1.0, fm.tbuf.p, f.nb, Gm, f.gp, nullptr, 0, W + m * blk,
@@ -1663,7 +1664,8 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
             f.L, f.nb, nrhs, f.G.p, f.gp, f.coup.p, W);
         CK_LAUNCH();
     }
-    launch_pdl<kPdlExact>(scatter_lines, dim3(tg), dim3(tb), 0, c.stream, f.col_lines, c.nx, c.nz, f.L, f.nb, nrhs, adjoint, W, x);
+    launch_pdl<kPdlExact>(scatter_lines, dim3(tg), dim3(tb), 0, c.stream, f.col_lines, c.nx, c.nz, f.L, f.nb, nrhs,
+                          adjoint, W, x);
     CK_LAUNCH();
     c.solve_count[FWI_PRECOND_EXACT] += nrhs;
 }

@@ -138,10 +138,9 @@ void kkt_apply_raw(Ctx& c, const double* xi, double* out) {
     if (c.kkt_variant != 1 && kkt_apply_tma(c, false, xi, out)) return;
     dim3 blk(32, 8), grd((c.nx + 31) / 32, (c.nz + 7) / 8);
     double* x = const_cast<double*>(xi);
-    launch_pdl<kPdlKkt>(kkt_apply_kernel<F64>, dim3(grd), dim3(blk), 0, c.stream, 
-        c.nx, c.nz, c.K, c.n, c.w2, c.eps, c.diag.p, c.east.p, c.south.p, c.u.p, c.nrec_ptr.p,
-        c.nrec_k.p, c.nrec_w2.p, c.du_of(x), c.ds_of(x), c.la_of(x), c.du_of(out), c.ds_of(out),
-        c.la_of(out), 0, c.K, nullptr);
+    launch_pdl<kPdlKkt>(kkt_apply_kernel<F64>, dim3(grd), dim3(blk), 0, c.stream, c.nx, c.nz, c.K, c.n, c.w2, c.eps,
+                        c.diag.p, c.east.p, c.south.p, c.u.p, c.nrec_ptr.p, c.nrec_k.p, c.nrec_w2.p, c.du_of(x),
+                        c.ds_of(x), c.la_of(x), c.du_of(out), c.ds_of(out), c.la_of(out), 0, c.K, nullptr);
     CK_LAUNCH();
     c.kkt_kernel[0] = "kkt_apply_kernel<F64> (plain K1, csrc/kkt.cu)";
 }
@@ -201,10 +200,9 @@ void kkt_apply_host(Ctx& c, const double* in, double* out) {
                            c.s_h2d));
         CK(cudaEventRecord(c.ev_in[ch], c.s_h2d));
         CK(cudaStreamWaitEvent(c.stream, c.ev_in[ch], 0));
-        launch_pdl<kPdlKkt>(kkt_apply_kernel<F64>, dim3(grd), dim3(blk), 0, c.stream, 
-            c.nx, c.nz, K, n, c.w2, c.eps, c.diag.p, c.east.p, c.south.p, c.u.p, c.nrec_ptr.p, c.nrec_k.p,
-            c.nrec_w2.p, c.du_of(x), c.ds_of(x), c.la_of(x), c.du_of(y), c.ds_of(y), c.la_of(y), k0, k1,
-            c.hpl.p);
+        launch_pdl<kPdlKkt>(kkt_apply_kernel<F64>, dim3(grd), dim3(blk), 0, c.stream, c.nx, c.nz, K, n, c.w2, c.eps,
+                            c.diag.p, c.east.p, c.south.p, c.u.p, c.nrec_ptr.p, c.nrec_k.p, c.nrec_w2.p, c.du_of(x),
+                            c.ds_of(x), c.la_of(x), c.du_of(y), c.ds_of(y), c.la_of(y), k0, k1, c.hpl.p);
         CK_LAUNCH();
         CK(cudaEventRecord(c.ev_out[ch], c.stream));
         CK(cudaStreamWaitEvent(c.s_d2h, c.ev_out[ch], 0));
@@ -231,11 +229,11 @@ void kkt_apply(Ctx& c, const Vec& xi, Vec& out) {
     const int64_t kn2 = 2 * int64_t(c.K) * c.n;
     float* x = const_cast<float*>(xi.f.p);
     float* o = out.f.p;
-    launch_pdl<kPdlKkt>(kkt_apply_kernel<F32>, dim3(grd), dim3(blk), 0, c.stream, 
-        c.nx, c.nz, c.K, c.n, float(c.w2), float(c.eps), c.diag32.p, c.east32.p, c.south32.p,
-        c.u32.p, c.nrec_ptr.p, c.nrec_k.p, c.nrec_w2.p, reinterpret_cast<float2*>(x), x + kn2,
-        reinterpret_cast<float2*>(x + kn2 + c.ds_stride), reinterpret_cast<float2*>(o), o + kn2,
-        reinterpret_cast<float2*>(o + kn2 + c.ds_stride), 0, c.K, nullptr);
+    launch_pdl<kPdlKkt>(kkt_apply_kernel<F32>, dim3(grd), dim3(blk), 0, c.stream, c.nx, c.nz, c.K, c.n, float(c.w2),
+                        float(c.eps), c.diag32.p, c.east32.p, c.south32.p, c.u32.p, c.nrec_ptr.p, c.nrec_k.p,
+                        c.nrec_w2.p, reinterpret_cast<float2*>(x), x + kn2,
+                        reinterpret_cast<float2*>(x + kn2 + c.ds_stride), reinterpret_cast<float2*>(o), o + kn2,
+                        reinterpret_cast<float2*>(o + kn2 + c.ds_stride), 0, c.K, nullptr);
     CK_LAUNCH();
     c.kkt_kernel[1] = "kkt_apply_kernel<F32> (plain K1, csrc/kkt.cu)";
 }

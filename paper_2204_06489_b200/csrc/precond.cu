@@ -117,14 +117,14 @@ void precond_apply_raw(Ctx& c, int mode, const double* v, double* out) {
     // (1)
     block_solve(c, mode, true, c.du_of(vv), c.la_of(out), K);
     // (2)
-    launch_pdl<kPdlPrecond>(precond_ds_kernel, dim3(ew(n)), dim3(256), 0, c.stream, K, n, c.w2, c.eps, c.u.p, c.la_of(out), c.ds_of(vv),
-                                                  c.ds_of(out));
+    launch_pdl<kPdlPrecond>(precond_ds_kernel, dim3(ew(n)), dim3(256), 0, c.stream, K, n, c.w2, c.eps, c.u.p,
+                            c.la_of(out), c.ds_of(vv), c.ds_of(out));
     CK_LAUNCH();
     // (3)
     // the right-hand side is built in out.du and solved in place (both block solvers
     // read their whole input before writing)
-    launch_pdl<kPdlPrecond>(precond_rhs_kernel, dim3(ew(kn)), dim3(256), 0, c.stream, kn, n, c.w2, c.u.p, c.ds_of(out), c.la_of(vv),
-                                                    c.du_of(out));
+    launch_pdl<kPdlPrecond>(precond_rhs_kernel, dim3(ew(kn)), dim3(256), 0, c.stream, kn, n, c.w2, c.u.p, c.ds_of(out),
+                            c.la_of(vv), c.du_of(out));
     CK_LAUNCH();
     block_solve(c, mode, false, c.du_of(out), c.du_of(out), K);
 }

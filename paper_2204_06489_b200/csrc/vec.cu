@@ -402,9 +402,9 @@ static int ew_blocks(int64_t m) { return grid_blocks(m, 256, 16 * sm_count()); }
 
 void dev_dot_async(cudaStream_t st, const double* x, const double* y, double* out_dev,
                    double* partials, unsigned* ticket, int64_t len) {
-    launch_pdl<kPdlVec>(dot_kernel, dim3(reduce_blocks()), dim3(kRedThreads), 0, st, reinterpret_cast<const double2*>(x),
-                                                        reinterpret_cast<const double2*>(y), len / 2,
-                                                        partials, ticket, out_dev);
+    launch_pdl<kPdlVec>(dot_kernel, dim3(reduce_blocks()), dim3(kRedThreads), 0, st,
+                        reinterpret_cast<const double2*>(x), reinterpret_cast<const double2*>(y), len / 2, partials,
+                        ticket, out_dev);
     CK_LAUNCH();
 }
 
@@ -418,12 +418,13 @@ double dev_dot(Ctx* c, cudaStream_t st, const double* x, const double* y, int64_
 
 void dev_axpy(cudaStream_t st, double a, const double* x, double* y, int64_t len) {
     launch_pdl<kPdlVec>(axpy_kernel, dim3(ew_blocks(len / 2)), dim3(256), 0, st, a, reinterpret_cast<const double2*>(x),
-                                                    reinterpret_cast<double2*>(y), len / 2);
+                        reinterpret_cast<double2*>(y), len / 2);
     CK_LAUNCH();
 }
 
 void dev_scal(cudaStream_t st, double a, double* x, int64_t len) {
-    launch_pdl<kPdlVec>(scal_kernel, dim3(ew_blocks(len / 2)), dim3(256), 0, st, a, reinterpret_cast<double2*>(x), len / 2);
+    launch_pdl<kPdlVec>(scal_kernel, dim3(ew_blocks(len / 2)), dim3(256), 0, st, a, reinterpret_cast<double2*>(x),
+                        len / 2);
     CK_LAUNCH();
 }
 
@@ -442,24 +443,25 @@ __global__ void scal_rsqrt_kernel(const double* __restrict__ h2, double2* __rest
 }
 
 void dev_scal_rsqrt(cudaStream_t st, const double* h2_dev, double* x, int64_t len) {
-    launch_pdl<kPdlVec>(scal_rsqrt_kernel, dim3(ew_blocks(len / 2)), dim3(256), 0, st, h2_dev, reinterpret_cast<double2*>(x), len / 2);
+    launch_pdl<kPdlVec>(scal_rsqrt_kernel, dim3(ew_blocks(len / 2)), dim3(256), 0, st, h2_dev,
+                        reinterpret_cast<double2*>(x), len / 2);
     CK_LAUNCH();
 }
 
 void dev_mgs_step(cudaStream_t st, double* w, const double* vprev, const double* hprev_dev,
                   const double* vnext, double* h_out_dev, double* partials, unsigned* ticket,
                   int64_t len) {
-    launch_pdl<kPdlVec>(mgs_kernel, dim3(reduce_blocks()), dim3(kRedThreads), 0, st, 
-        reinterpret_cast<double2*>(w), reinterpret_cast<const double2*>(vprev), hprev_dev,
-        reinterpret_cast<const double2*>(vnext), len / 2, partials, ticket, h_out_dev);
+    launch_pdl<kPdlVec>(mgs_kernel, dim3(reduce_blocks()), dim3(kRedThreads), 0, st, reinterpret_cast<double2*>(w),
+                        reinterpret_cast<const double2*>(vprev), hprev_dev, reinterpret_cast<const double2*>(vnext),
+                        len / 2, partials, ticket, h_out_dev);
     CK_LAUNCH();
 }
 
 void dev_mgs_step_parts(cudaStream_t st, double* w, const double* vprev, const double* hprev_dev,
                         const double* vnext, double* partials_out, int64_t len) {
-    launch_pdl<kPdlVec>(mgs_partial_kernel, dim3(reduce_blocks()), dim3(kRedThreads), 0, st, 
-        reinterpret_cast<double2*>(w), reinterpret_cast<const double2*>(vprev), hprev_dev,
-        reinterpret_cast<const double2*>(vnext), len / 2, partials_out);
+    launch_pdl<kPdlVec>(mgs_partial_kernel, dim3(reduce_blocks()), dim3(kRedThreads), 0, st,
+                        reinterpret_cast<double2*>(w), reinterpret_cast<const double2*>(vprev), hprev_dev,
+                        reinterpret_cast<const double2*>(vnext), len / 2, partials_out);
     CK_LAUNCH();
 }
 
@@ -478,8 +480,8 @@ bool dev_mgs_all(cudaStream_t st, double* w, const double* const* v, int m, doub
     for (int i = 0; i < m; ++i) a.v[i] = reinterpret_cast<const double2*>(v[i]);
     const int64_t len2 = len / 2, per = int64_t(reduce_blocks()) * kRedThreads;
     auto go = [&](auto kern) {
-        launch_pdl<kPdlMgs>(kern, dim3(reduce_blocks()), dim3(kRedThreads), 0, st, reinterpret_cast<double2*>(w), a, m, len2,
-                   partials, ticket, flag, epoch, h_dev);
+        launch_pdl<kPdlMgs>(kern, dim3(reduce_blocks()), dim3(kRedThreads), 0, st, reinterpret_cast<double2*>(w), a, m,
+                            len2, partials, ticket, flag, epoch, h_dev);
     };
     if (len2 <= 2 * per) go(mgs_all_kernel<2>);
     else if (len2 <= 4 * per) go(mgs_all_kernel<4>);
@@ -500,16 +502,15 @@ void dev_multi_axpy(cudaStream_t st, double* out, const double* x, const double*
     require(m <= 64, "gmres: restart larger than 63 is not supported by the fused update");
     for (int i = 0; i < m; ++i) a.v[i] = reinterpret_cast<const double2*>(v[i]);
     launch_pdl<kPdlVec>(multi_axpy_kernel, dim3(ew_blocks(len / 2)), dim3(256), 0, st, reinterpret_cast<double2*>(out),
-                                                          reinterpret_cast<const double2*>(x), a,
-                                                          y_dev, m, len / 2);
+                        reinterpret_cast<const double2*>(x), a, y_dev, m, len / 2);
     CK_LAUNCH();
 }
 
 void dev_sub_norm2(cudaStream_t st, const double* b, const double* ax, double* out_dev,
                    double* partials, unsigned* ticket, int64_t len) {
-    launch_pdl<kPdlVec>(sub_norm2_kernel, dim3(reduce_blocks()), dim3(kRedThreads), 0, st, 
-        reinterpret_cast<const double2*>(b), reinterpret_cast<const double2*>(ax), len / 2, partials,
-        ticket, out_dev);
+    launch_pdl<kPdlVec>(sub_norm2_kernel, dim3(reduce_blocks()), dim3(kRedThreads), 0, st,
+                        reinterpret_cast<const double2*>(b), reinterpret_cast<const double2*>(ax), len / 2, partials,
+                        ticket, out_dev);
     CK_LAUNCH();
 }
 
