@@ -718,6 +718,10 @@ __global__ void __launch_bounds__(THR, 1)
     using R = typename A::R;
     constexpr int kSl = THR / COLS;  // row slots; a thread owns rows slot (and slot + kSl when RPT = 2)
     constexpr int RPT = 1024 / THR;  // rows per thread: 2 with 512 threads, 1 with 1024
+    // output stores: no L1 allocation, except complex64 with one source per stage (.cs); a
+    // compile-time choice, so the store sites carry no branch (FWI_KKT_KM_ST applies to the
+    // banded kernel only)
+    constexpr int kStm = (sizeof(T) == 8 && KS == 1) ? 0 : 1;
     extern __shared__ __align__(1024) unsigned char sm[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + size_t(S) * P.stage_bytes);
     unsigned* done = reinterpret_cast<unsigned*>(bar + S);  // WS = 2: warps finished with stage s
@@ -821,7 +825,7 @@ __global__ void __launch_bounds__(THR, 1)
                 pl[r] = A::radd(pl[r], A::re_pconj(P.w2, uc, lac));
                 if (!act[r]) continue;
                 const int64_t o = int64_t(k) * n + cnode[r];
-                st_mode(P.ola + o, A::sub(s_, A::pmul(P.w2, uc, dsv[r])), P.stmode);
+                st_mode(P.ola + o, A::sub(s_, A::pmul(P.w2, uc, dsv[r])), kStm);
                 if (qr[r] < qe[r] && P.nrec_k[qr[r]] == k) {
                     T f = A::zero();
                     while (qr[r] < qe[r] && P.nrec_k[qr[r]] == k) {
@@ -830,7 +834,7 @@ __global__ void __launch_bounds__(THR, 1)
                     }
                     t_ = A::add(f, t_);
                 }
-                st_mode(P.odu + o, t_, P.stmode);
+                st_mode(P.odu + o, t_, kStm);
             }
         }
         if constexpr (WS == 2) {
