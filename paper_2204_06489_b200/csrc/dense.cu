@@ -707,6 +707,7 @@ struct Gemm2Term {
 };
 
 // one 8x8 output tile (rows m0.., columns n0.., batch entry z) of C_z = C0_z + sum_t alpha_t A B
+template <int CH>
 __device__ __forceinline__ void zgemm2_tile(int M, int N, int K, const Gemm2Term& t0, const Gemm2Term& t1, int nterms,
                                             const double2* C0, int64_t ldc0, int64_t sC0, double2* C, int64_t ldc,
                                             int64_t sC, int m0, int n0, int z, int lane) {
@@ -720,8 +721,7 @@ __device__ __forceinline__ void zgemm2_tile(int M, int N, int K, const Gemm2Term
         const double2* A = T.A + (z - T.lo) * T.sA;
         const double2* B = T.B + (z - T.lo) * T.sB;
         double P[2] = {0.0, 0.0}, Q[2] = {0.0, 0.0}, I[2] = {0.0, 0.0};
-        // chunks of 8 k4-steps: the next chunk's 16 loads are issued before this chunk's DMMAs
-        constexpr int CH = 8;
+        // chunks of CH k4-steps: the next chunk's loads are issued before this chunk's DMMAs
         double2 ca[CH], cb[CH], na[CH], nb_[CH];
         auto load = [&](int k0, double2 (&ra)[CH], double2 (&rb)[CH]) {
 #pragma unroll
@@ -768,14 +768,18 @@ __device__ __forceinline__ void zgemm2_tile(int M, int N, int K, const Gemm2Term
     }
 }
 
-__global__ void __launch_bounds__(128) zgemm2_warp_kernel(int M, int N, int K, Gemm2Term t0, Gemm2Term t1,
-                                                         int nterms, const double2* C0, int64_t ldc0, int64_t sC0,
-                                                         double2* C, int64_t ldc, int64_t sC) {
+// CH: k4-steps per prefetched chunk; MINB: CTAs per SM the register budget is cut for (the kernel
+// is latency-bound: more resident warps beat deeper per-warp prefetch, C3 1.92 -> 1.86 ms per
+// GMRES iteration with CH = 4 at four CTAs per SM against CH = 8 at three)
+template <int CH, int MINB>
+__global__ void __launch_bounds__(128, MINB) zgemm2_warp_kernel(int M, int N, int K, Gemm2Term t0, Gemm2Term t1,
+                                                               int nterms, const double2* C0, int64_t ldc0,
+                                                               int64_t sC0, double2* C, int64_t ldc, int64_t sC) {
     pdl_enter();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int n0 = (blockIdx.x * 4 + w) * 8, m0 = blockIdx.y * 8, z = blockIdx.z;
     if (n0 >= N) return;
-    zgemm2_tile(M, N, K, t0, t1, nterms, C0, ldc0, sC0, C, ldc, sC, m0, n0, z, lane);
+    zgemm2_tile<CH>(M, N, K, t0, t1, nterms, C0, ldc0, sC0, C, ldc, sC, m0, n0, z, lane);
 }
 
 // The same products for narrow batches (the upper cyclic-reduction levels: a few products, so
@@ -986,8 +990,24 @@ void cgemm2(cudaStream_t st, int M, int N, int K, const CgemmTerm& a, const Cgem
         return;
     }
     const dim3 g((N + 31) / 32, (M + 7) / 8, unsigned(batch));
-    launch_pdl<kPdlDense>(zgemm2_warp_kernel, dim3(g), dim3(128), 0, st, M, N, K, t0, t1, b ? 2 : 1, C0, ldc0, sC0, C,
-                          ldc, sC);
+    // FWI_ZG2=<CH>,<MINB> picks the variant (diagnostics): 8,1 / 4,4 (default) / 4,5 / 2,6
+    static const int var = [] {
+        const char* e = std::getenv("FWI_ZG2");
+        if (!e) return 1;
+        const std::string v(e);
+        return v == "8,1" ? 0 : v == "4,5" ? 2 : v == "2,6" ? 3 : 1;
+    }();
+    auto go = [&](auto kern) {
+        launch_pdl<kPdlDense>(kern, g, dim3(128), 0, st, M, N, K, t0, t1, b ? 2 : 1, C0, ldc0, sC0, C, ldc, sC);
+    };
+    if (var == 0)
+        go(zgemm2_warp_kernel<8, 1>);
+    else if (var == 2)
+        go(zgemm2_warp_kernel<4, 5>);
+    else if (var == 3)
+        go(zgemm2_warp_kernel<2, 6>);
+    else
+        go(zgemm2_warp_kernel<4, 4>);
     CK_LAUNCH();
 }
 
