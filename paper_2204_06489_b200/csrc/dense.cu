@@ -444,10 +444,10 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int BM, bool BT, int BN = kPBN>
+template <int BM, bool BT, int BN = kPBN, int NS = kPStages>
 constexpr int zgemm_pipe_smem() {
     // A: [BM][kPPitchK]; B: BT ? [BN][kPPitchK] : [kPBK][BN + 2]   (double2 elements)
-    return kPStages * (BM * kPPitchK + (BT ? BN * kPPitchK : kPBK * (BN + 2))) * 16;
+    return NS * (BM * kPPitchK + (BT ? BN * kPPitchK : kPBK * (BN + 2))) * 16;
 }
 
 // G3: Gauss's three-product form, S = (Ar+Ai)(Br+Bi): real = P - Q, imag = S - P - Q
@@ -459,7 +459,7 @@ struct GemmStrides {
 
 // BN: the CTA's N tile (64, or 32 for narrow batches: twice the CTAs, so a batch of ~100
 // products spreads over the SMs more evenly); warps 2 (m) x 4 (n), warp tile (BM/2) x (BN/4)
-template <int BM, bool BT, bool G3, int BN = kPBN>
+template <int BM, bool BT, bool G3, int BN = kPBN, int NS = kPStages>
 __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, double alpha,
                                                          const double2* __restrict__ A, int64_t lda,
                                                          const double2* __restrict__ B, int64_t ldb,
@@ -508,19 +508,19 @@ __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, do
 
     double P[TM][UN][2] = {}, Q[TM][UN][2] = {}, I[TM][UN][2] = {};
 #pragma unroll
-    for (int s = 0; s < kPStages - 1; ++s) {
+    for (int s = 0; s < NS - 1; ++s) {
         if (s < KT) load_stage(s, s * kPBK);
         cp_async_commit();
     }
     for (int kt = 0; kt < KT; ++kt) {
-        cp_async_wait<kPStages - 2>();
+        cp_async_wait<NS - 2>();
         __syncthreads();  // stage kt landed for every thread; stage kt-1 is free
         {
-            const int nk = kt + kPStages - 1;
-            if (nk < KT) load_stage(nk % kPStages, nk * kPBK);
+            const int nk = kt + NS - 1;
+            if (nk < KT) load_stage(nk % NS, nk * kPBK);
             cp_async_commit();
         }
-        const double2* As = psm + (kt % kPStages) * (ASZ + BSZ);
+        const double2* As = psm + (kt % NS) * (ASZ + BSZ);
         const double2* Bs = As + ASZ;
         double2 fa[2][TM], fb[2][UN];
         double sa[2][TM], sb[2][UN];  // G3 operand sums
@@ -577,18 +577,18 @@ __global__ void __launch_bounds__(256) zgemm_pipe_kernel(int M, int N, int K, do
             }
 }
 
-template <int BM, bool BT, bool G3, int BN = kPBN>
+template <int BM, bool BT, bool G3, int BN = kPBN, int NS = kPStages>
 void zgemm_pipe_launch(cudaStream_t st, int M, int N, int K, double alpha, const double2* A, int64_t lda,
                        const double2* B, int64_t ldb, const double2* C0, int64_t ldc0, double2* C, int64_t ldc,
                        GemmStrides bs = {}, int batch = 1) {
-    constexpr int smem = zgemm_pipe_smem<BM, BT, BN>();
+    constexpr int smem = zgemm_pipe_smem<BM, BT, BN, NS>();
     static bool attr = false;
     if (!attr) {
-        CK(cudaFuncSetAttribute(zgemm_pipe_kernel<BM, BT, G3, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(zgemm_pipe_kernel<BM, BT, G3, BN, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem));
         attr = true;
     }
-    launch_pdl<kPdlDense>(zgemm_pipe_kernel<BM, BT, G3, BN>, dim3((N + BN - 1) / BN, (M + BM - 1) / BM, batch),
+    launch_pdl<kPdlDense>(zgemm_pipe_kernel<BM, BT, G3, BN, NS>, dim3((N + BN - 1) / BN, (M + BM - 1) / BM, batch),
                           dim3(256), smem, st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs);
     CK_LAUNCH();
 }
@@ -934,7 +934,17 @@ void cgemm_batched(cudaStream_t st, bool bt, int M, int N, int K, double alpha, 
         const int sms = sm_count();
         const int64_t w64 = 2 * ((t64 + sms - 1) / sms), w32 = (2 * t64 + sms - 1) / sms;  // in half tiles
         const bool narrow = bn_env ? bn_env == 32 : 5 * w32 <= 4 * w64;
-        if (narrow) {
+        // narrow tiles keep two stages (51 KB: four CTAs per SM; C3 537 -> 551 it/s against three
+        // stages at two CTAs per SM); FWI_CGEMM_NS=3 restores three
+        static const int ns_env = std::getenv("FWI_CGEMM_NS") ? std::atoi(std::getenv("FWI_CGEMM_NS")) : 2;
+        if (narrow && ns_env == 2) {
+            if (bt)
+                zgemm_pipe_launch<48, true, true, 32, 2>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs,
+                                                         batch);
+            else
+                zgemm_pipe_launch<48, false, true, 32, 2>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs,
+                                                          batch);
+        } else if (narrow) {
             if (bt)
                 zgemm_pipe_launch<48, true, true, 32>(st, M, N, K, alpha, A, lda, B, ldb, C0, ldc0, C, ldc, bs, batch);
             else
