@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(256) zgemm_dmma_kernel(int M, int N, int K, do
 // fragment element; fragments for the next k4 step are loaded while the current
 // one issues its DMMAs. One block barrier per 16-deep K slab.
 // ---------------------------------------------------------------------------
-constexpr int kPBN = 64, kPBK = 16, kPStages = 3, kPPitchK = kPBK + 4, kPPitchN = kPBN + 2;
+constexpr int kPBN = 64, kPBK = 16, kPStages = 3, kPPitchK = kPBK + 4;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem));

@@ -153,7 +153,6 @@ __global__ void __launch_bounds__(512) line_factor_kernel(
     __shared__ int s_p;
     __shared__ double2 s_pivinv;
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int64_t nn = int64_t(nb) * nb;
 
     // ---- S_i = T_i - E_{i-1} G_{i-1} E_{i-1}
     const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
@@ -344,7 +343,6 @@ __global__ void __launch_bounds__(256) sweep_kernel(int L, int nb, int nrhs,
     const int S = nb <= nt ? nt / nb : 1;
     const int seg = (nb + S - 1) / S;
     const int my_s = nb <= nt ? tid / nb : 0;
-    const int64_t nn = int64_t(nb) * nb;
 
     auto matvec = [&](const double2* G, bool subtract_into_y, int line) {
         // acc[k][m] = sum_j G[m][j] wv[k][j]  over this thread's (m, segment)
@@ -493,9 +491,6 @@ __device__ __forceinline__ uint32_t map_rank(uint32_t local_addr, uint32_t rank)
     uint32_t r;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
     return r;
-}
-__device__ __forceinline__ void st_cluster(uint32_t addr, double2 v) {
-    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
 }
 // remote store that completes 16 bytes on the receiver's mbarrier (no fence)
 __device__ __forceinline__ void st_async16(uint32_t addr, double2 v, uint32_t remote_bar) {
@@ -1386,7 +1381,6 @@ static void exact_factor_once(Ctx& c, bool line_pivot) {
         CK(cudaFuncSetAttribute(line_factor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm)));
     else
         CK(cudaFuncSetAttribute(line_factor_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm)));
-    const int64_t nn = int64_t(nb) * nb;
     for (int i = 0; i < L; ++i) {
         const double2* prev = i > 0 ? f->G.p + (i - 1) * int64_t(nb) * f->gp : nullptr;
         if (smem)
