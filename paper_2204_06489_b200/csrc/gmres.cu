@@ -569,6 +569,14 @@ Log gmres_core(GmresOps& ops, const double* b, double* x, int restart, double to
         if (two) WS.second_stream();
         const cudaStream_t sb = two ? WS.s2 : st;  // the residual branch's stream
         Scratch& scb = two ? *WS.sc2 : sc;
+        // on every exit (an error included) the residual branch is drained before its buffers go
+        // back to the context's pool
+        struct Drain {
+            cudaStream_t s;
+            ~Drain() {
+                if (s) cudaStreamSynchronize(s);
+            }
+        } drain{two ? sb : nullptr};
         grab(xc2);
         if (two) grab(axb);
         DevBuf<double>* xcb[2] = {&xc, &xc2};
