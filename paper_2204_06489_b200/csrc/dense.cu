@@ -991,7 +991,7 @@ void cgemm2(cudaStream_t st, int M, int N, int K, const CgemmTerm& a, const Cgem
     const Gemm2Term t0 = conv(a), t1 = b ? conv(*b) : t0;
     // narrow batches (a launch's warps fewer than ~4 per SM): the split-K tile kernel
     // (FWI_CGEMM2_SPLIT=<batch> moves the switch point, 0 disables it)
-    static const int split_max = std::getenv("FWI_CGEMM2_SPLIT") ? std::atoi(std::getenv("FWI_CGEMM2_SPLIT")) : 8;
+    static const int split_max = std::getenv("FWI_CGEMM2_SPLIT") ? std::atoi(std::getenv("FWI_CGEMM2_SPLIT")) : 12;
     if (batch <= split_max && K <= 4 * 4 * 32) {
         const dim3 g((N + 7) / 8, (M + 7) / 8, unsigned(batch));
         launch_pdl<kPdlDense>(zgemm2_splitk_tile_kernel, dim3(g), dim3(128), 0, st, M, N, K, t0, t1, b ? 2 : 1, C0,
