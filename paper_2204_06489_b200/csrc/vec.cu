@@ -116,7 +116,7 @@ __global__ void scal_kernel(double a, double2* __restrict__ x, int64_t m) {
 // One thread's share of an MGS step, w -= h_{i-1} v_{i-1}; acc += <v_i, w>, over its
 // grid-stride elements in order. The loads of U elements are issued before any of
 // them is used (memory-level parallelism); the accumulation order is unchanged.
-constexpr int kMgsUnroll = 4;
+constexpr int kMgsUnroll = 8;
 __device__ __forceinline__ void mgs_elem(double2& wv, const double2& pv, const double2& nv, double nh, bool prev,
                                          bool next, double& acc) {
     if (prev) {
@@ -469,11 +469,18 @@ bool dev_mgs_all(cudaStream_t st, double* w, const double* const* v, int m, doub
                  unsigned* ticket, unsigned* flag, unsigned& epoch, int64_t len) {
     if (m + 1 > 64) return false;
     // co-residency of the software grid barrier: reduce_blocks() CTAs of 256 threads
+    // (every variant that may launch: the grid barrier needs all its CTAs resident at once)
     static int ok = -1;
     if (ok < 0) {
-        int per_sm = 0;
-        ok = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgs_all_kernel<4>, kRedThreads, 0) == cudaSuccess &&
-             per_sm * sm_count() >= reduce_blocks();
+        ok = 1;
+        for (const void* k : {reinterpret_cast<const void*>(mgs_all_kernel<0>),
+                              reinterpret_cast<const void*>(mgs_all_kernel<2>),
+                              reinterpret_cast<const void*>(mgs_all_kernel<4>)}) {
+            int per_sm = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kRedThreads, 0) != cudaSuccess ||
+                per_sm * sm_count() < reduce_blocks())
+                ok = 0;
+        }
     }
     if (!ok) return false;
     MgsAllArgs a{};
