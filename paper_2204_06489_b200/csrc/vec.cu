@@ -10,6 +10,8 @@
 // per-thread strides, a fixed shuffle tree, and the last CTA to finish sums
 // the per-CTA partials in index order. Element-wise updates keep the
 // reference's rounding (no FMA: y + (a*x) rounded twice).
+#include <cstdlib>
+
 #include "ctx.cuh"
 
 namespace fwi_b200 {
@@ -159,12 +161,11 @@ __device__ __forceinline__ double2 ld_na(const double2* p) {
     return v;
 }
 
-template <bool HINT = false>
+template <bool HINT = false, int U = kMgsUnroll>
 __device__ __forceinline__ double mgs_pass(double2* __restrict__ w, const double2* __restrict__ vprev, double nh,
                                            const double2* __restrict__ vnext, int64_t m, int64_t t0, int64_t stride,
-                                           bool release = false) {
-    constexpr int U = kMgsUnroll;
-    double acc = 0.0;
+                                           bool release = false, double acc0 = 0.0) {
+    double acc = acc0;
     int64_t t = t0;
     uint64_t keep = 0, stream = 0;
     if (HINT) {
@@ -256,13 +257,18 @@ struct MgsAllArgs {
     const double2* v[64];
 };
 
-template <int QMAX>
-__global__ void __launch_bounds__(kRedThreads) mgs_all_kernel(double2* __restrict__ w, MgsAllArgs a, int m,
+// QS > 0 (streaming form, vectors far beyond the registers): the first QS of a thread's
+// grid-stride elements of w live in shared memory for the whole sweep, so only the rest of w
+// streams through L2 (config 3: 16 of 62 elements) and fewer of its dirty lines are written back
+// between steps. Same elements, same accumulation order (bit-identical to the plain streaming form).
+template <int QMAX, int QS = 0>
+__global__ void __launch_bounds__(kRedThreads, 2) mgs_all_kernel(double2* __restrict__ w, MgsAllArgs a, int m,
                                                               int64_t len2, double* partials, unsigned* ticket,
                                                               volatile unsigned* flag, unsigned epoch, double* h) {
     pdl_enter();
     __shared__ double sh[32];
     __shared__ bool last;
+    extern __shared__ double2 wsm[];  // QS > 0: [QS][blockDim.x]
     // QMAX > 0: this thread's grid-stride elements of w (at most QMAX) stay in registers
     // for the whole sweep and the next basis vector's elements are loaded before the
     // grid barrier; same elements, same order of accumulation as the streaming form.
@@ -274,6 +280,12 @@ __global__ void __launch_bounds__(kRedThreads) mgs_all_kernel(double2* __restric
             const int64_t t = t0 + q * stride;
             wq[q] = t < len2 ? w[t] : make_double2(0.0, 0.0);
             nq[q] = (t < len2 && m > 0) ? a.v[0][t] : make_double2(0.0, 0.0);
+        }
+    }
+    if constexpr (QS > 0) {
+        for (int q = 0; q < QS; ++q) {
+            const int64_t t = t0 + q * stride;
+            wsm[q * blockDim.x + threadIdx.x] = t < len2 ? w[t] : make_double2(0.0, 0.0);
         }
     }
     for (int i = 0; i <= m; ++i) {
@@ -303,6 +315,30 @@ __global__ void __launch_bounds__(kRedThreads) mgs_all_kernel(double2* __restric
                 pq[q] = nq[q];
                 if (i + 1 < m && t < len2) nq[q] = a.v[i + 1][t];
             }
+        } else if constexpr (QS > 0) {
+            const uint64_t stream = l2_policy_first();
+            constexpr int U = 4;
+#pragma unroll 1
+            for (int q0 = 0; q0 < QS; q0 += U) {
+                double2 pv[U], nv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t t = t0 + int64_t(q0 + u) * stride;
+                    const bool ok = q0 + u < QS && t < len2;
+                    pv[u] = (vprev && ok) ? ld_hint(vprev + t, stream) : make_double2(0.0, 0.0);
+                    nv[u] = (vnext && ok) ? ld_hint(vnext + t, stream) : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t t = t0 + int64_t(q0 + u) * stride;
+                    if (q0 + u >= QS || t >= len2) continue;
+                    double2& ws = wsm[(q0 + u) * blockDim.x + threadIdx.x];
+                    double2 wv = ws;
+                    mgs_elem(wv, pv[u], nv[u], nh, vprev != nullptr, vnext != nullptr, acc);
+                    if (vprev) ws = wv;
+                }
+            }
+            acc = mgs_pass<true>(w, vprev, nh, vnext, len2, t0 + int64_t(QS) * stride, stride, i == m, acc);
         } else {
             acc = mgs_pass<true>(w, vprev, nh, vnext, len2, t0, stride, i == m);
         }
@@ -335,6 +371,12 @@ __global__ void __launch_bounds__(kRedThreads) mgs_all_kernel(double2* __restric
         for (int q = 0; q < QMAX; ++q) {
             const int64_t t = t0 + q * stride;
             if (t < len2) w[t] = wq[q];
+        }
+    }
+    if constexpr (QS > 0) {
+        for (int q = 0; q < QS; ++q) {
+            const int64_t t = t0 + q * stride;
+            if (t < len2) w[t] = wsm[q * blockDim.x + threadIdx.x];
         }
     }
 }
@@ -470,7 +512,15 @@ bool dev_mgs_all(cudaStream_t st, double* w, const double* const* v, int m, doub
     if (m + 1 > 64) return false;
     // co-residency of the software grid barrier: reduce_blocks() CTAs of 256 threads
     // (every variant that may launch: the grid barrier needs all its CTAs resident at once)
-    static int ok = -1;
+    // shared-memory-resident elements of w per thread in the streaming form (FWI_MGS_QS=16|24, 0 =
+    // off): C3 560 -> 588 it/s with either (w's L2 footprint 76 -> 57 or 47 MB)
+    static const int qsel = std::getenv("FWI_MGS_QS") ? std::atoi(std::getenv("FWI_MGS_QS")) : 16;
+    const int kQS = qsel == 16 ? 16 : qsel == 24 ? 24 : 0;
+    const size_t kQSmem = size_t(kQS) * kRedThreads * sizeof(double2);
+    using MgsKern = void (*)(double2*, MgsAllArgs, int, int64_t, double*, unsigned*, volatile unsigned*, unsigned,
+                             double*);
+    const MgsKern qs_kernel = kQS == 24 ? mgs_all_kernel<0, 24> : mgs_all_kernel<0, 16>;
+    static int ok = -1, ok_qs = -1;
     if (ok < 0) {
         ok = 1;
         for (const void* k : {reinterpret_cast<const void*>(mgs_all_kernel<0>),
@@ -481,6 +531,14 @@ bool dev_mgs_all(cudaStream_t st, double* w, const double* const* v, int m, doub
                 per_sm * sm_count() < reduce_blocks())
                 ok = 0;
         }
+        int per_sm = 0;
+        ok_qs = kQS > 0 &&
+                cudaFuncSetAttribute(qs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kQSmem)) ==
+                    cudaSuccess &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qs_kernel, kRedThreads, kQSmem) ==
+                    cudaSuccess &&
+                per_sm * sm_count() >= reduce_blocks();
+        cudaGetLastError();
     }
     if (!ok) return false;
     MgsAllArgs a{};
@@ -490,9 +548,16 @@ bool dev_mgs_all(cudaStream_t st, double* w, const double* const* v, int m, doub
         launch_pdl<kPdlMgs>(kern, dim3(reduce_blocks()), dim3(kRedThreads), 0, st, reinterpret_cast<double2*>(w), a, m,
                             len2, partials, ticket, flag, epoch, h_dev);
     };
-    if (len2 <= 2 * per) go(mgs_all_kernel<2>);
-    else if (len2 <= 4 * per) go(mgs_all_kernel<4>);
-    else go(mgs_all_kernel<0>);
+    if (len2 <= 2 * per) {
+        go(mgs_all_kernel<2>);
+    } else if (len2 <= 4 * per) {
+        go(mgs_all_kernel<4>);
+    } else if (ok_qs && len2 >= int64_t(2 * kQS) * per) {
+        launch_pdl<kPdlMgs>(qs_kernel, dim3(reduce_blocks()), dim3(kRedThreads), kQSmem, st,
+                            reinterpret_cast<double2*>(w), a, m, len2, partials, ticket, flag, epoch, h_dev);
+    } else {
+        go(mgs_all_kernel<0>);
+    }
     CK_LAUNCH();
     epoch += unsigned(m) + 1u;
     return true;
