@@ -110,6 +110,90 @@ __global__ void __launch_bounds__(256) kkt_apply_kernel(
         plbuf[c] = pl;
 }
 
+// The same apply for small problems with the sources spread over threads: one thread per (node,
+// source slot), a CTA = 32 nodes of a row x 8 source slots (config 1: 256 CTAs instead of 32 with
+// the node-per-thread kernel, whose threads walk all K sources). Each (node, source) output is
+// computed exactly as above; the ds row's K-sum is taken in source order from shared memory by the
+// slot-0 thread of each node, so the result is bit-identical.
+constexpr int kKsNodes = 32, kKsSlots = 8, kKsMaxK = 64;
+template <class A>
+__global__ void __launch_bounds__(kKsNodes * kKsSlots) kkt_apply_ks_kernel(
+    int nx, int nz, int K, int64_t n, typename A::R w2, typename A::R eps,
+    const typename A::T* __restrict__ diag, const typename A::T* __restrict__ east,
+    const typename A::T* __restrict__ south, const typename A::T* __restrict__ u,
+    const int* __restrict__ nrec_ptr, const int* __restrict__ nrec_k,
+    const double* __restrict__ nrec_w2, const typename A::T* __restrict__ du,
+    const typename A::R* __restrict__ ds, const typename A::T* __restrict__ la,
+    typename A::T* __restrict__ odu, typename A::R* __restrict__ ods, typename A::T* __restrict__ ola) {
+    pdl_enter();
+    using T = typename A::T;
+    using R = typename A::R;
+    __shared__ R pterm[kKsMaxK][kKsNodes];
+    const int lx = threadIdx.x, ks = threadIdx.y;
+    const int ix = blockIdx.x * kKsNodes + lx, iz = blockIdx.y;
+    const bool in = ix < nx;
+    const int64_t c = int64_t(iz) * nx + (in ? ix : 0);
+    if (in) {
+        const bool bnd = on_boundary(ix, iz, nx, nz);
+        const bool hN = !bnd && !on_boundary(ix, iz - 1, nx, nz);
+        const bool hW = !bnd && !on_boundary(ix - 1, iz, nx, nz);
+        const bool hE = !bnd && !on_boundary(ix + 1, iz, nx, nz);
+        const bool hS = !bnd && !on_boundary(ix, iz + 1, nx, nz);
+        const T cD = diag[c];
+        const T cN = hN ? south[c - nx] : A::zero();
+        const T cW = hW ? east[c - 1] : A::zero();
+        const T cE = hE ? east[c] : A::zero();
+        const T cS = hS ? south[c] : A::zero();
+        const R dsv = ds[c];
+        const int q0 = nrec_ptr[c], qe = nrec_ptr[c + 1];
+        for (int k = ks; k < K; k += kKsSlots) {
+            const int64_t o = int64_t(k) * n + c;
+            T s_ = A::zero();
+            T t_ = A::zero();
+            if (hN) {
+                s_ = A::add(s_, A::mul(cN, du[o - nx]));
+                t_ = A::add(t_, A::mulc(cN, la[o - nx]));
+            }
+            if (hW) {
+                s_ = A::add(s_, A::mul(cW, du[o - 1]));
+                t_ = A::add(t_, A::mulc(cW, la[o - 1]));
+            }
+            const T duc = du[o];
+            const T lac = la[o];
+            s_ = A::add(s_, A::mul(cD, duc));
+            t_ = A::add(t_, A::mulc(cD, lac));
+            if (hE) {
+                s_ = A::add(s_, A::mul(cE, du[o + 1]));
+                t_ = A::add(t_, A::mulc(cE, la[o + 1]));
+            }
+            if (hS) {
+                s_ = A::add(s_, A::mul(cS, du[o + nx]));
+                t_ = A::add(t_, A::mulc(cS, la[o + nx]));
+            }
+            const T uc = u[o];
+            ola[o] = A::sub(s_, A::pmul(w2, uc, dsv));
+            int q = q0;
+            while (q < qe && nrec_k[q] < k) ++q;
+            if (q < qe && nrec_k[q] == k) {
+                T f = A::zero();
+                while (q < qe && nrec_k[q] == k) {
+                    f = A::add(f, A::rm(R(nrec_w2[q]), duc));
+                    ++q;
+                }
+                t_ = A::add(f, t_);
+            }
+            odu[o] = t_;
+            pterm[k][lx] = A::re_pconj(w2, uc, lac);
+        }
+    }
+    __syncthreads();
+    if (in && ks == 0) {
+        R pl = R(0);
+        for (int k = 0; k < K; ++k) pl = A::radd(pl, pterm[k][lx]);
+        ods[c] = A::rsub(A::rmulr(eps, ds[c]), pl);
+    }
+}
+
 // kkt_rhs (src/kkt.cpp:98-112): b = (Q^H W^T W r scattered per source,
 // -eps s or 0, 0). One thread per source keeps the reference's data order
 // for duplicate receivers.
@@ -136,8 +220,19 @@ __global__ void kkt_rhs_ds(int64_t n, double neg_eps, const double* __restrict__
 
 void kkt_apply_raw(Ctx& c, const double* xi, double* out) {
     if (c.kkt_variant != 1 && kkt_apply_tma(c, false, xi, out)) return;
-    dim3 blk(32, 8), grd((c.nx + 31) / 32, (c.nz + 7) / 8);
     double* x = const_cast<double*>(xi);
+    // small problems: sources over threads (FWI_KKT_KS=0 keeps the node-per-thread kernel)
+    const bool ks_off = std::getenv("FWI_KKT_KS") && std::atoi(std::getenv("FWI_KKT_KS")) == 0;
+    if (!ks_off && c.K <= kKsMaxK) {
+        launch_pdl<kPdlKkt>(kkt_apply_ks_kernel<F64>, dim3((c.nx + kKsNodes - 1) / kKsNodes, c.nz),
+                            dim3(kKsNodes, kKsSlots), 0, c.stream, c.nx, c.nz, c.K, c.n, c.w2, c.eps, c.diag.p,
+                            c.east.p, c.south.p, c.u.p, c.nrec_ptr.p, c.nrec_k.p, c.nrec_w2.p, c.du_of(x),
+                            c.ds_of(x), c.la_of(x), c.du_of(out), c.ds_of(out), c.la_of(out));
+        CK_LAUNCH();
+        c.kkt_kernel[0] = "kkt_apply_ks_kernel<F64> (plain K1, sources over threads, csrc/kkt.cu)";
+        return;
+    }
+    dim3 blk(32, 8), grd((c.nx + 31) / 32, (c.nz + 7) / 8);
     launch_pdl<kPdlKkt>(kkt_apply_kernel<F64>, dim3(grd), dim3(blk), 0, c.stream, c.nx, c.nz, c.K, c.n, c.w2, c.eps,
                         c.diag.p, c.east.p, c.south.p, c.u.p, c.nrec_ptr.p, c.nrec_k.p, c.nrec_w2.p, c.du_of(x),
                         c.ds_of(x), c.la_of(x), c.du_of(out), c.ds_of(out), c.la_of(out), 0, c.K, nullptr);

@@ -123,16 +123,22 @@ def test_kkt_apply_c2_parity():
     assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("variant", ["plain", "tma", "tma_bands", "tma_balanced", "tile"])
+@pytest.mark.parametrize("variant", ["plain", "plain_nodes", "tma", "tma_bands", "tma_balanced", "tile"])
 @pytest.mark.parametrize("mk", PROBLEMS + [lambda: c2_problem(K=5, R=17),
+                                           lambda: small_problem(nx=45, nz=20, n_pml=3, K=19, R=6,
+                                                                 duplicate_receiver=True, seed=9),
                                            lambda: small_problem(nx=70, nz=42, n_pml=5, K=3, R=11,
                                                                  duplicate_receiver=True, seed=7)])
 def test_kkt_apply_kernel_variants_bit_exact(mk, variant, monkeypatch):
-    """Every K1 kernel (source-major TMA = "tma", the chunked tile-TMA kernel, plain) reproduces
+    """Every K1 kernel (source-major TMA = "tma", the chunked tile-TMA kernel, plain with sources
+    over threads or walked per node) reproduces
     the reference; the TMA kernels are forced on these small grids (partial strips and rectangles,
     duplicate receivers; odd widths fall back to the plain kernel)."""
     monkeypatch.setenv("FWI_KKT_KERNEL", variant)
-    if variant != "plain":
+    if variant == "plain_nodes":  # node-per-thread plain kernel (sources walked by each thread)
+        monkeypatch.setenv("FWI_KKT_KERNEL", "plain")
+        monkeypatch.setenv("FWI_KKT_KS", "0")
+    elif variant != "plain":
         monkeypatch.setenv("FWI_KKT_FORCE_TMA", "1")
         monkeypatch.setenv("FWI_KKT_KM_FORCE", "1")  # source-major kernel even for 1-row rectangles
     if variant == "tma_balanced":  # area-balanced strips of two widths (the rectangle table)
