@@ -28,7 +28,8 @@ from .krylov import ConvergenceLog
 from .problem import Problem
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfwi_b200.so")
+# FWI_B200_LIB: another build of the same library (binary A/B runs, tools/ab_lib.py)
+LIB_PATH = os.environ.get("FWI_B200_LIB") or os.path.join(HERE, "libfwi_b200.so")
 
 _dp = C.POINTER(C.c_double)
 _fp = C.POINTER(C.c_float)

@@ -60,24 +60,6 @@ struct ExactFactor {
     DenseWork dwork2;
     DevBuf<double2> tbuf2;
     BcrFactor* bcr = nullptr;  // block cyclic reduction (bcr.cu) instead of the Schur sweeps
-    // Segmented factorisation (four chains, three separator lines; see segmented_factor):
-    // seg[0] = lines [0, sep[0]) eliminated upwards, seg[1] = (sep[0], sep[1]) upwards with a
-    // spike to sep[0], seg[2] = (sep[1], sep[2]) downwards with a spike to sep[2], seg[3] =
-    // (sep[2], L) downwards.
-    bool segmented = false;
-    int sep[3] = {0, 0, 0};
-    int seg_count[4] = {0, 0, 0, 0};
-    int cmax = 0;              // longest spike segment
-    DevBuf<double2> Fa;        // [2][nb][cmax*nb]: separator row of the fill, per spike line
-    DevBuf<double2> FaT;       // [2][cmax][nb][nb]: Fa_q transposed
-    DevBuf<double2> WaT;       // [2][cmax][nb][nb]: (G_q Fa_q^T) transposed
-    DevBuf<double2> Ssep;      // 3nb x 3nb: the separators' Schur complement, then its inverse
-    DevBuf<double2> SinvT;     // the inverse transposed
-    DevBuf<double2> seg_tmp;   // nb x nb factor scratch
-    DevBuf<unsigned> seg_cnt;  // sep_rhs arrival counters
-    DevBuf<double2> Pq;        // solve scratch: per-line spike products [2][cmax][nrhs][nb]
-    DevBuf<double2> Ts;        // solve scratch: separator right-hand sides [3][nrhs][nb]
-    DevBuf<double2> Xs;        // solve scratch: separator solutions [3][nrhs][nb]
     void ensure_side() {
         if (s2) return;
         CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
@@ -97,9 +79,7 @@ struct ExactFactor {
 
 void exact_free(ExactFactor* f) { delete f; }
 int64_t exact_bytes(const ExactFactor* f) {
-    return f ? int64_t(f->G.bytes() + f->coup.bytes() + f->Fa.bytes() + f->FaT.bytes() + f->WaT.bytes() + 2 * f->Ssep.bytes()) +
-                   bcr_bytes(f->bcr)
-             : 0;
+    return f ? int64_t(f->G.bytes() + f->coup.bytes()) + bcr_bytes(f->bcr) : 0;
 }
 
 namespace {
@@ -699,9 +679,8 @@ struct WSweepArgs {
     double2* Y;
     uint32_t off_e, off_b, stage_bytes, off_y, off_w, off_bar;
     unsigned long long* trace;  // diagnostics: per-step clock64 stamps of CTA 0 / warp 0, or null
-    SweepChain chain[4];        // cluster c runs chain[c / groups] (groups = RHS groups per chain)
-    int nchains, groups;
-    int early;                  // set-up and G prefetch before griddepcontrol.wait (FWI_SWEEP_EARLY)
+    SweepChain chain[2];        // clusters [0, groups0) run chain[0], the rest chain[1]
+    int groups0;
 };
 
 __host__ __device__ __forceinline__ int chain_steps(const SweepChain& c) {
@@ -750,23 +729,17 @@ __device__ __forceinline__ void cmac(double2& c, const double2 g, const double2 
 
 template <int CS, int KG, int KR, bool TRACE, bool EVEN>
 __global__ void __launch_bounds__((KG / KR + 1) * 32) sweep_warp_kernel(const WSweepArgs a) {
-    // Programmatic dependent launch: everything up to the first read of the previous kernel's
-    // output (the right-hand sides W, y in Y, the boundary solution) runs before
-    // griddepcontrol.wait when a.early is set: the barrier set-up, the cluster sync and the
-    // producer's G / coupling loads for the first ring stages (G and the couplings are written
-    // by the factorisation, which completed before the previous kernel of the solve started).
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if (!a.early) asm volatile("griddepcontrol.wait;" ::: "memory");
+    pdl_enter();
     constexpr int NW = KG / KR;  // consumer warps
     extern __shared__ __align__(128) unsigned char wsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
     const int cid = blockIdx.x / CS;
-    const int chn = cid / a.groups;
+    const int chn = cid < a.groups0 ? 0 : 1;
     const SweepChain C = a.chain[chn];
-    const int grp = cid - chn * a.groups;
+    const int grp = chn == 0 ? cid : cid - a.groups0;
     const int nb = a.nb, gp = a.gp, nrhs = a.nrhs, R = a.R, Rp = a.Rp;
-    const int S = a.nst;  // ring depth (any count from 2 to kWMaxStages)
+    const int S = a.nst, smask = a.nst - 1;  // power of two
     const int nbp = nb + 1;
     const int k0 = grp * KG;
     const int kc = min(KG, nrhs - k0);
@@ -795,28 +768,8 @@ __global__ void __launch_bounds__((KG / KR + 1) * 32) sweep_warp_kernel(const WS
             const uint32_t gbytes = uint32_t(rows) * gp * sizeof(double2);
             const uint32_t ebytes = uint32_t(rows) * sizeof(double2);
             const uint32_t bbytes = uint32_t(kc) * nb * sizeof(double2);
-            int st0 = 0;
-            if (a.early) {  // the first stages' G and coupling slabs, then wait, then their RHS
-                const int pre = min(S, nsteps);
-                for (int st = 0; st < pre; ++st) {
-                    unsigned char* buf = wsm + st * a.stage_bytes;
-                    const int i = chain_line(C, st);
-                    const int cidx = st + 1 < nsteps ? min(i, chain_line(C, st + 1)) : 0;
-                    const uint32_t eb = (st + 1 < nsteps) ? ebytes : 0u;
-                    const uint32_t bb = chain_fwd(C, st) ? bbytes : 0u;
-                    bar_expect(&full[st], gbytes + eb + bb);
-                    if (gbytes) bulk_g2s(buf, a.G + (int64_t(i) * nb + r0) * gp, gbytes, &full[st]);
-                    if (eb) bulk_g2s(buf + a.off_e, a.coup + int64_t(cidx) * nb + r0, eb, &full[st]);
-                }
-                asm volatile("griddepcontrol.wait;" ::: "memory");
-                for (int st = 0; st < pre; ++st)
-                    if (chain_fwd(C, st) && bbytes)
-                        bulk_g2s(wsm + st * a.stage_bytes + a.off_b,
-                                 a.W + (int64_t(chain_line(C, st)) * nrhs + k0) * nb, bbytes, &full[st]);
-                st0 = pre;
-            }
-            for (int st = st0; st < nsteps; ++st) {
-                const int sb = st % S;
+            for (int st = 0; st < nsteps; ++st) {
+                const int sb = st & smask;
                 if (st >= S) bar_wait_lazy(&empty[sb], ((st - S) / S) & 1);
                 unsigned char* buf = wsm + sb * a.stage_bytes;
                 const bool fwd = chain_fwd(C, st);
@@ -833,7 +786,6 @@ __global__ void __launch_bounds__((KG / KR + 1) * 32) sweep_warp_kernel(const WS
             }
         }
     } else {  // ---- consumer warp: right-hand sides k0 + warp*KR + [0, KR)
-        if (a.early) asm volatile("griddepcontrol.wait;" ::: "memory");
         const int w = warp;
         const int kw = w * KR;                    // first local RHS of this warp
         const int kr = max(0, min(KR, kc - kw));  // active RHS of this warp
@@ -1039,194 +991,6 @@ __global__ void __launch_bounds__(256) middle_gemv(int nb, int nrhs, const doubl
     }
 }
 
-// ---- segmented factorisation / solve (four sweep chains meeting three separator lines) ----
-// A chain that starts next to a separator (not at the grid edge) fills in a coupling between
-// that separator and each of its lines (the "spike"): Fa_1 = E (the separator's coupling to
-// the chain's first line), Fa_{q+1} = -Fa_q G_q E_q. The solve adds t_sep -= sum_q Fa_q y_q
-// after the forward chains and z_q = y_q - (G_q Fa_q^T) x_sep before the backward chains.
-
-// dst[m][j] = -src[m][j] e[j]; with dst2 also dst2[j][m] = the same value (mirror block)
-__global__ void spike_next(int nb, const double2* __restrict__ src, const double2* __restrict__ e,
-                           double2* __restrict__ dst, int64_t ld, double2* __restrict__ dst2, int64_t ld2) {
-    const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (t >= int64_t(nb) * nb) return;
-    const int m = int(t / nb), j = int(t % nb);
-    const double2 v = fmul(src[t], e[j]);
-    const double2 nv = make_double2(-v.x, -v.y);
-    dst[int64_t(m) * ld + j] = nv;
-    if (dst2) dst2[int64_t(j) * ld2 + m] = nv;
-}
-
-// dst = diag(e) (nb x nb, row pitch ld)
-__global__ void diag_block(int nb, const double2* __restrict__ e, double2* __restrict__ dst, int64_t ld) {
-    const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (t >= int64_t(nb) * nb) return;
-    const int m = int(t / nb), j = int(t % nb);
-    dst[int64_t(m) * ld + j] = m == j ? e[m] : make_double2(0.0, 0.0);
-}
-
-struct SegSolveArgs {
-    int nb, nrhs, cmax;
-    int sep[3];
-    int sfirst[2], sdir[2], scount[2];  // the two spike chains (elimination order)
-    int ssep[2];                        // separator block (0..2) each spike belongs to
-    // chain ends feeding each separator through the ordinary coupling: line, coupling index
-    int nend[3], eline[3][2], ecoup[3][2];
-    const double2* FaT;   // [2][cmax][nb][nb]: FaT[s][q][i][m] = Fa_q[m][i]
-    const double2* WaT;   // [2][cmax][nb][nb]: WaT[s][q][j][m] = (G_q Fa_q^T)[m][j]
-    const double2* SinvT;  // 3nb x 3nb: SinvT[j][r] = Sinv[r][j]
-    const double2* coup;
-    const double2* W;  // b (line-major [line][k][m]); separator lines read only
-    double2* Wout;     // x of the separator lines written here (same buffer as W)
-    double2* Y;        // y of the chains; spike lines updated in place to z
-    double2* Pq;       // [2][cmax][nrhs][nb]: per-line spike products
-    double2* Ts;       // [3][nrhs][nb]: the separators' right-hand sides
-    double2* Xs;       // [3][nrhs][nb]
-    unsigned* cnt;     // [2][nb / 32 + 1] arrival counters (zero between solves)
-};
-
-// sum_i A[i][m] v[i] over i < n for this thread's row m: four interleaved accumulators
-// (fixed order of combination), A coalesced across the warp's rows, v a warp broadcast
-__device__ __forceinline__ double2 col_dot(const double2* __restrict__ A, int64_t lda, int m,
-                                           const double2* __restrict__ v, int n) {
-    double2 acc[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
-                      make_double2(0.0, 0.0)};
-    int i = 0;
-    for (; i + 4 <= n; i += 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) cmac(acc[u], A[int64_t(i + u) * lda + m], v[i + u]);
-    }
-    for (; i < n; ++i) cmac(acc[0], A[int64_t(i) * lda + m], v[i]);
-    return make_double2((acc[0].x + acc[1].x) + (acc[2].x + acc[3].x), (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y));
-}
-
-// Separator right-hand sides t_sep[j][k][m] = b - (ordinary chain ends) - sum_q Fa_q y_q:
-// CTA (row block of 32, spike line q, spike s) forms Fa_q y_q for its rows and all k; the last
-// CTA of a row block to arrive sums the lines' products in line order and writes t. Grid
-// z = 2: the middle separator (no spike), elementwise, by the q = 0 CTAs.
-__global__ void __launch_bounds__(256) sep_rhs(const SegSolveArgs a) {
-    pdl_enter();
-    const int nb = a.nb, nrhs = a.nrhs;
-    const int64_t blk = int64_t(nrhs) * nb;
-    const int rb = blockIdx.x, q = blockIdx.y, s = blockIdx.z;
-    const int m = rb * 32 + (threadIdx.x & 31), kl = threadIdx.x >> 5;
-    auto finish = [&](int j, bool spike_sum, int sidx) {
-        if (m >= nb) return;
-        for (int k = kl; k < nrhs; k += 8) {
-            double2 v = a.W[a.sep[j] * blk + int64_t(k) * nb + m];
-            for (int e = 0; e < a.nend[j]; ++e) {
-                const double2 t = fmul(a.coup[int64_t(a.ecoup[j][e]) * nb + m], a.Y[a.eline[j][e] * blk + int64_t(k) * nb + m]);
-                v.x -= t.x;
-                v.y -= t.y;
-            }
-            if (spike_sum)
-                for (int p = 0; p < a.scount[sidx]; ++p) {
-                    const double2 t = a.Pq[((int64_t(sidx) * a.cmax + p) * nrhs + k) * nb + m];
-                    v.x -= t.x;
-                    v.y -= t.y;
-                }
-            a.Ts[(int64_t(j) * nrhs + k) * nb + m] = v;
-        }
-    };
-    if (s == 2) {  // middle separator
-        if (q == 0) finish(1, false, 0);
-        return;
-    }
-    if (q >= a.scount[s]) return;
-    const int line = a.sfirst[s] + a.sdir[s] * q;
-    const double2* A = a.FaT + (int64_t(s) * a.cmax + q) * nb * nb;
-    if (m < nb)
-        for (int k = kl; k < nrhs; k += 8)
-            a.Pq[((int64_t(s) * a.cmax + q) * nrhs + k) * nb + m] = col_dot(A, nb, m, a.Y + line * blk + int64_t(k) * nb, nb);
-    // the last arrival of this row block combines (the fence makes the products visible first)
-    __shared__ unsigned last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned* c = a.cnt + s * (nb / 32 + 1) + rb;
-        last = atomicAdd(c, 1u) == unsigned(a.scount[s] - 1);
-        if (last) *c = 0u;  // ready for the next solve
-    }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    finish(a.ssep[s], true, s);
-}
-
-// x_sep = Sinv t_sep: thread per (row r, right-hand side k, half of the inner index), the two
-// halves added in order through shared memory; SinvT coalesced across rows, t a broadcast
-__global__ void __launch_bounds__(128) sep_solve(const SegSolveArgs a) {
-    pdl_enter();
-    __shared__ double2 part[64];
-    const int nb = a.nb, nrhs = a.nrhs, n3 = 3 * nb;
-    const int rl = threadIdx.x & 7, kl = (threadIdx.x >> 3) & 7, h = threadIdx.x >> 6;
-    const int r = blockIdx.x * 8 + rl;
-    const int j0 = h * (n3 / 2), j1 = h ? n3 : n3 / 2;
-    for (int k0 = 0; k0 < nrhs; k0 += 8) {
-        const int k = k0 + kl;
-        double2 v = make_double2(0.0, 0.0);
-        if (r < n3 && k < nrhs) {
-            double2 acc[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
-                              make_double2(0.0, 0.0)};
-            int j = j0;
-            for (; j + 4 <= j1; j += 4) {
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int jj = j + u, sj = jj / nb;
-                    cmac(acc[u], a.SinvT[int64_t(jj) * n3 + r], a.Ts[(int64_t(sj) * nrhs + k) * nb + (jj - sj * nb)]);
-                }
-            }
-            for (; j < j1; ++j) {
-                const int sj = j / nb;
-                cmac(acc[0], a.SinvT[int64_t(j) * n3 + r], a.Ts[(int64_t(sj) * nrhs + k) * nb + (j - sj * nb)]);
-            }
-            v = make_double2((acc[0].x + acc[1].x) + (acc[2].x + acc[3].x), (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y));
-        }
-        if (h == 1) part[threadIdx.x - 64] = v;
-        __syncthreads();
-        if (h == 0 && r < n3 && k < nrhs) {
-            const double2 w = part[threadIdx.x];
-            const int sj = r / nb;
-            a.Xs[(int64_t(sj) * nrhs + k) * nb + (r - sj * nb)] = make_double2(v.x + w.x, v.y + w.y);
-        }
-        __syncthreads();
-    }
-}
-
-// z_q = y_q - Wa_q x_sep on the spike lines: CTA (row block of 32, line q, spike s), thread per
-// (row, k); the (q = 0, s = 0) CTAs also copy the separator solutions into the output lines
-__global__ void __launch_bounds__(256) spike_expand(const SegSolveArgs a) {
-    pdl_enter();
-    const int nb = a.nb, nrhs = a.nrhs;
-    const int64_t blk = int64_t(nrhs) * nb;
-    const int rb = blockIdx.x, q = blockIdx.y, s = blockIdx.z;
-    const int m = rb * 32 + (threadIdx.x & 31), kl = threadIdx.x >> 5;
-    if (m >= nb) return;
-    if (q == 0 && s == 0)
-        for (int t = kl; t < 3 * nrhs; t += 8) {
-            const int j = t / nrhs, k = t - j * nrhs;
-            a.Wout[a.sep[j] * blk + int64_t(k) * nb + m] = a.Xs[(int64_t(j) * nrhs + k) * nb + m];
-        }
-    if (q >= a.scount[s]) return;
-    const int line = a.sfirst[s] + a.sdir[s] * q;
-    const double2* A = a.WaT + (int64_t(s) * a.cmax + q) * nb * nb;
-    const double2* X = a.Xs + int64_t(a.ssep[s]) * blk;
-    for (int k = kl; k < nrhs; k += 8) {
-        const double2 w = col_dot(A, nb, m, X + int64_t(k) * nb, nb);
-        double2& y = a.Y[line * blk + int64_t(k) * nb + m];
-        y = make_double2(y.x - w.x, y.y - w.y);
-    }
-}
-
-// dst[j][i] = src[i][j] (n x n, pitches lds, ldd)
-__global__ void transpose_block(int n, const double2* __restrict__ src, int64_t lds, double2* __restrict__ dst,
-                                int64_t ldd) {
-    const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (t >= int64_t(n) * n) return;
-    const int i = int(t / n), j = int(t % n);
-    dst[int64_t(j) * ldd + i] = src[int64_t(i) * lds + j];
-}
-
 struct WarpPlan {
     WSweepArgs a;
     int CS = 0, KG = 0, KR = 0;
@@ -1235,7 +999,7 @@ struct WarpPlan {
     double est = 0;
 };
 
-bool warp_layout(int nb, int L, int gp, int nrhs, int CS, int KG, int KR, WarpPlan& p, int nst_cap = 0) {
+bool warp_layout(int nb, int L, int gp, int nrhs, int CS, int KG, int KR, WarpPlan& p) {
     const int R = (nb + CS - 1) / CS;
     if (R > 32) return false;
     int Rp = 1;
@@ -1247,7 +1011,7 @@ bool warp_layout(int nb, int L, int gp, int nrhs, int CS, int KG, int KR, WarpPl
     a.chain[0].count = L;
     a.chain[0].dir = 1;
     a.chain[0].mode = 0;
-    a.nchains = 1;
+    a.chain[1].count = 0;
     a.nb = nb;
     a.nrhs = nrhs;
     a.gp = gp;
@@ -1261,12 +1025,12 @@ bool warp_layout(int nb, int L, int gp, int nrhs, int CS, int KG, int KR, WarpPl
     const size_t wb = 0;  // w is formed in registers
     const char* ns = std::getenv("FWI_EXACT_STAGES");
     a.nst = ns ? std::max(2, std::min(kWMaxStages, std::atoi(ns))) : kWMaxStages;
-    if (nst_cap > 0) a.nst = std::min(a.nst, nst_cap);
-    while (a.nst > 2 && size_t(a.nst) * a.stage_bytes + yb + wb + 256 > 220 * 1024) a.nst /= 2;
+    while (a.nst & (a.nst - 1)) --a.nst;  // power of two: the kernel masks the step index
+    while (a.nst > 2 && size_t(a.nst) * a.stage_bytes + yb + wb + 512 > 220 * 1024) a.nst /= 2;
     a.off_y = a.nst * a.stage_bytes;
     a.off_w = a.off_y + yb;
     a.off_bar = a.off_w + wb;
-    p.smem = a.off_bar + 256;  // 3 * kWMaxStages + 2 * NW <= 32 mbarriers
+    p.smem = a.off_bar + 512;
     p.CS = CS;
     p.KG = KG;
     p.KR = KR;
@@ -1311,13 +1075,9 @@ template <int CS, int KG, int KR, bool TRACE, bool EVEN>
 bool warp_launch(const WarpPlan& p, int nrhs, cudaStream_t st) {
     if (!warp_prepare<CS, KG, KR, TRACE, EVEN>(p, nullptr)) return false;
     const int groups = (nrhs + KG - 1) / KG;
-    const int chains = p.a.nchains;
+    const int chains = p.a.chain[1].count > 0 ? 2 : 1;
     WSweepArgs args = p.a;
-    args.groups = groups;
-    {
-        const char* e = std::getenv("FWI_SWEEP_EARLY");  // read per launch (A/B in one process)
-        args.early = pdl_enabled(kPdlExact) && !(e && e[0] == '0') ? 1 : 0;
-    }
+    args.groups0 = groups;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(chains * groups * CS);
     cfg.blockDim = dim3((KG / KR + 1) * 32);
@@ -1390,26 +1150,12 @@ bool warp_plan(int nb, int L, int gp, int nrhs, WarpPlan& best, int chains = 1, 
             int maxc = 0;
             if (!warp_dispatch_prepare(p, &maxc)) continue;
             const int groups = chains * ((nrhs + kg - 1) / kg);
-            // clusters beyond one wave: a 3-stage ring may fit two CTAs per SM
-            // (segmented solves only: for the one- and two-chain plans the 3-stage ring measured slower)
-            if (chains == 4 && groups > maxc && p.a.nst > 3 && !std::getenv("FWI_EXACT_STAGES")) {
-                WarpPlan p3;
-                int maxc3 = 0;
-                if (warp_layout(nb, L, gp, nrhs, cs, kg, kr, p3, 3) && warp_dispatch_prepare(p3, &maxc3) &&
-                    maxc3 > maxc) {
-                    p = p3;
-                    maxc = maxc3;
-                }
-            }
             const int waves = (groups + maxc - 1) / maxc;
             const int ncls = 32 / p.a.Rp;
             const double per_lane = double((nb + ncls - 1) / ncls);
             const int nw = kg / kr;
             p.est = double(waves) * double(steps) *
                     (1400.0 + 35.0 * per_lane * kr + 4.5 * per_lane * kr * std::max(0, nw - 2));
-            if (const char* lg = std::getenv("FWI_EXACT_PLAN_LOG"); lg && std::string(lg) == "2")
-                std::fprintf(stderr, "[fwi]   plan candidate nb=%d chains=%d steps=%d CS=%d KG=%d KR=%d maxc=%d nst=%d est=%.0f\n",
-                             nb, chains, steps, cs, kg, kr, maxc, p.a.nst, p.est);
             if (!found || p.est < best.est - 1e-9) {
                 best = p;
                 found = true;
@@ -1588,43 +1334,6 @@ static void exact_factor_once(Ctx& c, bool line_pivot) {
                          p2.est + 40000.0 < 0.9 * p1.est;
         }
     }
-    // Segmented factorisation: four chains (two of them with spikes) meeting three separator
-    // lines, so a solve's sweep chains are ~L/4 lines long instead of ~L/2 (twisted); costs
-    // three small extra kernels per solve and ~2 nb^2 complex per spike line of storage.
-    // FWI_EXACT_SEGMENTS=1|0 forces it on or off.
-    {
-        const char* es = line_pivot ? nullptr : std::getenv("FWI_EXACT_SEGMENTS");
-        const bool force = es && std::string(es) == "1";
-        if (force && !f->dense) f->dense_factor = true;
-        if (f->dense_factor && !f->dense && !line_pivot && L >= 16 && !(es && std::string(es) == "0")) {
-            const int c4 = (L - 3) / 4, rem = (L - 3) % 4;
-            const int cnt[4] = {c4 + (rem > 0), c4 + (rem > 1), c4 + (rem > 2), c4};
-            // Opt-in: on config 1 (64 lines of 128) the chains halve (sweep launch 38.9 -> 30 us)
-            // but the three separator kernels cost more than that saves (2,883 against 3,043 it/s,
-            // DESIGN.md 3.3), so the model below is only consulted with FWI_EXACT_SEGMENTS=auto.
-            bool want = force;
-            if (!force && es && std::string(es) == "auto") {
-                WarpPlan p2, p4;
-                const int m = L / 2;
-                const int steps2 = 2 * std::max(m, L - 1 - m);
-                const int steps4 = 2 * std::max(std::max(cnt[0], cnt[1]), std::max(cnt[2], cnt[3]));
-                WarpPlan p1;
-                const bool ok1 = warp_plan(nb, L, nb + 1, c.K, p1);
-                const double base = f->twisted ? (warp_plan(nb, L, nb + 1, c.K, p2, 2, steps2) ? p2.est + 40000.0 : -1)
-                                               : (ok1 ? p1.est : -1);
-                want = base > 0 && warp_plan(nb, L, nb + 1, c.K, p4, 4, steps4) && p4.est + 90000.0 < 0.9 * base;
-            }
-            if (want) {
-                f->segmented = true;
-                f->twisted = false;
-                for (int q = 0; q < 4; ++q) f->seg_count[q] = cnt[q];
-                f->sep[0] = cnt[0];
-                f->sep[1] = f->sep[0] + 1 + cnt[1];
-                f->sep[2] = f->sep[1] + 1 + cnt[2];
-                f->cmax = std::max(cnt[1], cnt[2]);
-            }
-        }
-    }
     if (f->dense_factor) {
         const int64_t nn = int64_t(nb) * nb;
         auto Gl = [&](int i) { return f->G.p + i * int64_t(nb) * f->gp; };
@@ -1636,72 +1345,7 @@ static void exact_factor_once(Ctx& c, bool line_pivot) {
             CK_LAUNCH();
             dense_invert(st, nb, Gl(i), f->gp, dw, f->status.p, i * nb);
         };
-        if (f->segmented) {
-            const int s1 = f->sep[0], s2 = f->sep[1], s3 = f->sep[2], cm = f->cmax;
-            const int64_t ldF = int64_t(cm) * nb, n3 = 3 * int64_t(nb);
-            f->Fa.alloc(size_t(2) * nb * ldF);
-            f->FaT.alloc(size_t(2) * cm * nn);
-            f->WaT.alloc(size_t(2) * cm * nn);
-            f->Ssep.alloc(size_t(n3 * n3));
-            f->SinvT.alloc(size_t(n3 * n3));
-            f->seg_tmp.alloc(size_t(nn));
-            f->seg_cnt.alloc(size_t(2) * (nb / 32 + 1));
-            CK(cudaMemsetAsync(f->seg_cnt.p, 0, f->seg_cnt.bytes(), c.stream));
-            CK(cudaMemsetAsync(f->Ssep.p, 0, f->Ssep.bytes(), c.stream));
-            const int nbk = int((nn + 255) / 256);
-            auto Sblk = [&](int r, int q) { return f->Ssep.p + int64_t(r) * nb * n3 + int64_t(q) * nb; };
-            auto schur = [&](int i, const double2* cA, const double2* GA, const double2* cB, const double2* GB) {
-                form_schur<<<nbk, 256, 0, c.stream>>>(f->col_lines, c.nx, nb, i, c.diag.p, c.east.p, c.south.p, cA,
-                                                      GA, cB, GB, f->gp, Gl(i));
-                CK_LAUNCH();
-            };
-            // one chain: lines first, first + dir, ... (count of them), eliminated in order;
-            // spike >= 0: the chain starts next to separator block ssep (whose diagonal block,
-            // in G(sep line), takes -Fa_q G_q Fa_q^T per line) and ends next to block fsep
-            auto chain = [&](int first, int count, int dir, int spike, int ssep, int fsep) {
-                for (int q = 0; q < count; ++q) {
-                    const int i = first + dir * q, prev = i - dir;
-                    line(c.stream, f->dwork, i, q > 0 ? cl(std::min(i, prev)) : nullptr, q > 0 ? Gl(prev) : nullptr,
-                         nullptr, nullptr);
-                    if (spike < 0) continue;
-                    double2* Fq = f->Fa.p + int64_t(spike) * nb * ldF + int64_t(q) * nb;
-                    if (q == 0) {
-                        diag_block<<<nbk, 256, 0, c.stream>>>(nb, cl(std::min(i, prev)), Fq, ldF);
-                        CK_LAUNCH();
-                    }
-                    const int64_t slot = (int64_t(spike) * cm + q) * nn;
-                    transpose_block<<<nbk, 256, 0, c.stream>>>(nb, Fq, ldF, f->FaT.p + slot, nb);
-                    CK_LAUNCH();
-                    // WaT_q = Fa_q G_q^T (= (G_q Fa_q^T)^T); D_sep -= Fa_q WaT_q^T
-                    cgemm(c.stream, true, nb, nb, nb, 1.0, Fq, ldF, Gl(i), f->gp, nullptr, 0, f->WaT.p + slot, nb);
-                    const int sl = f->sep[ssep];
-                    cgemm(c.stream, true, nb, nb, nb, -1.0, Fq, ldF, f->WaT.p + slot, nb, Gl(sl), f->gp, Gl(sl), f->gp);
-                    cgemm(c.stream, false, nb, nb, nb, 1.0, Fq, ldF, Gl(i), f->gp, nullptr, 0, f->seg_tmp.p, nb);
-                    const double2* e = cl(std::min(i, i + dir));  // line i to the next line (or the far separator)
-                    if (q + 1 < count)
-                        spike_next<<<nbk, 256, 0, c.stream>>>(nb, f->seg_tmp.p, e, Fq + nb, ldF, nullptr, 0);
-                    else
-                        spike_next<<<nbk, 256, 0, c.stream>>>(nb, f->seg_tmp.p, e, Sblk(ssep, fsep), n3,
-                                                               Sblk(fsep, ssep), n3);
-                    CK_LAUNCH();
-                }
-            };
-            const bool e0 = f->seg_count[0] > 0, e3 = f->seg_count[3] > 0;
-            chain(0, f->seg_count[0], 1, -1, 0, 0);
-            chain(L - 1, f->seg_count[3], -1, -1, 0, 0);
-            // the outer separators' Schur complements start from their ordinary chain ends
-            schur(s1, e0 ? cl(s1 - 1) : nullptr, e0 ? Gl(s1 - 1) : nullptr, nullptr, nullptr);
-            schur(s3, e3 ? cl(s3) : nullptr, e3 ? Gl(s3 + 1) : nullptr, nullptr, nullptr);
-            chain(s1 + 1, f->seg_count[1], 1, 0, 0, 1);
-            chain(s3 - 1, f->seg_count[2], -1, 1, 2, 1);
-            schur(s2, cl(s2 - 1), Gl(s2 - 1), cl(s2), Gl(s2 + 1));
-            for (int j = 0; j < 3; ++j)
-                CK(cudaMemcpy2DAsync(Sblk(j, j), n3 * sizeof(double2), Gl(f->sep[j]), f->gp * sizeof(double2),
-                                     nb * sizeof(double2), nb, cudaMemcpyDeviceToDevice, c.stream));
-            dense_invert(c.stream, 3 * nb, f->Ssep.p, n3, f->dwork2, f->status.p, s1 * nb);
-            transpose_block<<<int((n3 * n3 + 255) / 256), 256, 0, c.stream>>>(int(n3), f->Ssep.p, n3, f->SinvT.p, n3);
-            CK_LAUNCH();
-        } else if (!f->twisted) {
+        if (!f->twisted) {
             for (int i = 0; i < L; ++i)
                 line(c.stream, f->dwork, i, i > 0 ? cl(i - 1) : nullptr, i > 0 ? Gl(i - 1) : nullptr, nullptr, nullptr);
         } else {
@@ -1755,8 +1399,8 @@ static void exact_factor_once(Ctx& c, bool line_pivot) {
     CK(cudaMemcpyAsync(&st, f->status.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
     if (std::getenv("FWI_EXACT_PLAN_LOG"))
-        std::fprintf(stderr, "[fwi] exact factor nb=%d L=%d dense=%d twisted=%d segmented=%d bcr=%d: %.3f s\n", nb,
-                     L, int(f->dense), int(f->twisted), int(f->segmented), int(f->bcr != nullptr),
+        std::fprintf(stderr, "[fwi] exact factor nb=%d L=%d dense=%d twisted=%d bcr=%d: %.3f s\n", nb, L,
+                     int(f->dense), int(f->twisted), int(f->bcr != nullptr),
                      std::chrono::duration<double>(std::chrono::steady_clock::now() - t_host0).count());
     if (st != 0) {
         // status = line * nb + (position in the line) + 1. Reported as the grid node, the
@@ -1909,13 +1553,10 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
         static std::mutex mu;
         static std::vector<std::pair<std::array<int, 4>, WarpPlan>> cache;
         const bool forced = std::getenv("FWI_EXACT_CS") || std::getenv("FWI_EXACT_KG") || std::getenv("FWI_EXACT_KR");
-        const std::array<int, 4> key{f.nb, f.L, nrhs, f.segmented ? 2 : f.twisted ? 1 : 0};
+        const std::array<int, 4> key{f.nb, f.L, nrhs, f.twisted ? 1 : 0};
         const int m = f.mid;
-        const int chains = f.segmented ? 4 : f.twisted ? 2 : 1;
-        const int steps = f.segmented ? 2 * std::max(std::max(f.seg_count[0], f.seg_count[1]),
-                                                     std::max(f.seg_count[2], f.seg_count[3]))
-                          : f.twisted ? 2 * std::max(m, f.L - 1 - m)
-                                      : 2 * f.L - 1;
+        const int chains = f.twisted ? 2 : 1;
+        const int steps = f.twisted ? 2 * std::max(m, f.L - 1 - m) : 2 * f.L - 1;
         bool have = false;
         WarpPlan plan;
         {
@@ -1947,82 +1588,11 @@ void exact_solve_batch(Ctx& c, bool adjoint, const double2* b, double2* x, int n
                 CK(cudaMemsetAsync(tbuf.p, 0, tbuf.count * 8, c.stream));
                 p.a.trace = tbuf.p;
             }
-            if (f.segmented) {
-                ExactFactor& fm = const_cast<ExactFactor&>(f);
-                const int s1 = f.sep[0], s2 = f.sep[1], s3 = f.sep[2];
-                const int* cnt = f.seg_count;
-                const int64_t blk = int64_t(nrhs) * f.nb;
-                if (fm.Ts.count < size_t(3) * blk) fm.Ts.alloc(size_t(3) * blk);
-                if (fm.Pq.count < size_t(2) * f.cmax * blk) fm.Pq.alloc(size_t(2) * f.cmax * blk);
-                if (fm.Xs.count < size_t(3) * blk) fm.Xs.alloc(size_t(3) * blk);
-                // (1) the four chains forward: y for every non-separator line
-                p.a.trace = nullptr;
-                p.a.nchains = 4;
-                p.a.chain[0] = SweepChain{0, cnt[0], 1, 1, nullptr};
-                p.a.chain[1] = SweepChain{s1 + 1, cnt[1], 1, 1, nullptr};
-                p.a.chain[2] = SweepChain{s3 - 1, cnt[2], -1, 1, nullptr};
-                p.a.chain[3] = SweepChain{f.L - 1, cnt[3], -1, 1, nullptr};
-                done = warp_dispatch_launch(p, nrhs, c.stream);
-                if (done) {
-                    SegSolveArgs sa{};
-                    sa.nb = f.nb;
-                    sa.nrhs = nrhs;
-                    sa.cmax = f.cmax;
-                    sa.sep[0] = s1;
-                    sa.sep[1] = s2;
-                    sa.sep[2] = s3;
-                    sa.sfirst[0] = s1 + 1;
-                    sa.sdir[0] = 1;
-                    sa.scount[0] = cnt[1];
-                    sa.ssep[0] = 0;
-                    sa.sfirst[1] = s3 - 1;
-                    sa.sdir[1] = -1;
-                    sa.scount[1] = cnt[2];
-                    sa.ssep[1] = 2;
-                    sa.nend[0] = cnt[0] > 0 ? 1 : 0;  // seg 0 ends at s1 - 1
-                    sa.eline[0][0] = s1 - 1;
-                    sa.ecoup[0][0] = s1 - 1;
-                    sa.nend[1] = 2;  // seg 1 ends at s2 - 1, seg 2 at s2 + 1
-                    sa.eline[1][0] = s2 - 1;
-                    sa.ecoup[1][0] = s2 - 1;
-                    sa.eline[1][1] = s2 + 1;
-                    sa.ecoup[1][1] = s2;
-                    sa.nend[2] = cnt[3] > 0 ? 1 : 0;  // seg 3 ends at s3 + 1
-                    sa.eline[2][0] = s3 + 1;
-                    sa.ecoup[2][0] = s3;
-                    sa.FaT = f.FaT.p;
-                    sa.WaT = f.WaT.p;
-                    sa.SinvT = f.SinvT.p;
-                    sa.Pq = fm.Pq.p;
-                    sa.cnt = fm.seg_cnt.p;
-                    sa.coup = f.coup.p;
-                    sa.W = W;
-                    sa.Wout = W;
-                    sa.Y = f.ybuf.p;
-                    sa.Ts = fm.Ts.p;
-                    sa.Xs = fm.Xs.p;
-                    const int rb = (f.nb + 31) / 32;
-                    // (2) the separators' right-hand sides, (3) their dense solve, (4) z on the spike lines
-                    launch_pdl<kPdlExact>(sep_rhs, dim3(rb, std::max(1, f.cmax), 3), dim3(256), 0, c.stream, sa);
-                    CK_LAUNCH();
-                    launch_pdl<kPdlExact>(sep_solve, dim3((3 * f.nb + 7) / 8), dim3(128), 0, c.stream, sa);
-                    CK_LAUNCH();
-                    launch_pdl<kPdlExact>(spike_expand, dim3(rb, std::max(1, f.cmax), 2), dim3(256), 0, c.stream, sa);
-                    CK_LAUNCH();
-                    // (5) the four chains backward, outwards from their separators
-                    p.a.chain[0] = SweepChain{s1 - 1, cnt[0], -1, 2, fm.Xs.p};
-                    p.a.chain[1] = SweepChain{s2 - 1, cnt[1], -1, 2, fm.Xs.p + blk};
-                    p.a.chain[2] = SweepChain{s2 + 1, cnt[2], 1, 2, fm.Xs.p + blk};
-                    p.a.chain[3] = SweepChain{s3 + 1, cnt[3], 1, 2, fm.Xs.p + 2 * blk};
-                    done = warp_dispatch_launch(p, nrhs, c.stream);
-                    if (!done) throw FwiError(FWI_ERR_CUDA, "exact solve: segmented backward sweep could not launch");
-                }
-            } else if (!f.twisted) {
+            if (!f.twisted) {
                 done = warp_dispatch_launch(p, nrhs, c.stream);
             } else {
                 // (1) both halves forward, concurrently: y_i for lines 0..m-1 and L-1..m+1
                 p.a.trace = nullptr;
-                p.a.nchains = 2;
                 p.a.chain[0] = SweepChain{0, m, 1, 1, nullptr};
                 p.a.chain[1] = SweepChain{f.L - 1, f.L - 1 - m, -1, 1, nullptr};
                 done = warp_dispatch_launch(p, nrhs, c.stream);

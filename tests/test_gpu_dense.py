@@ -185,55 +185,6 @@ def test_twisted_factorisation_matches_reference(mk):
     assert rel(got, want) <= 1e-10
 
 
-@pytest.mark.parametrize("mk", [lambda: small_problem(nx=40, nz=26, n_pml=4, K=3, R=5),
-                                lambda: small_problem(nx=22, nz=37, n_pml=3, K=2, R=4, seed=5),
-                                lambda: small_problem(nx=31, nz=23, n_pml=4, K=9, R=7, seed=3),
-                                lambda: small_problem(nx=150, nz=130, n_pml=8, K=3, R=6)])
-def test_segmented_factorisation_matches_reference(mk, monkeypatch):
-    """Four sweep chains meeting three separator lines (two chains carry spikes to their
-    starting separator; the separators' 3nb x 3nb Schur complement is inverted densely).
-    Forced with FWI_EXACT_SEGMENTS=1; solves, adjoint solves and the preconditioner against
-    the reference LU (src/lu.cpp:168-209), 9 right-hand sides crossing the 8-wide chunks."""
-    monkeypatch.setenv("FWI_EXACT_SEGMENTS", "1")
-    p = mk()
-    ref = po.Ref(p, full=False, exact=True)
-    dev = fw.GnState(p, exact=True)
-    assert dev.exact_probe_residual <= 1e-11
-    rng = np.random.default_rng(41)
-    b = rng.standard_normal((2, p.n)) + 1j * rng.standard_normal((2, p.n))
-    for adj in (False, True):
-        for r in range(2):
-            want = ref.solve(b[r], _abi.FWI_PRECOND_EXACT, adj)
-            got = dev.solve(b[r], fw.PrecondMode.exact, adj)
-            assert rel(got, want) <= 1e-10, (adj, rel(got, want))
-    x = random_kkt(p, 4)
-    want = ref.precond_apply(x, _abi.FWI_PRECOND_EXACT)
-    got = fw.precond_apply(dev, fw.KktVector.from_host(dev, x), fw.PrecondMode.exact).to_host()
-    assert rel(got, want) <= 1e-10
-    again = fw.precond_apply(dev, fw.KktVector.from_host(dev, x), fw.PrecondMode.exact).to_host()
-    assert np.array_equal(got, again)  # deterministic (fixed-order reductions)
-
-
-@pytest.mark.parametrize("segments", ["0", "1"])
-def test_segmented_gmres_history_c1(segments, monkeypatch):
-    """C1 exact-preconditioned GMRES with and without the segmented factorisation: 50
-    iterations (restart 30 crossed), per-iteration residuals within 1e-8 of the reference's."""
-    monkeypatch.setenv("FWI_EXACT_SEGMENTS", segments)
-    p = c1_problem()
-    p.d_obs = po.ref_simulate(p)
-    ref = po.Ref(p, full=True, exact=True)
-    q = c1_problem()
-    q.d_obs, q.u, q.r = p.d_obs, ref.u(), ref.residual()
-    dev = fw.GnState(q, exact=True)
-    _, log_r = ref.fsgn(_abi.FWI_PRECOND_EXACT, 30, 0.0, 50, 0)
-    opts = fw.FsgnOptions(mode=fw.PrecondMode.exact, restart=30, tol=0.0, maxit=50, ecg_stride=0)
-    _, log_dev = fw.fsgn_gmres_step(dev, opts)
-    a, b = np.asarray(log_dev.residuals()), np.asarray(log_r.residuals())
-    assert a.shape == b.shape == (51,)
-    dev_rel = np.abs(a - b) / b
-    assert dev_rel.max() <= 1e-8, (dev_rel.max(), dev_rel.argmax())
-
-
 @pytest.mark.parametrize("mode,restart,maxit", [("exact", 1, 12), ("exact", 2, 12), ("exact", 4, 20),
                                                 ("ilu", 3, 30)])
 def test_host_basis_returns_the_device_mode_solution(mode, restart, maxit):
