@@ -15,6 +15,9 @@ struct F64 {
     static __device__ __forceinline__ T sub(T a, T b) { return csub(a, b); }
     static __device__ __forceinline__ T mul(T a, T b) { return cmul(a, b); }
     static __device__ __forceinline__ T mulc(T a, T b) { return cmulc(a, b); }
+    // s + a b and s + conj(a) b: the reference's product, then its sum (no fusing)
+    static __device__ __forceinline__ T madd(T s, T a, T b) { return cadd(s, cmul(a, b)); }
+    static __device__ __forceinline__ T maddc(T s, T a, T b) { return cadd(s, cmulc(a, b)); }
     static __device__ __forceinline__ T rm(R r, T a) { return rmul(r, a); }
     static __device__ __forceinline__ R radd(R a, R b) { return __dadd_rn(a, b); }
     static __device__ __forceinline__ R rmulr(R a, R b) { return __dmul_rn(a, b); }
@@ -41,6 +44,17 @@ struct F32 {
     }
     static __device__ __forceinline__ T mulc(T a, T b) {
         return make_float2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+    }
+    // s + a b and s + conj(a) b as explicit FMA chains: the stencil sums round the same way in
+    // every instantiation (left to the compiler, which product of a pair gets fused depends on the
+    // surrounding code, and kernel variants stop being bit-identical to each other)
+    static __device__ __forceinline__ T madd(T s, T a, T b) {
+        return make_float2(__fmaf_rn(a.x, b.x, __fmaf_rn(-a.y, b.y, s.x)),
+                           __fmaf_rn(a.x, b.y, __fmaf_rn(a.y, b.x, s.y)));
+    }
+    static __device__ __forceinline__ T maddc(T s, T a, T b) {
+        return make_float2(__fmaf_rn(a.x, b.x, __fmaf_rn(a.y, b.y, s.x)),
+                           __fmaf_rn(a.x, b.y, __fmaf_rn(-a.y, b.x, s.y)));
     }
     static __device__ __forceinline__ T rm(R r, T a) { return make_float2(r * a.x, r * a.y); }
     static __device__ __forceinline__ R radd(R a, R b) { return a + b; }

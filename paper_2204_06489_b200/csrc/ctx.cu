@@ -242,6 +242,13 @@ Ctx* ctx_create(const fwi_state_desc& d) {
                 ek[p] = k;
                 ew[p] = c->h_w[j] * c->h_w[j];
             }
+        c->nrec_dup = false;
+        for (int64_t i = 0; i < n && !c->nrec_dup; ++i)
+            for (int q = cnt[i]; q + 1 < cnt[i + 1]; ++q)
+                if (ek[q] == ek[q + 1]) {
+                    c->nrec_dup = true;
+                    break;
+                }
         upload(c->nrec_ptr, cnt.data(), n + 1, st);
         upload(c->nrec_k, ek.data(), ek.size(), st);
         upload(c->nrec_w2, ew.data(), ew.size(), st);

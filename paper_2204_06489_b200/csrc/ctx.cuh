@@ -54,6 +54,7 @@ struct Ctx {
     DevBuf<double> w;
     DevBuf<int> nrec_ptr, nrec_k;  // per-node receiver table
     DevBuf<double> nrec_w2;
+    bool nrec_dup = false;  // some node has two entries of one source (co-located receivers)
     // factorisations
     ExactFactor* exact = nullptr;  // owned (exact_free)
     IluFactor* ilu = nullptr;      // owned (ilu_free)

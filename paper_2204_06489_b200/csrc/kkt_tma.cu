@@ -157,26 +157,27 @@ __device__ __forceinline__ void node_step(const typename A::T* dr, const typenam
                                           typename A::T cN, typename A::T cW, typename A::T cE,
                                           typename A::T cS, typename A::T& s_, typename A::T& t_) {
     using T = typename A::T;
-    s_ = A::zero();
-    t_ = A::zero();
-    if (FULL || hN) {
-        s_ = A::add(s_, A::mul(cN, dr[-RP]));
-        t_ = A::add(t_, A::mulc(cN, lr[-RP]));
-    }
-    if (FULL || hW) {
-        s_ = A::add(s_, A::mul(cW, dr[-1]));
-        t_ = A::add(t_, A::mulc(cW, lr[-1]));
-    }
-    s_ = A::add(s_, A::mul(cD, dr[0]));
-    t_ = A::add(t_, A::mulc(cD, lr[0]));
-    if (FULL || hE) {
-        s_ = A::add(s_, A::mul(cE, dr[1]));
-        t_ = A::add(t_, A::mulc(cE, lr[1]));
-    }
-    if (FULL || hS) {
-        s_ = A::add(s_, A::mul(cS, dr[RP]));
-        t_ = A::add(t_, A::mulc(cS, lr[RP]));
-    }
+    // Warps that touch the Dirichlet ring (FULL = false) run the same straight-line code on
+    // operands selected to +0 where the reference has no stencil entry (the coefficient is +0
+    // there too): 0 * 0 = +0 and a running sum that started at +0 is never -0, so s + (+0) == s
+    // bit for bit, for non-finite inputs as well — identical to skipping the term, without the
+    // four divergent branches (the per-CTA timeline showed the edge strips ending 4 % (complex128)
+    // to 11 % (complex64) after the interior ones).
+    const T z = A::zero();
+    const T dN = (FULL || hN) ? dr[-RP] : z, lN = (FULL || hN) ? lr[-RP] : z;
+    const T dW = (FULL || hW) ? dr[-1] : z, lW = (FULL || hW) ? lr[-1] : z;
+    const T dE = (FULL || hE) ? dr[1] : z, lE = (FULL || hE) ? lr[1] : z;
+    const T dS = (FULL || hS) ? dr[RP] : z, lS = (FULL || hS) ? lr[RP] : z;
+    s_ = A::madd(z, cN, dN);
+    t_ = A::maddc(z, cN, lN);
+    s_ = A::madd(s_, cW, dW);
+    t_ = A::maddc(t_, cW, lW);
+    s_ = A::madd(s_, cD, dr[0]);
+    t_ = A::maddc(t_, cD, lr[0]);
+    s_ = A::madd(s_, cE, dE);
+    t_ = A::maddc(t_, cE, lE);
+    s_ = A::madd(s_, cS, dS);
+    t_ = A::maddc(t_, cS, lS);
     (void)sizeof(T);
 }
 
@@ -647,7 +648,15 @@ struct KmArgs {
     const T* u;                       // u through registers instead of a TMA box (ul = 1)
     int ul;
     int stmode;                       // output store flavour (st_mode)
+    unsigned long long* trace;        // diagnostics (FWI_KKT_KM_TRACE): per CTA start, loop start, loop end, end, smid
+    int rdup;                         // some node holds two receiver entries of one source (Ctx::nrec_dup)
 };
+
+__device__ __forceinline__ unsigned long long km_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 // output store flavours (FWI_KKT_KM_ST): 0 st.global.cs, 1 st.global.L1::no_allocate,
 // 2 st.global (default policy)
@@ -728,6 +737,12 @@ __global__ void __launch_bounds__(THR, 1)
     const CUtensorMap* tla = &M.la[shp];
     const uint32_t hb = P.shb[shp], tx = P.stx[shp], pb = P.spb[shp];
     const int steps = K / KS;
+    if (P.trace && tid == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        P.trace[5 * blockIdx.x] = km_now();
+        P.trace[5 * blockIdx.x + 4] = smid;
+    }
     auto issue = [&](int g) {  // step g: sources [g KS, g KS + KS)
         const int s = g % S;
         unsigned char* st = sm + size_t(s) * P.stage_bytes;
@@ -779,7 +794,24 @@ __global__ void __launch_bounds__(THR, 1)
     for (int kk = 0; kk < KS; ++kk)
 #pragma unroll
         for (int r = 0; r < RPT; ++r) un[kk][r] = act[r] ? ldg_na(P.u + int64_t(kk) * n + cnode[r]) : A::zero();
+    // receiver entries one step ahead (one-band kernel, tables without duplicate (node, source)
+    // entries): the entry at qr[r] sits in registers, so a receiver row's warps do not wait for
+    // two dependent table loads inside every step (the per-CTA timeline showed the receiver
+    // bands ending 15 us after the others at C2)
+    const bool rfast = !P.rdup;
+    int pk[RPT];
+    double pw[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        pk[r] = -1;
+        pw[r] = 0.0;
+        if (rfast && qr[r] < qe[r]) {
+            pk[r] = P.nrec_k[qr[r]];
+            pw[r] = P.nrec_w2[qr[r]];
+        }
+    }
     __syncthreads();
+    if (P.trace && tid == 0) P.trace[5 * blockIdx.x + 1] = km_now();
     for (int g = 0; g < steps; ++g) {
         T ucur[KS][RPT];
 #pragma unroll
@@ -817,7 +849,17 @@ __global__ void __launch_bounds__(THR, 1)
                 if (!act[r]) continue;
                 const int64_t o = int64_t(k) * n + cnode[r];
                 st_mode(P.ola + o, A::sub(s_, A::pmul(P.w2, uc, dsv[r])), kStm);
-                if (qr[r] < qe[r] && P.nrec_k[qr[r]] == k) {
+                if (rfast) {
+                    if (pk[r] == k) {  // at most one entry per (node, source): same sum, 0 + w2 du
+                        t_ = A::add(A::add(A::zero(), A::rm(R(pw[r]), duc)), t_);
+                        ++qr[r];
+                        pk[r] = -1;
+                        if (qr[r] < qe[r]) {
+                            pk[r] = P.nrec_k[qr[r]];
+                            pw[r] = P.nrec_w2[qr[r]];
+                        }
+                    }
+                } else if (qr[r] < qe[r] && P.nrec_k[qr[r]] == k) {
                     T f = A::zero();
                     while (qr[r] < qe[r] && P.nrec_k[qr[r]] == k) {
                         f = A::add(f, A::rm(R(P.nrec_w2[qr[r]]), duc));
@@ -845,9 +887,11 @@ __global__ void __launch_bounds__(THR, 1)
             if (tid == 0 && g + S < steps) issue(g + S);
         }
     }
+    if (P.trace && tid == 0) P.trace[5 * blockIdx.x + 2] = km_now();
 #pragma unroll
     for (int r = 0; r < RPT; ++r)
         if (act[r]) P.ods[cnode[r]] = A::rsub(A::rmulr(P.eps, dsv[r]), pl[r]);
+    if (P.trace && tid == 0) P.trace[5 * blockIdx.x + 3] = km_now();
 }
 template <class A, int COLS, int S, bool MB>
 __global__ void __launch_bounds__(512, 1)
@@ -1015,6 +1059,7 @@ struct KktKmPlan {
     int max_area = 0;  // largest rectangle (nodes): the apply's time follows it (C2, round 2)
     DevBuf<int4> rects;
     DevBuf<unsigned char> rshape;
+    DevBuf<unsigned long long> trace;  // FWI_KKT_KM_TRACE
 };
 
 void kkt_km_plan_free(KktKmPlan* p) { delete p; }
@@ -1364,6 +1409,15 @@ bool launch_km(Ctx& c, KktKmPlan* p, const typename A::T* du, const typename A::
     if (const char* e = std::getenv("FWI_KKT_KM_ST")) a.stmode = std::atoi(e);
     a.u = reinterpret_cast<const typename A::T*>(f32 ? static_cast<const void*>(c.u32.p)
                                                     : static_cast<const void*>(c.u.p));
+    // diagnostics: FWI_KKT_KM_TRACE=<file> writes each launch's per-CTA timeline (globaltimer ns:
+    // start, loop start, loop end, end; SM id), synchronising after the launch — never set in production
+    const char* trace_path = mb ? nullptr : std::getenv("FWI_KKT_KM_TRACE");
+    a.rdup = (c.nrec_dup || std::getenv("FWI_KKT_KM_RDUP")) ? 1 : 0;  // env: force the general loop (tests, A/B)
+    a.trace = nullptr;
+    if (trace_path) {
+        if (!p->trace.p) p->trace.alloc(size_t(5) * p->G);
+        a.trace = p->trace.p;
+    }
 #define FWI_KM_LAUNCH(COLSc, Sc, MBc, WSc, KSc, THRc)                                                      \
     ((MBc ? kkt_km_kernel<A, COLSc, Sc, true><<<p->G, 512, p->smem, c.stream>>>(tdu[0], tla[0], p->tm_u[0],     \
                                                                               tdu[1], tla[1], p->tm_u[1], a)  \
@@ -1375,6 +1429,17 @@ bool launch_km(Ctx& c, KktKmPlan* p, const typename A::T* du, const typename A::
     FWI_KM_DISPATCH(p->cols, p->stages, mb ? 1 : 0, p->ws, p->ks, p->thr, FWI_KM_LAUNCH);
 #undef FWI_KM_LAUNCH
     CK_LAUNCH();
+    if (trace_path) {
+        std::vector<unsigned long long> h(size_t(5) * p->G);
+        CK(cudaStreamSynchronize(c.stream));
+        CK(cudaMemcpy(h.data(), p->trace.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        if (FILE* f = std::fopen(trace_path, "w")) {
+            for (int b = 0; b < p->G; ++b)
+                std::fprintf(f, "%d %llu %llu %llu %llu %llu\n", b, h[5 * b], h[5 * b + 1], h[5 * b + 2], h[5 * b + 3],
+                             h[5 * b + 4]);
+            std::fclose(f);
+        }
+    }
     return true;
 }
 
