@@ -20,3 +20,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -
 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv \
     --log-file gpurun_out/ev/bcr_c3.csv python tools/bcr_prof.py > /dev/null 2>&1
 python tools/krylov_ab.py all > gpurun_out/ev/krylov_ab.log 2>&1
+python tools/k1_timeline.py c128 gpurun_out/ev/k1_timeline_c128.json > gpurun_out/ev/k1_timeline_c128.log 2>&1
+python tools/k1_timeline.py c64 gpurun_out/ev/k1_timeline_c64.json > gpurun_out/ev/k1_timeline_c64.log 2>&1
+FWI_KKT_KM_RDUP=1 python tools/apply_sizes.py c2 > gpurun_out/ev/k1_rdup_ab.log 2>&1
+python tools/apply_sizes.py c2 >> gpurun_out/ev/k1_rdup_ab.log 2>&1
+FWI_KKT_KM_RDUP=1 python tools/apply_sizes.py c2 c64 >> gpurun_out/ev/k1_rdup_ab.log 2>&1
+python tools/apply_sizes.py c2 c64 >> gpurun_out/ev/k1_rdup_ab.log 2>&1
